@@ -1,0 +1,392 @@
+"""Benchmark: BFS + cover-edge triangle count on a seeded synthetic graph.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat24]
+    python bench.py --impl reference ...      # the CPU reference arm
+
+One step = one pass of the hot path over the device-resident graph: min-id
+component roots + multi-source BFS levels -> cover-edge selection ->
+per-cover-edge intersection -> exact 64-bit count (tcb_cetc).  Graph
+construction is outside the timed region, as in the reference's protocol
+(bench.py:1-9 of the reference).  metric = m / t_step (undirected edges/s).
+
+For N > 1 (torchrun, one rank per GPU, NCCL): every rank holds a replica of
+the CSR, labels it, and intersects its 1/N slice of the cover set; the three
+partial tallies are summed with one all-reduce.  Total work
+is fixed as N grows: "scaling": "strong".
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+cuda.synchronize, CUDA events on the launching stream, max over ranks.  The
+RMAT-24 CSR (4.3 GB) is larger than the 126 MB L2, so no flush is needed;
+smaller configs flush L2 between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "edges/s for BFS + cover-edge triangle count; achieved HBM GB/s vs peak"
+UNIT = "edges/s"
+L2_BYTES = 126 * 2**20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="rmat24")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-baseline", default="auto", choices=["auto", "off"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target CPU seconds for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# peaks, clocks
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle = C restatement of the reference; the reference itself
+# is pure Python/numba and is not installed on the GPU box)
+
+
+def cpu_sample(n, row, nb, eu, ev, target_s: float, threads: int):
+    """Time the oracle on a bounded sample of the workload: the full
+    single-threaded BFS (_kernels.py:129-157) plus CETC-SM
+    (_kernels.py:729-755, all threads) over every s-th edge; the full-graph
+    time is t_bfs + s * t_sample.  Returns a dict for "cpu_baseline"."""
+    import oracle
+    m = len(eu)
+    t0 = time.perf_counter()
+    level, _, _, _ = oracle.bfs_levels(row, nb, n)
+    t_bfs = time.perf_counter() - t0
+    # probe ~50k evenly spaced edges, then size the sample to ~target_s
+    stride = max(1, m // 50_000)
+    t0 = time.perf_counter()
+    oracle.cetc_sm_counts(row, nb, level, np.ascontiguousarray(eu[::stride]),
+                          np.ascontiguousarray(ev[::stride]), threads=threads)
+    per_edge = max(time.perf_counter() - t0, 1e-6) / max(1, len(eu[::stride]))
+    budget = max(1.0, target_s - t_bfs)
+    stride = max(1, int(np.ceil(m * per_edge / budget)))
+    sub_u = np.ascontiguousarray(eu[::stride])
+    sub_v = np.ascontiguousarray(ev[::stride])
+    t0 = time.perf_counter()
+    oracle.cetc_sm_counts(row, nb, level, sub_u, sub_v, threads=threads)
+    t_int = time.perf_counter() - t0
+    t_total = t_bfs + t_int * stride
+    return {"value": m / t_total, "unit": UNIT, "cores": threads, "kind": "port",
+            "seconds_full_extrapolated": t_total, "t_bfs_s": t_bfs,
+            "t_intersect_sample_s": t_int,
+            "sample": f"oracle (C restatement of the reference kernels): full BFS on 1 core "
+                      f"+ CETC-SM on {threads} threads over every {stride}th edge "
+                      f"({len(sub_u)} of {m}), extrapolated x{stride}"}
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (the oracle port; see
+    DESIGN.md) on the host cores, same config/metric.  Rank 0 only."""
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return
+    import oracle
+    from paper_2403_02997_b200 import configs as C
+    cfg = C.CONFIGS[args.config]
+    threads = oracle.max_threads()
+    t0 = time.time()
+    if cfg.kind == "rmat":
+        perm = C.id_permutation(cfg.n, cfg.perm_seed)
+        pairs = oracle.rmat_pairs(cfg.scale, cfg.edge_factor, seed=cfg.seed, perm=perm)
+    elif cfg.kind == "er":
+        pairs = C.er_pairs(cfg.n, cfg.p, cfg.seed)
+    else:
+        pairs = C.lattice_pairs(cfg.side)
+    row, nb, eu, ev = oracle.normalize(cfg.n, pairs)
+    del pairs
+    build_s = time.time() - t0
+    per_step = max(5.0, 60.0 / max(1, args.steps + args.warmup))
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        last = cpu_sample(cfg.n, row, nb, eu, ev, per_step, threads)
+        if i >= args.warmup:
+            vals.append(last["value"])
+    value = float(np.mean(vals))
+    ms = len(eu) / value * 1e3
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "m": len(eu),
+                       "host_build_s": round(build_s, 1)},
+            "cpu_baseline": dict(last, value=value),
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_02997_b200 as tb
+    from paper_2403_02997_b200 import configs as C
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    cfg = C.CONFIGS[args.config]
+    t0 = time.time()
+    dg = C.build_device_graph(cfg, device=local)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    ctx = tb._lib.context(local)
+
+    # L2 flush buffer for configs whose working set fits in L2
+    flush = None
+    if dg.nbytes < 4 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def step():
+        if world > 1:
+            r = tb.cetc.cetc_shard(dg, rank, world)
+            t = torch.tensor([r.triangles, r.c1, r.c2], dtype=torch.int64, device=dev)
+            dist.all_reduce(t)
+            return r, t.tolist()
+        r = tb.cetc(dg)
+        return r, [r.triangles, r.c1, r.c2]
+
+    # work statistics from one labeled pass (not timed)
+    full = tb.cetc(dg, keep_level=True, keep_cover=True)
+    deg = (dg.row_offsets[1:] - dg.row_offsets[:-1])
+    du = deg[full.cover_u.long()]
+    dv = deg[full.cover_v.long()]
+    W = int((du + dv).sum().item())
+    W_min = int(torch.minimum(du, dv).sum().item())
+    H = full.c1 + full.c2
+    ncover = full.ncover
+    expect = [full.triangles, full.c1, full.c2]
+    del du, dv, deg, full
+
+    for _ in range(args.warmup):
+        if flush is not None:
+            flush.zero_()
+        _, tot = step()
+        assert tot == expect, (tot, expect)
+
+    ctx.set_timing(True)
+    stage_acc = {k: 0.0 for k in tb._lib.STAGES}
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    launches0 = ctx.launches()
+    step_ms = []
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        _, tot = step()
+        ev1.record()
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        st = ctx.stage_times()
+        for k in stage_acc:
+            stage_acc[k] += st[k]
+        assert tot == expect
+    launches = ctx.launches() - launches0
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ctx.set_timing(False)
+
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    stages = {k: v / args.steps for k, v in stage_acc.items()}
+    value = dg.m / (ms * 1e-3)
+
+    # e2e through the host-buffer C entry (pinned host CSR, uploads inside)
+    e2e = None
+    if world == 1:
+        row_h = torch.empty(dg.n + 1, dtype=torch.int64, pin_memory=True)
+        nb_h = torch.empty(2 * dg.m, dtype=torch.int32, pin_memory=True)
+        row_h.copy_(dg.row_offsets)
+        nb_h.copy_(dg.neighbors)
+        row_np, nb_np = row_h.numpy(), nb_h.numpy()
+        for _ in range(max(1, args.warmup)):
+            tb.cetc_host(row_np, nb_np, dg.n, device=local)
+        torch.cuda.synchronize()
+        t_e2e = []
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = tb.cetc_host(row_np, nb_np, dg.n, device=local)
+            t_e2e.append(time.perf_counter() - t0)
+            assert [r["triangles"], r["c1"], r["c2"]] == expect
+        e2e = {"value": dg.m / float(np.mean(t_e2e)), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * (dg.n + 1) + 4 * 2 * dg.m,
+               "d2h_bytes_per_step": 120,
+               "ms_per_step": float(np.mean(t_e2e)) * 1e3,
+               "path": "tcb_cetc_host (paper_2403_02997_b200.cetc_host): pinned host CSR"}
+        del row_h, nb_h
+
+    peak, peak_kind = hbm_peak()
+    # roofline of the dominant kernel (intersection): SURVEY.md §8(d)
+    # B_int = 4 W + 24 |S| + 4 H algorithmic bytes per launch
+    b_int = 4 * W + 24 * ncover + 4 * H
+    t_int = stages["intersect"] * 1e-3
+    achieved = b_int / t_int / 1e9 if t_int > 0 else None
+    b_bfs = 8 * (dg.n + 1) + 16 * dg.m + 4 * dg.n
+    t_bfs = (stages["components"] + stages["bfs"]) * 1e-3
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(cfg.name, {}).get("intersect_dram_bytes")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": "k_intersect (per-cover-edge intersection)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_kind": peak_kind,
+                "algorithmic_bytes": b_int,
+                "formula": "4*W + 24*|S| + 4*(c1+c2), W = sum_S (d(u)+d(v))",
+                "t_ms": stages["intersect"],
+                "bfs": {"achieved": b_bfs / t_bfs / 1e9 if t_bfs > 0 else None,
+                        "bytes": b_bfs, "t_ms": stages["components"] + stages["bfs"],
+                        "formula": "8(n+1) + 16m + 4n"}}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int32", "data": "synthetic (seeded generator, see DESIGN.md)",
+            "config": {"workload": cfg.name, "n": dg.n, "m": dg.m, "ncover": ncover,
+                       "triangles": expect[0], "W": W, "W_min": W_min,
+                       "parallelism": f"replicated CSR, cover set sharded x{world}",
+                       "l2": ("inputs larger than L2" if flush is None
+                              else "L2 flushed between steps"),
+                       "graph_build_s": round(build_s, 3)},
+            "stages_ms": stages, "clocks": clocks, "gpu_launches": launches,
+            "e2e": e2e, "roofline": roofline}
+
+    if rank == 0 and world == 1 and args.cpu_baseline != "off":
+        import oracle
+        row = dg.row_offsets.cpu().numpy()
+        nb = dg.neighbors.cpu().numpy()
+        eu = dg.edge_u.cpu().numpy()
+        ev = dg.edge_v.cpu().numpy()
+        line["cpu_baseline"] = cpu_sample(dg.n, row, nb, eu, ev, args.cpu_seconds,
+                                          oracle.max_threads())
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

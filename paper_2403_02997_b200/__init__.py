@@ -1,0 +1,36 @@
+"""B200-native cover-edge triangle counting (arXiv 2403.02997).
+
+Drop-in for the reference package ``tricount``'s cover-edge path: the same
+entry points (``normalize``, ``bfs_label``, ``cover_edges``, ``tc_cetc``,
+``tc_cetc_sm``, the ``"CETC-Seq"``/``"CETC-SM"`` registry entries), backed by
+hand-written sm_100a kernels behind the C ABI in include/tricount_b200.h.
+There is no CPU fallback: compute calls raise without the CUDA library/GPU.
+"""
+from .graph import (
+    DeviceGraph,
+    EdgeList,
+    Graph,
+    ParseError,
+    device_graph,
+    load_edge_list,
+    normalize,
+    normalize_device,
+    parse_edge_list,
+    to_edge_list,
+)
+from .rmat import RmatParams, generate_rmat, rmat_pairs_device
+from .bfs import (
+    BfsLabeling,
+    CoverEdgeSet,
+    EdgeClass,
+    bfs_label,
+    cover_edges,
+    enumerate_triangles,
+    verify_cover,
+)
+from .sequential import SEQUENTIAL_IDS, count_sequential, tc_cetc
+from .parallel import PARALLEL_IDS, ParallelConfig, tc_cetc_sm, tc_par
+from .cetc import CetcResult, cetc, cetc_host
+from . import configs
+
+__version__ = "0.1.0"

@@ -1,0 +1,141 @@
+"""Device-level operations of the CETC path over a DeviceGraph.
+
+Thin wrappers over the C ABI (include/tricount_b200.h); each cites the
+reference function it replaces.  Everything runs on the current torch stream
+of the graph's device.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .graph import DeviceGraph
+
+__all__ = [
+    "CetcResult",
+    "bfs_levels",
+    "cover_select",
+    "cetc_count",
+    "cetc",
+    "cetc_shard",
+    "cetc_host",
+]
+
+
+@dataclass(frozen=True)
+class CetcResult:
+    triangles: int
+    c1: int
+    c2: int
+    ncover: int
+    components: int
+    max_level: int
+    level: object = None      # torch int32 [n] on device (when requested)
+    cover_u: object = None    # torch int32 [ncover]
+    cover_v: object = None
+
+
+def bfs_levels(dg: DeviceGraph):
+    """_kernels.py:129-157 bfs_levels_k (levels, components, max_level).
+    Returns (level int32 tensor [n], components, max_level)."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    level = torch.empty(max(dg.n, 1), dtype=torch.int32, device=dg.device)
+    comps = ctypes.c_int64(0)
+    ml = ctypes.c_int64(0)
+    ctx.check(ctx.lib.tcb_bfs_levels(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                     _lib.ptr(dg.edge_u), _lib.ptr(dg.edge_v), dg.n, dg.m,
+                                     _lib.ptr(level), ctypes.byref(comps), ctypes.byref(ml)))
+    return level[: dg.n], int(comps.value), int(ml.value)
+
+
+def cover_select(dg: DeviceGraph, level):
+    """bfs.py:97-106 cover_edges: horizontal u<v edges, lexicographic.
+    Returns (cover_u, cover_v) int32 tensors."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    cu = torch.empty(max(dg.m, 1), dtype=torch.int32, device=dg.device)
+    cv = torch.empty(max(dg.m, 1), dtype=torch.int32, device=dg.device)
+    k = ctypes.c_int64(0)
+    ctx.check(ctx.lib.tcb_cover_select(ctx.h, _lib.ptr(level), _lib.ptr(dg.edge_u),
+                                       _lib.ptr(dg.edge_v), dg.m, _lib.ptr(cu), _lib.ptr(cv),
+                                       ctypes.byref(k)))
+    k = int(k.value)
+    return cu[:k], cv[:k]
+
+
+def cetc_count(dg: DeviceGraph, level, cover_u, cover_v, k0: int = 0, k1: int | None = None):
+    """_kernels.py:729-755 cetc_sm_range_k over cover edges [k0, k1).
+    Returns (t, c1, c2); over the full set t == c1 + c2 // 3."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    if k1 is None:
+        k1 = int(cover_u.numel())
+    out = (ctypes.c_int64 * 3)()
+    level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    ctx.check(ctx.lib.tcb_cetc_count(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                     _lib.ptr(level), dg.n, _lib.ptr(cover_u),
+                                     _lib.ptr(cover_v), k0, k1,
+                                     ctypes.cast(out, ctypes.POINTER(ctypes.c_int64))))
+    return int(out[0]), int(out[1]), int(out[2])
+
+
+def cetc(dg: DeviceGraph, keep_level: bool = False, keep_cover: bool = False) -> CetcResult:
+    """sequential.py:164-168 tc_cetc, fused on the device: CC roots -> BFS
+    levels -> cover selection -> intersection -> exact 64-bit count."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    level = cu = cv = None
+    if keep_level:
+        level = torch.empty(max(dg.n, 1), dtype=torch.int32, device=dg.device)
+    if keep_cover:
+        cu = torch.empty(max(dg.m, 1), dtype=torch.int32, device=dg.device)
+        cv = torch.empty(max(dg.m, 1), dtype=torch.int32, device=dg.device)
+    r = _lib.TcbResult()
+    ctx.check(ctx.lib.tcb_cetc(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                               _lib.ptr(dg.edge_u), _lib.ptr(dg.edge_v), dg.n, dg.m,
+                               _lib.ptr(level), _lib.ptr(cu), _lib.ptr(cv), ctypes.byref(r)))
+    d = r.as_dict()
+    return CetcResult(
+        level=level[: dg.n] if level is not None else None,
+        cover_u=cu[: d["ncover"]] if cu is not None else None,
+        cover_v=cv[: d["ncover"]] if cv is not None else None,
+        **d)
+
+
+def cetc_shard(dg: DeviceGraph, shard: int, nshards: int) -> CetcResult:
+    """One rank's share of the fused path: replicated
+    labeling/selection, intersection over slice `shard` of `nshards`.
+    triangles/c1/c2 are partials; sum them across shards."""
+    ctx = _lib.context(dg.device.index)
+    r = _lib.TcbResult()
+    ctx.check(ctx.lib.tcb_cetc_shard(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                     _lib.ptr(dg.edge_u), _lib.ptr(dg.edge_v), dg.n, dg.m,
+                                     shard, nshards, ctypes.byref(r)))
+    return CetcResult(**r.as_dict())
+
+
+def cetc_host(row_offsets: np.ndarray, neighbors: np.ndarray, n: int,
+              want_level: bool = False, device: int | None = None):
+    """The host-buffer entry (tcb_cetc_host): numpy CSR in, result (and int64
+    levels, BfsLabeling.level's dtype) out; uploads and downloads are inside."""
+    ctx = _lib.context(device)
+    row = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    nb = np.ascontiguousarray(neighbors, dtype=np.int32)
+    if len(row) != n + 1:
+        raise ValueError("row_offsets must have n+1 entries")
+    level = np.empty(max(n, 1), dtype=np.int64) if want_level else None
+    r = _lib.TcbResult()
+    ctx.check(ctx.lib.tcb_cetc_host(
+        ctx.h, row.ctypes.data_as(ctypes.c_void_p),
+        nb.ctypes.data_as(ctypes.c_void_p) if len(nb) else ctypes.c_void_p(0), n,
+        level.ctypes.data_as(ctypes.c_void_p) if level is not None else ctypes.c_void_p(0),
+        ctypes.byref(r)))
+    d = r.as_dict()
+    if level is not None:
+        d["level"] = level[:n]
+    return d

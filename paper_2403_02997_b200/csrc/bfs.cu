@@ -1,0 +1,271 @@
+// bfs.cu — levels of the reference's all-component BFS (_kernels.py:129-157).
+//
+// The reference roots each component at its lowest unvisited id
+// (_kernels.py:137-142), i.e. at the component's minimum vertex id, and
+// levels are BFS distances from that root.  So the levels equal those of ONE
+// multi-source BFS seeded with every component's min-id vertex at level 0:
+//
+//   1. components: union-find over the u<v edges where a larger root is always
+//      hooked under a smaller one (ECL-CC style, lock-free CAS), so each tree's
+//      root is its minimum id; roots give `components` (isolated vertices are
+//      their own roots and sit at level 0).
+//   2. BFS: one cooperative persistent kernel runs every level with a grid-wide
+//      barrier between levels (no host round trip per level — the 2048-level
+//      lattice would otherwise be launch/sync bound).  Direction-optimising:
+//      top-down warp-per-frontier-vertex expansion with CAS claims and
+//      warp-aggregated queue appends; bottom-up over unvisited vertices with
+//      early exit when the frontier's incident edges exceed the unexplored
+//      ones / ALPHA; back to top-down when the frontier shrinks below n / BETA.
+//
+// parent/TREE-vs-STRUT classes depend on the reference's FIFO order and are
+// not produced; levels, components and max_level are exact.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tcb {
+
+// ---------------------------------------------------------------------------
+// connected components with min-id representatives
+
+__device__ __forceinline__ int ld_volatile(const int* p) { return *(volatile const int*)p; }
+
+__device__ __forceinline__ int find_root(int v, int* parent) {
+    int curr = ld_volatile(&parent[v]);
+    if (curr != v) {
+        int prev = v, next;
+        // parents only ever point to smaller ids; path halving on the way up
+        while (curr > (next = ld_volatile(&parent[curr]))) {
+            parent[prev] = next;
+            prev = curr;
+            curr = next;
+        }
+    }
+    return curr;
+}
+
+__global__ void k_cc_init(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
+                          int64_t n, int* __restrict__ parent) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        // rows are sorted: the first neighbour is the smallest one
+        int p = int(v);
+        if (row[v + 1] > row[v]) {
+            int w = nb[row[v]];
+            if (w < p) p = w;
+        }
+        parent[v] = p;
+    }
+}
+
+__global__ void k_cc_hook(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                          int64_t m, int* parent) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
+        int ustat = find_root(eu[e], parent);
+        int vstat = find_root(ev[e], parent);
+        while (ustat != vstat) {
+            // hook the larger root under the smaller one
+            if (ustat < vstat) {
+                int ret = atomicCAS(&parent[vstat], vstat, ustat);
+                if (ret == vstat) break;
+                vstat = find_root(ret, parent);
+            } else {
+                int ret = atomicCAS(&parent[ustat], ustat, vstat);
+                if (ret == ustat) break;
+                ustat = find_root(ret, parent);
+            }
+        }
+    }
+}
+
+// Flatten and seed the BFS: level 0 at roots (comp[v]==v), -1 elsewhere;
+// roots with neighbours form the first frontier.
+__global__ void k_bfs_seed(const int64_t* __restrict__ row, int64_t n, int* parent,
+                           int32_t* __restrict__ level, int32_t* __restrict__ queue,
+                           DevCounters* C) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    unsigned long long roots = 0, deg0 = 0;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+        const int64_t v = base + threadIdx.x;
+        bool is_root = false, seed = false;
+        int64_t deg = 0;
+        if (v < n) {
+            int r = find_root(int(v), parent);
+            parent[v] = r;
+            is_root = (r == int(v));
+            deg = row[v + 1] - row[v];
+            seed = is_root && deg > 0;
+            level[v] = is_root ? 0 : -1;
+        }
+        roots += is_root;
+        unsigned long long slot = warp_append(seed, &C->q_len[0]);
+        if (seed) {
+            queue[slot] = int32_t(v);
+            deg0 += deg;
+        }
+    }
+    roots = warp_sum(roots);
+    deg0 = warp_sum(deg0);
+    if (lane_id() == 0) {
+        if (roots) atomicAdd(&C->components, roots);
+        if (deg0) atomicAdd(&C->deg_sum[0], deg0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cooperative multi-source BFS
+
+constexpr int BFS_BLOCK = 256;
+constexpr int64_t BFS_ALPHA = 14;  // top-down -> bottom-up when m_f > m_u / ALPHA
+constexpr int64_t BFS_BETA = 24;   // bottom-up -> top-down when n_f < n / BETA
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    return *(volatile const unsigned long long*)p;
+}
+
+__global__ void __launch_bounds__(BFS_BLOCK)
+    k_bfs_coop(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
+               int32_t* level, int32_t* qa, int32_t* qb, DevCounters* C, int64_t dir_edges) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t gwarp = gtid >> 5;
+    const int64_t nwarps = gthreads >> 5;
+    const unsigned lane = lane_id();
+
+    int L = 0;
+    int64_t nf = int64_t(ld_volatile_u64(&C->q_len[0]));
+    int64_t mf = int64_t(ld_volatile_u64(&C->deg_sum[0]));
+    int64_t mu = dir_edges - mf;  // directed entries of not-yet-visited vertices
+    bool td = true;
+    int32_t* cur = qa;
+    int32_t* nxt = qb;
+    int max_level = 0;
+
+    while (nf > 0) {
+        const int sn = (L + 1) % 3;
+        unsigned long long my_deg = 0;
+        if (td) {
+            // top-down: warp per frontier vertex, lanes stride its neighbour list
+            for (int64_t i = gwarp; i < nf; i += nwarps) {
+                const int u = cur[i];
+                const int64_t b = row[u], e = row[u + 1];
+                for (int64_t p0 = b; p0 < e; p0 += 32) {
+                    const int64_t p = p0 + lane;
+                    bool claim = false;
+                    int w = 0;
+                    if (p < e) {
+                        w = nb[p];
+                        if (level[w] == -1 && atomicCAS(&level[w], -1, L + 1) == -1) claim = true;
+                    }
+                    unsigned long long slot = warp_append(claim, &C->q_len[sn]);
+                    if (claim) {
+                        nxt[slot] = w;
+                        my_deg += row[w + 1] - row[w];
+                    }
+                }
+            }
+        } else {
+            // bottom-up: every unvisited vertex looks for a parent on level L
+            for (int64_t base = gtid - lane; base < n; base += gthreads) {
+                const int64_t v = base + lane;
+                bool found = false;
+                if (v < n && level[v] == -1) {
+                    const int64_t b = row[v], e = row[v + 1];
+                    for (int64_t p = b; p < e; ++p) {
+                        if (level[nb[p]] == L) {
+                            found = true;
+                            break;
+                        }
+                    }
+                    if (found) {
+                        level[v] = L + 1;
+                        my_deg += e - b;
+                    }
+                }
+                unsigned cnt = __popc(__ballot_sync(0xffffffffu, found));
+                if (lane == 0 && cnt) atomicAdd(&C->q_len[sn], (unsigned long long)cnt);
+            }
+        }
+        my_deg = warp_sum(my_deg);
+        if (lane == 0 && my_deg) atomicAdd(&C->deg_sum[sn], my_deg);
+
+        grid.sync();
+
+        const int64_t nf_next = int64_t(ld_volatile_u64(&C->q_len[sn]));
+        const int64_t mf_next = int64_t(ld_volatile_u64(&C->deg_sum[sn]));
+        if (gtid == 0) {  // slot (L+2)%3 is next written at step L+2 (after another sync)
+            C->q_len[(L + 2) % 3] = 0;
+            C->deg_sum[(L + 2) % 3] = 0;
+        }
+        if (nf_next > 0) max_level = L + 1;
+        mu -= mf_next;
+        bool next_td;
+        if (td)
+            next_td = !(mf_next > mu / BFS_ALPHA);
+        else
+            next_td = (nf_next < n / BFS_BETA) && (nf_next < nf);
+
+        if (nf_next > 0 && next_td && !td) {
+            // materialise the level-(L+1) frontier as a queue for top-down
+            unsigned long long* qc = &C->scratch[4];
+            for (int64_t base = gtid - lane; base < n; base += gthreads) {
+                const int64_t v = base + lane;
+                bool in = v < n && level[v] == L + 1;
+                unsigned long long slot = warp_append(in, qc);
+                if (in) nxt[slot] = int32_t(v);
+            }
+            grid.sync();
+            if (gtid == 0) *qc = 0;  // nobody reads it; next use is >= 1 sync away
+        }
+        if (td || next_td) {
+            int32_t* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+        td = next_td;
+        nf = nf_next;
+        ++L;
+    }
+    if (gtid == 0) C->max_level = max_level;
+}
+
+// ---------------------------------------------------------------------------
+
+void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* eu,
+                const int32_t* ev, int64_t n, int64_t m, int32_t* level, bool reset_counters) {
+    require(n < (int64_t(1) << 31), "vertex ids must fit int32");
+    DevCounters* C = ctx->d_counters;
+    if (reset_counters) TCB_CUDA(cudaMemsetAsync(C, 0, sizeof(DevCounters), ctx->stream));
+    if (n == 0) return;
+    int* parent = ctx->wsT<int>(WS_COMP, n);
+    ctx->record(0);
+    TCB_LAUNCH(ctx, k_cc_init, grid_for(ctx, n, 256), 256, 0, row, nb, n, parent);
+    if (m > 0)
+        TCB_LAUNCH(ctx, k_cc_hook, grid_for(ctx, m, 256), 256, 0, eu, ev, m, parent);
+    int32_t* qa = ctx->wsT<int32_t>(WS_QUEUE_A, n);
+    int32_t* qb = ctx->wsT<int32_t>(WS_QUEUE_B, n);
+    TCB_LAUNCH(ctx, k_bfs_seed, grid_for(ctx, n, 256), 256, 0, row, n, parent, level, qa, C);
+    ctx->record(1);
+    if (m > 0) {
+        if (ctx->bfs_coop_blocks == 0) {
+            int per_sm = 0;
+            TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_coop,
+                                                                   BFS_BLOCK, 0));
+            require(per_sm > 0, "BFS kernel cannot be co-resident");
+            ctx->bfs_coop_blocks = per_sm * ctx->num_sms;
+        }
+        int64_t dir_edges = 2 * m;
+        void* args[] = {(void*)&row, (void*)&nb, (void*)&n, (void*)&level,
+                        (void*)&qa,  (void*)&qb, (void*)&C, (void*)&dir_edges};
+        TCB_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_coop, dim3(ctx->bfs_coop_blocks),
+                                             dim3(BFS_BLOCK), args, 0, ctx->stream));
+        ctx->launches++;
+    }
+    ctx->record(2);
+}
+
+}  // namespace tcb

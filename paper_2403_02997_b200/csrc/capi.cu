@@ -1,0 +1,324 @@
+// capi.cu — the C ABI (include/tricount_b200.h) over the sm_100a kernels.
+//
+// Every entry point catches tcb::Error and returns its code; the message is
+// kept on the context (tcb_last_error).  The fused driver tcb_cetc mirrors
+// tc_cetc (sequential.py:164-168): bfs_label -> cover edges -> intersection,
+// all stream-ordered with a single host synchronisation at the end.
+#include <cstring>
+
+#include "common.cuh"
+
+struct tcb_context : tcb::Context {};
+
+namespace tcb {
+void csr_build(Context*, const int64_t*, int64_t, int64_t, int64_t*, int32_t*, int32_t*,
+               int32_t*, int64_t*);
+void csr_edges(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*, int32_t*);
+void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, const int32_t*,
+                int64_t, int64_t, int32_t*, bool);
+void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
+                  int32_t*, int64_t*);
+void cetc_intersect(Context*, const int64_t*, const int32_t*, const int32_t*, const int32_t*,
+                    const int32_t*, const int64_t*, int64_t, int64_t, int, int, int64_t);
+void rmat_generate(Context*, int, int64_t, double, double, double, uint64_t, uint64_t, uint64_t,
+                   uint64_t, const int64_t*, int64_t*);
+
+namespace {
+
+template <typename F>
+int guarded(tcb_context* ctx, F&& f) {
+    if (!ctx) return TCB_ERR_INVALID;
+    try {
+        TCB_CUDA(cudaSetDevice(ctx->device));
+        f();
+        ctx->last_error.clear();
+        return TCB_OK;
+    } catch (const Error& e) {
+        ctx->last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        ctx->last_error = e.what();
+        return TCB_ERR_INTERNAL;
+    }
+}
+
+void sync(Context* ctx) { TCB_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+void fetch_counters(Context* ctx) {
+    TCB_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, sizeof(DevCounters),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+}
+
+void collect_stage_times(Context* ctx, int first_event, int first_stage, int nstages) {
+    if (!ctx->timing) return;
+    sync(ctx);
+    for (int s = 0; s < nstages; ++s) {
+        float ms = 0.f;
+        TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[first_event + s], ctx->ev[first_event + s + 1]));
+        ctx->stage_ms[first_stage + s] = ms;
+    }
+}
+
+// fused path on device-resident arrays; leaves results in ctx->d_counters
+void cetc_device(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* eu,
+                 const int32_t* ev, int64_t n, int64_t m, int32_t* level, int32_t* cu,
+                 int32_t* cv, int shard = 0, int nshards = 1) {
+    TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
+    if (n == 0) return;
+    bfs_levels(ctx, row, nb, eu, ev, n, m, level, false);  // events 0,1,2
+    int64_t* d_ncover = reinterpret_cast<int64_t*>(&ctx->d_counters->ncover);
+    cover_select(ctx, level, eu, ev, m, cu, cv, d_ncover);
+    ctx->record(3);
+    cetc_intersect(ctx, row, nb, level, cu, cv, d_ncover, 0, 0, shard, nshards, m);
+    ctx->record(4);
+}
+
+void fill_result(Context* ctx, tcb_result* out, bool partial = false) {
+    const DevCounters& h = *ctx->h_counters;
+    tcb_result r;
+    r.c1 = int64_t(h.c1);
+    r.c2 = int64_t(h.c2);
+    r.triangles = int64_t(h.t);
+    r.ncover = int64_t(h.ncover);
+    r.components = int64_t(h.components);
+    r.max_level = h.max_level;
+    if (!partial && r.c2 % 3 != 0)  // parallel.py:127-128
+        throw Error(TCB_ERR_ASSERT, "same-level apex tally must be divisible by 3");
+    if (!partial && r.triangles != r.c1 + r.c2 / 3)
+        throw Error(TCB_ERR_ASSERT, "T != c1 + c2/3: tie-break tally inconsistent");
+    if (out) *out = r;
+}
+
+}  // namespace
+}  // namespace tcb
+
+using namespace tcb;
+
+extern "C" {
+
+TCB_API int tcb_version(void) { return TCB_VERSION; }
+
+TCB_API int tcb_context_create(int device, void* stream, tcb_context** out) {
+    if (!out) return TCB_ERR_INVALID;
+    *out = nullptr;
+    tcb_context* ctx = new tcb_context();
+    ctx->device = device;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    int rc = guarded(ctx, [&] {
+        TCB_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+        TCB_CUDA(cudaMalloc(&ctx->d_counters, sizeof(DevCounters)));
+        TCB_CUDA(cudaMallocHost(&ctx->h_counters, sizeof(DevCounters)));
+        std::memset(ctx->h_counters, 0, sizeof(DevCounters));
+        for (auto& e : ctx->ev) TCB_CUDA(cudaEventCreate(&e));
+    });
+    if (rc != TCB_OK) {
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return TCB_OK;
+}
+
+TCB_API int tcb_context_destroy(tcb_context* ctx) {
+    if (!ctx) return TCB_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (int s = 0; s < WS_NSLOTS; ++s)
+        if (ctx->slot_ptr[s]) cudaFree(ctx->slot_ptr[s]);
+    if (ctx->d_counters) cudaFree(ctx->d_counters);
+    if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+    return TCB_OK;
+}
+
+TCB_API int tcb_context_set_stream(tcb_context* ctx, void* stream) {
+    return guarded(ctx, [&] { ctx->stream = static_cast<cudaStream_t>(stream); });
+}
+
+TCB_API const char* tcb_last_error(tcb_context* ctx) {
+    return ctx ? ctx->last_error.c_str() : "null context";
+}
+
+TCB_API int64_t tcb_launch_count(tcb_context* ctx) { return ctx ? int64_t(ctx->launches) : -1; }
+
+TCB_API int tcb_set_timing(tcb_context* ctx, int enabled) {
+    return guarded(ctx, [&] { ctx->timing = enabled != 0; });
+}
+
+TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n) {
+    return guarded(ctx, [&] {
+        require(ms_out != nullptr, "ms_out is null");
+        for (int i = 0; i < n && i < TCB_NSTAGES; ++i) ms_out[i] = ctx->stage_ms[i];
+    });
+}
+
+TCB_API int tcb_rmat_generate(tcb_context* ctx, int scale, int64_t edge_factor, double a,
+                              double b, double c, uint64_t state_hi, uint64_t state_lo,
+                              uint64_t inc_hi, uint64_t inc_lo, const int64_t* d_perm,
+                              int64_t* d_pairs) {
+    return guarded(ctx, [&] {
+        require(d_pairs != nullptr, "d_pairs is null");
+        rmat_generate(ctx, scale, edge_factor, a, b, c, state_hi, state_lo, inc_hi, inc_lo,
+                      d_perm, d_pairs);
+    });
+}
+
+TCB_API int tcb_csr_build(tcb_context* ctx, const int64_t* d_pairs, int64_t k, int64_t n,
+                          int64_t* d_row_offsets, int32_t* d_neighbors, int32_t* d_edge_u,
+                          int32_t* d_edge_v, int64_t* m_out) {
+    return guarded(ctx, [&] {
+        require(d_row_offsets && m_out, "null output");
+        require(k == 0 || (d_pairs && d_neighbors), "null input");
+        csr_build(ctx, d_pairs, k, n, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, m_out);
+    });
+}
+
+TCB_API int tcb_csr_edges(tcb_context* ctx, const int64_t* d_row_offsets,
+                          const int32_t* d_neighbors, int64_t n, int64_t m, int32_t* d_edge_u,
+                          int32_t* d_edge_v) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        csr_edges(ctx, d_row_offsets, d_neighbors, n, m, d_edge_u, d_edge_v);
+    });
+}
+
+TCB_API int tcb_bfs_levels(tcb_context* ctx, const int64_t* d_row_offsets,
+                           const int32_t* d_neighbors, const int32_t* d_edge_u,
+                           const int32_t* d_edge_v, int64_t n, int64_t m, int32_t* d_level,
+                           int64_t* components_out, int64_t* max_level_out) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        require(n == 0 || (d_row_offsets && d_level), "null array");
+        bfs_levels(ctx, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, n, m, d_level, true);
+        fetch_counters(ctx);
+        collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 2);
+        if (components_out) *components_out = int64_t(ctx->h_counters->components);
+        if (max_level_out) *max_level_out = ctx->h_counters->max_level;
+    });
+}
+
+TCB_API int tcb_cover_select(tcb_context* ctx, const int32_t* d_level, const int32_t* d_edge_u,
+                             const int32_t* d_edge_v, int64_t m, int32_t* d_cover_u,
+                             int32_t* d_cover_v, int64_t* ncover_out) {
+    return guarded(ctx, [&] {
+        require(m >= 0, "negative size");
+        int64_t* d_n = reinterpret_cast<int64_t*>(&ctx->d_counters->scratch[2]);
+        cover_select(ctx, d_level, d_edge_u, d_edge_v, m, d_cover_u, d_cover_v, d_n);
+        int64_t k = 0;
+        TCB_CUDA(cudaMemcpyAsync(&k, d_n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        if (ncover_out) *ncover_out = k;
+    });
+}
+
+TCB_API int tcb_cetc_count(tcb_context* ctx, const int64_t* d_row_offsets,
+                           const int32_t* d_neighbors, const int32_t* d_level, int64_t n,
+                           const int32_t* d_cover_u, const int32_t* d_cover_v, int64_t k0,
+                           int64_t k1, int64_t* counts_out) {
+    return guarded(ctx, [&] {
+        require(0 <= k0 && k0 <= k1, "bad cover-edge range");
+        require(counts_out != nullptr, "counts_out is null");
+        (void)n;
+        TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
+        cetc_intersect(ctx, d_row_offsets, d_neighbors, d_level, d_cover_u, d_cover_v, nullptr,
+                       k0, k1, 0, 1, k1);
+        fetch_counters(ctx);
+        counts_out[0] = int64_t(ctx->h_counters->t);
+        counts_out[1] = int64_t(ctx->h_counters->c1);
+        counts_out[2] = int64_t(ctx->h_counters->c2);
+    });
+}
+
+TCB_API int tcb_cetc(tcb_context* ctx, const int64_t* d_row_offsets, const int32_t* d_neighbors,
+                     const int32_t* d_edge_u, const int32_t* d_edge_v, int64_t n, int64_t m,
+                     int32_t* d_level_out, int32_t* d_cover_u, int32_t* d_cover_v,
+                     tcb_result* out) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        int32_t* level = d_level_out ? d_level_out : ctx->wsT<int32_t>(WS_LEVEL, n);
+        int32_t* cu = d_cover_u ? d_cover_u : ctx->wsT<int32_t>(WS_COVER_U, m);
+        int32_t* cv = d_cover_v ? d_cover_v : ctx->wsT<int32_t>(WS_COVER_V, m);
+        cetc_device(ctx, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, n, m, level, cu, cv);
+        fetch_counters(ctx);
+        fill_result(ctx, out);
+        if (n > 0) collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 4);
+    });
+}
+
+TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
+                           const int32_t* d_neighbors, const int32_t* d_edge_u,
+                           const int32_t* d_edge_v, int64_t n, int64_t m, int shard, int nshards,
+                           tcb_result* out) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        require(nshards >= 1 && shard >= 0 && shard < nshards, "bad shard index");
+        int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
+        int32_t* cu = ctx->wsT<int32_t>(WS_COVER_U, m);
+        int32_t* cv = ctx->wsT<int32_t>(WS_COVER_V, m);
+        cetc_device(ctx, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, n, m, level, cu, cv,
+                    shard, nshards);
+        fetch_counters(ctx);
+        fill_result(ctx, out, /*partial=*/nshards > 1);
+        if (n > 0) collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 4);
+    });
+}
+
+__global__ void k_level_to_i64(const int32_t* __restrict__ in, int64_t* __restrict__ out,
+                               int64_t n) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = in[i];
+}
+
+TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
+                          const int32_t* h_neighbors, int64_t n, int64_t* h_level_out,
+                          tcb_result* out) {
+    return guarded(ctx, [&] {
+        require(n >= 0, "negative size");
+        require(h_row_offsets != nullptr, "null row offsets");
+        const int64_t nnz = h_row_offsets[n];
+        require(nnz % 2 == 0, "CSR is not symmetric (odd entry count)");
+        const int64_t m = nnz / 2;
+        if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[8], ctx->stream));
+        int64_t* row = ctx->wsT<int64_t>(WS_ROW, n + 1);
+        int32_t* nb = ctx->wsT<int32_t>(WS_NB, nnz);
+        TCB_CUDA(cudaMemcpyAsync(row, h_row_offsets, sizeof(int64_t) * (n + 1),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        if (nnz)
+            TCB_CUDA(cudaMemcpyAsync(nb, h_neighbors, sizeof(int32_t) * nnz,
+                                     cudaMemcpyHostToDevice, ctx->stream));
+        int32_t* eu = ctx->wsT<int32_t>(WS_EDGE_U, m);
+        int32_t* ev = ctx->wsT<int32_t>(WS_EDGE_V, m);
+        csr_edges(ctx, row, nb, n, m, eu, ev);
+        if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[9], ctx->stream));
+        int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
+        int32_t* cu = ctx->wsT<int32_t>(WS_COVER_U, m);
+        int32_t* cv = ctx->wsT<int32_t>(WS_COVER_V, m);
+        cetc_device(ctx, row, nb, eu, ev, n, m, level, cu, cv);
+        if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[10], ctx->stream));
+        if (h_level_out && n > 0) {
+            int64_t* l64 = ctx->wsT<int64_t>(WS_MISC, n);
+            TCB_LAUNCH(ctx, k_level_to_i64, grid_for(ctx, n, 256), 256, 0, level, l64, n);
+            TCB_CUDA(cudaMemcpyAsync(h_level_out, l64, sizeof(int64_t) * n,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        TCB_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, sizeof(DevCounters),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[11], ctx->stream));
+        sync(ctx);
+        fill_result(ctx, out);
+        if (n > 0) collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 4);
+        if (ctx->timing) {
+            float ms = 0.f;
+            TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]));
+            ctx->stage_ms[TCB_STAGE_H2D] = ms;
+            TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[10], ctx->ev[11]));
+            ctx->stage_ms[TCB_STAGE_D2H] = ms;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+outputs (golden fixtures) and the CPU oracle.  Bit-exact: integer work."""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2403_02997_b200 as tb
+from conftest import SMALL_CASES, SMALL_IDS, config_goldens
+from paper_2403_02997_b200 import configs as C
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib_loaded():
+    tb._lib.load_library()
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=SMALL_IDS)
+def test_normalize_matches_reference(case):
+    g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+    assert g.n == case.n and g.m == case.m
+    assert g.row_offsets.dtype == np.int64 and g.neighbors.dtype == np.int32
+    assert np.array_equal(g.row_offsets, case.row)
+    assert np.array_equal(g.neighbors, case.nb)
+    assert np.array_equal(g.edge_u, case.eu) and np.array_equal(g.edge_v, case.ev)
+    with pytest.raises(ValueError):
+        g.neighbors[:1] = 0  # frozen, as graph.py:99-101
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=SMALL_IDS)
+def test_labels_cover_counts_match_reference(case):
+    g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+    lab = tb.bfs_label(g)
+    assert lab.level.dtype == np.int64
+    assert np.array_equal(lab.level, case.level)
+    assert lab.components == case.components
+    assert lab.max_level == case.max_level
+    cov = tb.cover_edges(lab, g)
+    assert cov.edges.dtype == np.int64 and cov.edges.shape == (len(case.cover), 2)
+    assert np.array_equal(cov.edges, case.cover)
+    assert cov.ratio == case.ratio
+    assert lab.horizontal_count == len(case.cover)
+    assert tb.tc_cetc(g) == case.T
+    assert tb.SEQUENTIAL_IDS["CETC-Seq"](g) == case.T
+    for w in (1, 2, 8):
+        assert tb.tc_cetc_sm(g, tb.ParallelConfig(workers=w)) == case.T
+    assert tb.parallel._cetc_sm_counts(g, tb.ParallelConfig(workers=2)) == (case.c1, case.c2)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=SMALL_IDS)
+def test_host_buffer_entry(case):
+    r = tb.cetc_host(case.row, case.nb, case.n, want_level=True)
+    assert (r["triangles"], r["c1"], r["c2"]) == (case.T, case.c1, case.c2)
+    assert r["ncover"] == len(case.cover)
+    assert r["components"] == case.components and r["max_level"] == case.max_level
+    assert np.array_equal(r["level"], case.level)
+
+
+def test_cetc_count_ranges_sum():
+    case = next(c for c in SMALL_CASES if c.name == "rmat10_42")
+    dg = tb.device_graph(tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs)))
+    level, _, _ = tb.cetc.bfs_levels(dg)
+    cu, cv = tb.cetc.cover_select(dg, level)
+    k = cu.numel()
+    parts = [tb.cetc.cetc_count(dg, level, cu, cv, a, b)
+             for a, b in tb.ParallelConfig(workers=3).ranges(k)]
+    assert sum(p[1] for p in parts) == case.c1
+    assert sum(p[2] for p in parts) == case.c2
+    assert sum(p[0] for p in parts) == case.T
+
+
+@pytest.mark.parametrize("scale,ef,seed", [(4, 8, 4), (10, 16, 42), (14, 16, 3), (16, 16, 1)])
+def test_device_rmat_matches_oracle(scale, ef, seed):
+    got = tb.generate_rmat(tb.RmatParams(scale=scale, edge_factor=ef, seed=seed)).edges
+    assert np.array_equal(got, oracle.rmat_pairs(scale, ef, seed=seed))
+
+
+def test_device_rmat_matches_reference_fixture():
+    case = next(c for c in SMALL_CASES if c.name == "rmat10_42")
+    got = tb.generate_rmat(tb.RmatParams(scale=10, edge_factor=16, seed=42)).edges
+    assert np.array_equal(got, case.pairs)
+
+
+def test_csr_with_loops_and_duplicates_random():
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 7, 100, 5000):
+        pairs = rng.integers(0, n, size=(3 * n + 5, 2))
+        g = tb.normalize(tb.EdgeList(n=n, edges=pairs))
+        row, nb, eu, ev = oracle.normalize(n, pairs)
+        assert np.array_equal(g.row_offsets, row) and np.array_equal(g.neighbors, nb)
+        assert np.array_equal(g.edge_u, eu) and np.array_equal(g.edge_v, ev)
+
+
+def _check_config(name):
+    import torch
+    gold = config_goldens()[name]
+    dg = C.build_device_graph(name)
+    assert dg.m == gold["m"]
+    assert sha(dg.row_offsets.cpu().numpy()) == gold["row_offsets_sha"]
+    assert sha(dg.neighbors.cpu().numpy()) == gold["neighbors_sha"]
+    r = tb.cetc(dg, keep_level=True, keep_cover=True)
+    assert (r.triangles, r.c1, r.c2) == (gold["T"], gold["c1"], gold["c2"])
+    assert r.components == gold["components"] and r.max_level == gold["max_level"]
+    assert r.ncover == gold["cover_count"]
+    assert sha(r.level.cpu().numpy()) == gold["level_sha"]
+    cover = torch.stack([r.cover_u, r.cover_v], dim=1).cpu().numpy()
+    assert sha(cover) == gold["cover_sha"]
+    hist = np.bincount(r.level.cpu().numpy(), minlength=len(gold["level_hist"]))
+    assert hist.tolist() == gold["level_hist"]
+
+
+@pytest.mark.parametrize("name", ["er4096", "rmat16", "lattice2048"])
+def test_config_parity(name):
+    _check_config(name)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["rmat22", "rmat24"])
+def test_config_parity_large(name):
+    if name not in config_goldens():
+        pytest.skip(f"no golden for {name}")
+    _check_config(name)
