@@ -247,7 +247,7 @@ def main():
 
     def step():
         if world > 1:
-            r = tb.cetc.cetc_shard(dg, rank, world)
+            r = tb.ops.cetc_shard(dg, rank, world)
             t = torch.tensor([r.triangles, r.c1, r.c2], dtype=torch.int64, device=dev)
             dist.all_reduce(t)
             return r, t.tolist()

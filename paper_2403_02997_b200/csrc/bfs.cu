@@ -147,6 +147,12 @@ __global__ void __launch_bounds__(BFS_BLOCK)
 
     while (nf > 0) {
         const int sn = (L + 1) % 3;
+        // Slot (L+2)%3 is written by step L+1 (after the next barrier) and was
+        // last read right after barrier L-2, so clear it during this step.
+        if (gtid == 0) {
+            C->q_len[(L + 2) % 3] = 0;
+            C->deg_sum[(L + 2) % 3] = 0;
+        }
         unsigned long long my_deg = 0;
         if (td) {
             // top-down: warp per frontier vertex, lanes stride its neighbour list
@@ -197,10 +203,6 @@ __global__ void __launch_bounds__(BFS_BLOCK)
 
         const int64_t nf_next = int64_t(ld_volatile_u64(&C->q_len[sn]));
         const int64_t mf_next = int64_t(ld_volatile_u64(&C->deg_sum[sn]));
-        if (gtid == 0) {  // slot (L+2)%3 is next written at step L+2 (after another sync)
-            C->q_len[(L + 2) % 3] = 0;
-            C->deg_sum[(L + 2) % 3] = 0;
-        }
         if (nf_next > 0) max_level = L + 1;
         mu -= mf_next;
         bool next_td;

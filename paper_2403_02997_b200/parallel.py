@@ -13,7 +13,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from . import cetc as _ops
+from . import ops as _ops
 from .graph import Graph, device_graph
 
 __all__ = ["ParallelConfig", "PARALLEL_IDS", "tc_cetc_sm", "tc_par"]

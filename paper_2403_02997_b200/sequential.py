@@ -8,7 +8,7 @@ path (``tcb_cetc``).
 """
 from __future__ import annotations
 
-from . import cetc as _ops
+from . import ops as _ops
 from .graph import Graph, device_graph
 
 __all__ = ["SEQUENTIAL_IDS", "tc_cetc", "count_sequential"]

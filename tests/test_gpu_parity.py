@@ -68,10 +68,10 @@ def test_host_buffer_entry(case):
 def test_cetc_count_ranges_sum():
     case = next(c for c in SMALL_CASES if c.name == "rmat10_42")
     dg = tb.device_graph(tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs)))
-    level, _, _ = tb.cetc.bfs_levels(dg)
-    cu, cv = tb.cetc.cover_select(dg, level)
+    level, _, _ = tb.ops.bfs_levels(dg)
+    cu, cv = tb.ops.cover_select(dg, level)
     k = cu.numel()
-    parts = [tb.cetc.cetc_count(dg, level, cu, cv, a, b)
+    parts = [tb.ops.cetc_count(dg, level, cu, cv, a, b)
              for a, b in tb.ParallelConfig(workers=3).ranges(k)]
     assert sum(p[1] for p in parts) == case.c1
     assert sum(p[2] for p in parts) == case.c2
