@@ -9,6 +9,10 @@
  *  - d_* arguments are device pointers (caller owned), h_* host pointers.
  *    Inputs are read-only.  Vertex ids are int32, CSR offsets int64 — the
  *    reference Graph's layout (graph.py:57-92, graph.py:95-96).
+ *  - The device graph is the CSR (row_offsets int64[n+1], neighbors
+ *    int32[2m], strictly increasing rows) plus src int32[2m], the row id of
+ *    every entry (COO rows; the same footprint as the reference Graph's
+ *    edge_u/edge_v pair, which are the src<neighbors entries in order).
  *  - All device work is ordered on the context's stream.  Functions that
  *    return a host-side count (m, ncover, components, counts) synchronise
  *    that stream before returning.
@@ -17,9 +21,9 @@
  *    concurrent calls on one Graph — _kernels.py:1-8 — and so is this ABI
  *    with one context per caller).
  *
- * Reference interface each entry point replaces is cited as
- * file:line of /root/reference/pkg/src/tricount/ (the numba kernels'
- * signatures are listed in SURVEY.md §8(b)).
+ * The reference interface each entry point replaces is cited as
+ * file:line of the reference package (pkg/src/tricount/); the numba
+ * kernels' signatures are listed in SURVEY.md §8(b).
  */
 #ifndef TRICOUNT_B200_H
 #define TRICOUNT_B200_H
@@ -33,7 +37,7 @@ extern "C" {
 
 #define TCB_API __attribute__((visibility("default")))
 
-#define TCB_VERSION 1
+#define TCB_VERSION 2
 
 enum {
     TCB_OK = 0,
@@ -46,12 +50,12 @@ enum {
 
 /* Stage indices for tcb_stage_times(). */
 enum {
-    TCB_STAGE_COMPONENTS = 0,  /* min-id component roots (CC)           */
-    TCB_STAGE_BFS = 1,         /* multi-source level-synchronous BFS     */
-    TCB_STAGE_SELECT = 2,      /* horizontal (cover) edge compaction     */
-    TCB_STAGE_INTERSECT = 3,   /* per-cover-edge |N(u) ∩ N(v)| + dedup   */
-    TCB_STAGE_H2D = 4,         /* host-buffer entry: uploads             */
-    TCB_STAGE_D2H = 5,         /* host-buffer entry: downloads           */
+    TCB_STAGE_COMPONENTS = 0,  /* min-id component roots (CC)                 */
+    TCB_STAGE_BFS = 1,         /* multi-source level-synchronous BFS           */
+    TCB_STAGE_SELECT = 2,      /* horizontal (cover) edge selection            */
+    TCB_STAGE_INTERSECT = 3,   /* per-cover-edge |N(u) ∩ N(v)| + level dedup   */
+    TCB_STAGE_H2D = 4,         /* host-buffer entry: uploads + row expansion   */
+    TCB_STAGE_D2H = 5,         /* host-buffer entry: downloads                 */
     TCB_NSTAGES = 6
 };
 
@@ -78,15 +82,16 @@ TCB_API const char* tcb_last_error(tcb_context* ctx);
 /* Count of kernels this context launched so far. */
 TCB_API int64_t tcb_launch_count(tcb_context* ctx);
 /* Enable per-stage CUDA-event timing; tcb_stage_times fills ms[TCB_NSTAGES]
- * for the last tcb_cetc / tcb_cetc_host call (synchronises). */
+ * for the last fused call (tcb_cetc / tcb_cetc_shard / tcb_cetc_host). */
 TCB_API int tcb_set_timing(tcb_context* ctx, int enabled);
 TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n);
 
-/* ---- input synthesis (rmat.py:45-72; configs in DESIGN.md) ------------ */
-/* generate_rmat (rmat.py:45-72): edge_factor*2^scale pairs into
- * d_pairs[2*total] (u,v interleaved int64), drawing from the PCG64 stream
- * whose 128-bit (state, inc) numpy.random.default_rng(seed) starts with.
- * d_perm (nullable, int64[2^scale]) relabels both endpoints. */
+/* ---- input synthesis (rmat.py:45-72) ---------------------------------- */
+/* generate_rmat: edge_factor*2^scale pairs into d_pairs[2*total] (u,v
+ * interleaved int64), drawing from the PCG64 stream whose 128-bit
+ * (state, inc) numpy.random.default_rng(seed) starts with (bit-identical to
+ * the reference's pairs).  d_perm (nullable, int64[2^scale]) relabels both
+ * endpoints: new = perm[old]. */
 TCB_API int tcb_rmat_generate(tcb_context* ctx, int scale, int64_t edge_factor,
                               double a, double b, double c,
                               uint64_t state_hi, uint64_t state_lo,
@@ -97,12 +102,17 @@ TCB_API int tcb_rmat_generate(tcb_context* ctx, int scale, int64_t edge_factor,
  *      graph.py:104-125 _graph_from_canonical_pairs) ------------------ */
 /* Drops self-loops, dedups, symmetrises, sorts adjacency lists.
  * d_pairs: int64[2k] interleaved (u,v), ids in [0,n).
- * d_row_offsets: int64[n+1]; d_neighbors: capacity 2k int32.
+ * d_row_offsets: int64[n+1]; d_neighbors and d_src (nullable): capacity 2k.
  * d_edge_u/d_edge_v (nullable): capacity k int32, the u<v pairs in
  * lexicographic order (Graph.edge_u/edge_v).  *m_out = undirected edges. */
 TCB_API int tcb_csr_build(tcb_context* ctx, const int64_t* d_pairs, int64_t k,
                           int64_t n, int64_t* d_row_offsets, int32_t* d_neighbors,
-                          int32_t* d_edge_u, int32_t* d_edge_v, int64_t* m_out);
+                          int32_t* d_src, int32_t* d_edge_u, int32_t* d_edge_v,
+                          int64_t* m_out);
+
+/* src (per-entry row id) of a CSR: d_src[row[v]..row[v+1]) = v. */
+TCB_API int tcb_csr_rows(tcb_context* ctx, const int64_t* d_row_offsets, int64_t n,
+                         int32_t* d_src);
 
 /* Graph.edge_u/edge_v from a CSR (load_graph's derivation, graph.py:248-250):
  * the u<v entries of each sorted row, in CSR order. */
@@ -113,25 +123,25 @@ TCB_API int tcb_csr_edges(tcb_context* ctx, const int64_t* d_row_offsets,
 /* ---- BFS levels (_kernels.py:129-157 bfs_levels_k; bfs.py:76-94) ------ */
 /* Levels of a BFS over all components rooted at each component's lowest
  * id (the reference's root rule, _kernels.py:137-142).  d_level int32[n].
- * parent/edge classes are not produced (FIFO-order dependent). */
+ * parent / TREE-vs-STRUT classes are not produced (FIFO-order dependent). */
 TCB_API int tcb_bfs_levels(tcb_context* ctx, const int64_t* d_row_offsets,
-                           const int32_t* d_neighbors, const int32_t* d_edge_u,
-                           const int32_t* d_edge_v, int64_t n, int64_t m,
-                           int32_t* d_level, int64_t* components_out,
-                           int64_t* max_level_out);
+                           const int32_t* d_neighbors, const int32_t* d_src,
+                           int64_t n, int64_t m, int32_t* d_level,
+                           int64_t* components_out, int64_t* max_level_out);
 
 /* ---- cover edges (bfs.py:97-106 cover_edges) -------------------------- */
-/* Horizontal edges level[u]==level[v] of (edge_u, edge_v) in order.
- * d_cover_u/d_cover_v capacity m.  *ncover_out = |S|. */
+/* Horizontal edges (level[u]==level[v], u<v) in the reference's
+ * lexicographic order.  d_cover_u/d_cover_v capacity m.  *ncover_out=|S|. */
 TCB_API int tcb_cover_select(tcb_context* ctx, const int32_t* d_level,
-                             const int32_t* d_edge_u, const int32_t* d_edge_v,
+                             const int32_t* d_src, const int32_t* d_neighbors,
                              int64_t m, int32_t* d_cover_u, int32_t* d_cover_v,
                              int64_t* ncover_out);
 
-/* ---- intersection (_kernels.py:669-695 cetc_count_k,
- *      _kernels.py:729-755 cetc_sm_range_k) ---------------------------- */
-/* Over cover edges [k0, k1): counts_out[0]=T part (c1 + same-level apexes
- * w > v), [1]=c1, [2]=c2.  For k0=0,k1=ncover: T = c1 + c2/3. */
+/* ---- intersection over an explicit cover list (_kernels.py:729-755
+ *      cetc_sm_range_k over edge chunks, parallel.py:53-70) ------------ */
+/* Over cover edges [k0, k1) of (d_cover_u, d_cover_v), u < v:
+ * counts_out[0] = T partial (c1 + same-level apexes w > v), [1] = c1,
+ * [2] = c2.  Over the full set T = c1 + c2/3. */
 TCB_API int tcb_cetc_count(tcb_context* ctx, const int64_t* d_row_offsets,
                            const int32_t* d_neighbors, const int32_t* d_level,
                            int64_t n, const int32_t* d_cover_u,
@@ -141,28 +151,27 @@ TCB_API int tcb_cetc_count(tcb_context* ctx, const int64_t* d_row_offsets,
 /* ---- fused path (sequential.py:164-168 tc_cetc) ----------------------- */
 /* Device-resident graph in, exact count out.  d_level_out (nullable,
  * int32[n]) receives the levels; d_cover_u/v (nullable, capacity m) the
- * cover set. */
+ * cover set in the reference's order. */
 TCB_API int tcb_cetc(tcb_context* ctx, const int64_t* d_row_offsets,
-                     const int32_t* d_neighbors, const int32_t* d_edge_u,
-                     const int32_t* d_edge_v, int64_t n, int64_t m,
-                     int32_t* d_level_out, int32_t* d_cover_u, int32_t* d_cover_v,
-                     tcb_result* out);
+                     const int32_t* d_neighbors, const int32_t* d_src,
+                     int64_t n, int64_t m, int32_t* d_level_out,
+                     int32_t* d_cover_u, int32_t* d_cover_v, tcb_result* out);
 
 /* Multi-GPU shard of the fused path: full labeling and
- * cover selection on this device's replica, intersection over shard
- * `shard` of `nshards` equal slices of the cover set.  triangles/c1/c2 are
- * this shard's partials (sum them over shards, e.g. one all-reduce);
- * ncover/components/max_level are global. */
+ * selection on this device's replica; intersection for the owners
+ * x with x % nshards == shard.  triangles/c1/c2 are this shard's partials
+ * (sum over shards, e.g. one all-reduce); ncover/components/max_level are
+ * global. */
 TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
-                           const int32_t* d_neighbors, const int32_t* d_edge_u,
-                           const int32_t* d_edge_v, int64_t n, int64_t m, int shard,
-                           int nshards, tcb_result* out);
+                           const int32_t* d_neighbors, const int32_t* d_src,
+                           int64_t n, int64_t m, int shard, int nshards,
+                           tcb_result* out);
 
 /* Host-buffer entry, the call a binding of cetc_count_k's argument list
- * (row, nb, n) makes: uploads the CSR, derives edge arrays, runs the fused
- * path, downloads the result (and levels as int64 when h_level_out != NULL,
- * the dtype of BfsLabeling.level).  h_row_offsets int64[n+1],
- * h_neighbors int32[row[n]]. */
+ * (row, nb, n; _kernels.py:669) makes: uploads the CSR, derives src, runs
+ * the fused path, downloads the result (and levels as int64 when
+ * h_level_out != NULL, BfsLabeling.level's dtype).
+ * h_row_offsets int64[n+1], h_neighbors int32[row[n]]. */
 TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
                           const int32_t* h_neighbors, int64_t n,
                           int64_t* h_level_out, tcb_result* out);

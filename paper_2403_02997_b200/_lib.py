@@ -71,14 +71,15 @@ def load_library(path: Path | None = None):
             "tcb_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), i32], i32),
             "tcb_rmat_generate": ([vp, i32, i64, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, u64, u64, u64, u64, vp, vp], i32),
-            "tcb_csr_build": ([vp, vp, i64, i64, vp, vp, vp, vp, pi64], i32),
+            "tcb_csr_build": ([vp, vp, i64, i64, vp, vp, vp, vp, vp, pi64], i32),
+            "tcb_csr_rows": ([vp, vp, i64, vp], i32),
             "tcb_csr_edges": ([vp, vp, vp, i64, i64, vp, vp], i32),
-            "tcb_bfs_levels": ([vp, vp, vp, vp, vp, i64, i64, vp, pi64, pi64], i32),
+            "tcb_bfs_levels": ([vp, vp, vp, vp, i64, i64, vp, pi64, pi64], i32),
             "tcb_cover_select": ([vp, vp, vp, vp, i64, vp, vp, pi64], i32),
             "tcb_cetc_count": ([vp, vp, vp, vp, i64, vp, vp, i64, i64, pi64], i32),
-            "tcb_cetc": ([vp, vp, vp, vp, vp, i64, i64, vp, vp, vp,
+            "tcb_cetc": ([vp, vp, vp, vp, i64, i64, vp, vp, vp,
                           ctypes.POINTER(TcbResult)], i32),
-            "tcb_cetc_shard": ([vp, vp, vp, vp, vp, i64, i64, i32, i32,
+            "tcb_cetc_shard": ([vp, vp, vp, vp, i64, i64, i32, i32,
                                 ctypes.POINTER(TcbResult)], i32),
             "tcb_cetc_host": ([vp, vp, vp, i64, vp, ctypes.POINTER(TcbResult)], i32),
         }

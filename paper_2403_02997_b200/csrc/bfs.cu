@@ -60,12 +60,15 @@ __global__ void k_cc_init(const int64_t* __restrict__ row, const int32_t* __rest
     }
 }
 
-__global__ void k_cc_hook(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
-                          int64_t m, int* parent) {
+// one hook per undirected edge: the CSR entries (u, v) with u < v
+__global__ void k_cc_hook(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
+                          int64_t nnz, int* parent) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m; e += stride) {
-        int ustat = find_root(eu[e], parent);
-        int vstat = find_root(ev[e], parent);
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
+        const int u = src[e], v = nb[e];
+        if (v < u) continue;
+        int ustat = find_root(u, parent);
+        int vstat = find_root(v, parent);
         while (ustat != vstat) {
             // hook the larger root under the smaller one
             if (ustat < vstat) {
@@ -237,8 +240,8 @@ __global__ void __launch_bounds__(BFS_BLOCK)
 
 // ---------------------------------------------------------------------------
 
-void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* eu,
-                const int32_t* ev, int64_t n, int64_t m, int32_t* level, bool reset_counters) {
+void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
+                int64_t n, int64_t m, int32_t* level, bool reset_counters) {
     require(n < (int64_t(1) << 31), "vertex ids must fit int32");
     DevCounters* C = ctx->d_counters;
     if (reset_counters) TCB_CUDA(cudaMemsetAsync(C, 0, sizeof(DevCounters), ctx->stream));
@@ -247,7 +250,7 @@ void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32
     ctx->record(0);
     TCB_LAUNCH(ctx, k_cc_init, grid_for(ctx, n, 256), 256, 0, row, nb, n, parent);
     if (m > 0)
-        TCB_LAUNCH(ctx, k_cc_hook, grid_for(ctx, m, 256), 256, 0, eu, ev, m, parent);
+        TCB_LAUNCH(ctx, k_cc_hook, grid_for(ctx, 2 * m, 256), 256, 0, src, nb, 2 * m, parent);
     int32_t* qa = ctx->wsT<int32_t>(WS_QUEUE_A, n);
     int32_t* qb = ctx->wsT<int32_t>(WS_QUEUE_B, n);
     TCB_LAUNCH(ctx, k_bfs_seed, grid_for(ctx, n, 256), 256, 0, row, n, parent, level, qa, C);

@@ -1,9 +1,9 @@
 // capi.cu — the C ABI (include/tricount_b200.h) over the sm_100a kernels.
 //
 // Every entry point catches tcb::Error and returns its code; the message is
-// kept on the context (tcb_last_error).  The fused driver tcb_cetc mirrors
-// tc_cetc (sequential.py:164-168): bfs_label -> cover edges -> intersection,
-// all stream-ordered with a single host synchronisation at the end.
+// kept on the context (tcb_last_error).  The fused driver mirrors tc_cetc
+// (sequential.py:164-168): bfs_label -> cover edges -> intersection, all
+// stream-ordered with a single host synchronisation at the end.
 #include <cstring>
 
 #include "common.cuh"
@@ -12,14 +12,17 @@ struct tcb_context : tcb::Context {};
 
 namespace tcb {
 void csr_build(Context*, const int64_t*, int64_t, int64_t, int64_t*, int32_t*, int32_t*,
-               int32_t*, int64_t*);
+               int32_t*, int32_t*, int64_t*);
+void csr_rows(Context*, const int64_t*, int64_t, int32_t*);
 void csr_edges(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*, int32_t*);
-void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, const int32_t*,
-                int64_t, int64_t, int32_t*, bool);
+void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
+                int32_t*, bool);
 void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
                   int32_t*, int64_t*);
 void cetc_intersect(Context*, const int64_t*, const int32_t*, const int32_t*, const int32_t*,
                     const int32_t*, const int64_t*, int64_t, int64_t, int, int, int64_t);
+void cetc_intersect_owner(Context*, const int64_t*, const int32_t*, const int32_t*,
+                          const int32_t*, int64_t, int64_t, int, int);
 void rmat_generate(Context*, int, int64_t, double, double, double, uint64_t, uint64_t, uint64_t,
                    uint64_t, const int64_t*, int64_t*);
 
@@ -50,27 +53,29 @@ void fetch_counters(Context* ctx) {
     sync(ctx);
 }
 
-void collect_stage_times(Context* ctx, int first_event, int first_stage, int nstages) {
+// events 0..4 bracket components, bfs, select, intersect
+void collect_stage_times(Context* ctx) {
     if (!ctx->timing) return;
     sync(ctx);
-    for (int s = 0; s < nstages; ++s) {
+    for (int s = 0; s < 4; ++s) {
         float ms = 0.f;
-        TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[first_event + s], ctx->ev[first_event + s + 1]));
-        ctx->stage_ms[first_stage + s] = ms;
+        TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[s], ctx->ev[s + 1]));
+        ctx->stage_ms[TCB_STAGE_COMPONENTS + s] = ms;
     }
 }
 
 // fused path on device-resident arrays; leaves results in ctx->d_counters
-void cetc_device(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* eu,
-                 const int32_t* ev, int64_t n, int64_t m, int32_t* level, int32_t* cu,
-                 int32_t* cv, int shard = 0, int nshards = 1) {
+void cetc_device(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
+                 int64_t n, int64_t m, int32_t* level, int shard = 0, int nshards = 1) {
     TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
     if (n == 0) return;
-    bfs_levels(ctx, row, nb, eu, ev, n, m, level, false);  // events 0,1,2
-    int64_t* d_ncover = reinterpret_cast<int64_t*>(&ctx->d_counters->ncover);
-    cover_select(ctx, level, eu, ev, m, cu, cv, d_ncover);
-    ctx->record(3);
-    cetc_intersect(ctx, row, nb, level, cu, cv, d_ncover, 0, 0, shard, nshards, m);
+    bfs_levels(ctx, row, nb, src, n, m, level, false);  // events 0, 1, 2
+    if (m == 0) {
+        ctx->record(3);
+        ctx->record(4);
+        return;
+    }
+    cetc_intersect_owner(ctx, row, nb, src, level, n, m, shard, nshards);  // event 3 inside
     ctx->record(4);
 }
 
@@ -88,6 +93,13 @@ void fill_result(Context* ctx, tcb_result* out, bool partial = false) {
     if (!partial && r.triangles != r.c1 + r.c2 / 3)
         throw Error(TCB_ERR_ASSERT, "T != c1 + c2/3: tie-break tally inconsistent");
     if (out) *out = r;
+}
+
+__global__ void k_level_to_i64(const int32_t* __restrict__ in, int64_t* __restrict__ out,
+                               int64_t n) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = in[i];
 }
 
 }  // namespace
@@ -167,12 +179,21 @@ TCB_API int tcb_rmat_generate(tcb_context* ctx, int scale, int64_t edge_factor, 
 }
 
 TCB_API int tcb_csr_build(tcb_context* ctx, const int64_t* d_pairs, int64_t k, int64_t n,
-                          int64_t* d_row_offsets, int32_t* d_neighbors, int32_t* d_edge_u,
-                          int32_t* d_edge_v, int64_t* m_out) {
+                          int64_t* d_row_offsets, int32_t* d_neighbors, int32_t* d_src,
+                          int32_t* d_edge_u, int32_t* d_edge_v, int64_t* m_out) {
     return guarded(ctx, [&] {
         require(d_row_offsets && m_out, "null output");
         require(k == 0 || (d_pairs && d_neighbors), "null input");
-        csr_build(ctx, d_pairs, k, n, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, m_out);
+        csr_build(ctx, d_pairs, k, n, d_row_offsets, d_neighbors, d_src, d_edge_u, d_edge_v,
+                  m_out);
+    });
+}
+
+TCB_API int tcb_csr_rows(tcb_context* ctx, const int64_t* d_row_offsets, int64_t n,
+                         int32_t* d_src) {
+    return guarded(ctx, [&] {
+        require(n >= 0, "negative size");
+        csr_rows(ctx, d_row_offsets, n, d_src);
     });
 }
 
@@ -186,27 +207,25 @@ TCB_API int tcb_csr_edges(tcb_context* ctx, const int64_t* d_row_offsets,
 }
 
 TCB_API int tcb_bfs_levels(tcb_context* ctx, const int64_t* d_row_offsets,
-                           const int32_t* d_neighbors, const int32_t* d_edge_u,
-                           const int32_t* d_edge_v, int64_t n, int64_t m, int32_t* d_level,
-                           int64_t* components_out, int64_t* max_level_out) {
+                           const int32_t* d_neighbors, const int32_t* d_src, int64_t n, int64_t m,
+                           int32_t* d_level, int64_t* components_out, int64_t* max_level_out) {
     return guarded(ctx, [&] {
         require(n >= 0 && m >= 0, "negative size");
         require(n == 0 || (d_row_offsets && d_level), "null array");
-        bfs_levels(ctx, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, n, m, d_level, true);
+        bfs_levels(ctx, d_row_offsets, d_neighbors, d_src, n, m, d_level, true);
         fetch_counters(ctx);
-        collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 2);
         if (components_out) *components_out = int64_t(ctx->h_counters->components);
         if (max_level_out) *max_level_out = ctx->h_counters->max_level;
     });
 }
 
-TCB_API int tcb_cover_select(tcb_context* ctx, const int32_t* d_level, const int32_t* d_edge_u,
-                             const int32_t* d_edge_v, int64_t m, int32_t* d_cover_u,
+TCB_API int tcb_cover_select(tcb_context* ctx, const int32_t* d_level, const int32_t* d_src,
+                             const int32_t* d_neighbors, int64_t m, int32_t* d_cover_u,
                              int32_t* d_cover_v, int64_t* ncover_out) {
     return guarded(ctx, [&] {
         require(m >= 0, "negative size");
         int64_t* d_n = reinterpret_cast<int64_t*>(&ctx->d_counters->scratch[2]);
-        cover_select(ctx, d_level, d_edge_u, d_edge_v, m, d_cover_u, d_cover_v, d_n);
+        cover_select(ctx, d_level, d_src, d_neighbors, 2 * m, d_cover_u, d_cover_v, d_n);
         int64_t k = 0;
         TCB_CUDA(cudaMemcpyAsync(&k, d_n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
         sync(ctx);
@@ -233,44 +252,34 @@ TCB_API int tcb_cetc_count(tcb_context* ctx, const int64_t* d_row_offsets,
 }
 
 TCB_API int tcb_cetc(tcb_context* ctx, const int64_t* d_row_offsets, const int32_t* d_neighbors,
-                     const int32_t* d_edge_u, const int32_t* d_edge_v, int64_t n, int64_t m,
-                     int32_t* d_level_out, int32_t* d_cover_u, int32_t* d_cover_v,
-                     tcb_result* out) {
+                     const int32_t* d_src, int64_t n, int64_t m, int32_t* d_level_out,
+                     int32_t* d_cover_u, int32_t* d_cover_v, tcb_result* out) {
     return guarded(ctx, [&] {
         require(n >= 0 && m >= 0, "negative size");
         int32_t* level = d_level_out ? d_level_out : ctx->wsT<int32_t>(WS_LEVEL, n);
-        int32_t* cu = d_cover_u ? d_cover_u : ctx->wsT<int32_t>(WS_COVER_U, m);
-        int32_t* cv = d_cover_v ? d_cover_v : ctx->wsT<int32_t>(WS_COVER_V, m);
-        cetc_device(ctx, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, n, m, level, cu, cv);
+        cetc_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, level);
+        if (n > 0) collect_stage_times(ctx);
+        if (d_cover_u && d_cover_v && n > 0) {  // the reference-order cover set, on request
+            int64_t* d_k = reinterpret_cast<int64_t*>(&ctx->d_counters->scratch[2]);
+            cover_select(ctx, level, d_src, d_neighbors, 2 * m, d_cover_u, d_cover_v, d_k);
+        }
         fetch_counters(ctx);
         fill_result(ctx, out);
-        if (n > 0) collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 4);
     });
 }
 
 TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
-                           const int32_t* d_neighbors, const int32_t* d_edge_u,
-                           const int32_t* d_edge_v, int64_t n, int64_t m, int shard, int nshards,
-                           tcb_result* out) {
+                           const int32_t* d_neighbors, const int32_t* d_src, int64_t n, int64_t m,
+                           int shard, int nshards, tcb_result* out) {
     return guarded(ctx, [&] {
         require(n >= 0 && m >= 0, "negative size");
         require(nshards >= 1 && shard >= 0 && shard < nshards, "bad shard index");
         int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
-        int32_t* cu = ctx->wsT<int32_t>(WS_COVER_U, m);
-        int32_t* cv = ctx->wsT<int32_t>(WS_COVER_V, m);
-        cetc_device(ctx, d_row_offsets, d_neighbors, d_edge_u, d_edge_v, n, m, level, cu, cv,
-                    shard, nshards);
+        cetc_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, level, shard, nshards);
         fetch_counters(ctx);
         fill_result(ctx, out, /*partial=*/nshards > 1);
-        if (n > 0) collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 4);
+        if (n > 0) collect_stage_times(ctx);
     });
-}
-
-__global__ void k_level_to_i64(const int32_t* __restrict__ in, int64_t* __restrict__ out,
-                               int64_t n) {
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        out[i] = in[i];
 }
 
 TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
@@ -285,22 +294,19 @@ TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[8], ctx->stream));
         int64_t* row = ctx->wsT<int64_t>(WS_ROW, n + 1);
         int32_t* nb = ctx->wsT<int32_t>(WS_NB, nnz);
+        int32_t* src = ctx->wsT<int32_t>(WS_EDGE_U, nnz);
         TCB_CUDA(cudaMemcpyAsync(row, h_row_offsets, sizeof(int64_t) * (n + 1),
                                  cudaMemcpyHostToDevice, ctx->stream));
         if (nnz)
             TCB_CUDA(cudaMemcpyAsync(nb, h_neighbors, sizeof(int32_t) * nnz,
                                      cudaMemcpyHostToDevice, ctx->stream));
-        int32_t* eu = ctx->wsT<int32_t>(WS_EDGE_U, m);
-        int32_t* ev = ctx->wsT<int32_t>(WS_EDGE_V, m);
-        csr_edges(ctx, row, nb, n, m, eu, ev);
+        csr_rows(ctx, row, n, src);
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[9], ctx->stream));
         int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
-        int32_t* cu = ctx->wsT<int32_t>(WS_COVER_U, m);
-        int32_t* cv = ctx->wsT<int32_t>(WS_COVER_V, m);
-        cetc_device(ctx, row, nb, eu, ev, n, m, level, cu, cv);
+        cetc_device(ctx, row, nb, src, n, m, level);
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[10], ctx->stream));
         if (h_level_out && n > 0) {
-            int64_t* l64 = ctx->wsT<int64_t>(WS_MISC, n);
+            int64_t* l64 = ctx->wsT<int64_t>(WS_EDGE_V, n);
             TCB_LAUNCH(ctx, k_level_to_i64, grid_for(ctx, n, 256), 256, 0, level, l64, n);
             TCB_CUDA(cudaMemcpyAsync(h_level_out, l64, sizeof(int64_t) * n,
                                      cudaMemcpyDeviceToHost, ctx->stream));
@@ -310,7 +316,7 @@ TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[11], ctx->stream));
         sync(ctx);
         fill_result(ctx, out);
-        if (n > 0) collect_stage_times(ctx, 0, TCB_STAGE_COMPONENTS, 4);
+        if (n > 0) collect_stage_times(ctx);
         if (ctx->timing) {
             float ms = 0.f;
             TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]));

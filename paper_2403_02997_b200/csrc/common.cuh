@@ -70,7 +70,7 @@ struct DevCounters {
     // BFS rotating slots
     unsigned long long q_len[3];
     unsigned long long deg_sum[3];
-    unsigned long long scratch[8];
+    unsigned long long scratch[16];
 };
 
 struct Context {

@@ -16,17 +16,21 @@
 
 namespace tcb {
 
-void cover_select(Context* ctx, const int32_t* level, const int32_t* eu, const int32_t* ev,
-                  int64_t m, int32_t* cu, int32_t* cv, int64_t* d_ncover) {
+// CSR entries (u, v) with u < v are the edge list in lexicographic order
+// (graph.py:108-110), so an ordered compaction over them reproduces
+// cover_edges' order exactly.
+void cover_select(Context* ctx, const int32_t* level, const int32_t* src, const int32_t* nb,
+                  int64_t nnz, int32_t* cu, int32_t* cv, int64_t* d_ncover) {
     scan_apply(
-        ctx, m,
-        [level, eu, ev] __device__(int64_t e) -> int64_t {
-            return level[eu[e]] == level[ev[e]] ? 1 : 0;
+        ctx, nnz,
+        [level, src, nb] __device__(int64_t e) -> int64_t {
+            const int u = src[e], v = nb[e];
+            return (v > u && level[u] == level[v]) ? 1 : 0;
         },
-        [eu, ev, cu, cv] __device__(int64_t e, int64_t pos, int64_t keep) {
+        [src, nb, cu, cv] __device__(int64_t e, int64_t pos, int64_t keep) {
             if (keep) {
-                cu[pos] = eu[e];
-                cv[pos] = ev[e];
+                cu[pos] = src[e];
+                cv[pos] = nb[e];
             }
         },
         d_ncover);

@@ -136,7 +136,7 @@ __global__ void k_make_keys(const int64_t* __restrict__ pairs, int64_t k, int vb
 // From the unique sorted keys: neighbours and row offsets (graph.py:113-117).
 __global__ void k_csr_from_keys(const uint64_t* __restrict__ uk, const int64_t* __restrict__ m2p,
                                 int64_t n, int vb, int64_t* __restrict__ row,
-                                int32_t* __restrict__ nb) {
+                                int32_t* __restrict__ nb, int32_t* __restrict__ src) {
     const int64_t m2 = *m2p;
     const uint64_t dmask = (uint64_t(1) << vb) - 1;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -144,6 +144,7 @@ __global__ void k_csr_from_keys(const uint64_t* __restrict__ uk, const int64_t* 
         const uint64_t key = uk[i];
         const int64_t s = int64_t(key >> vb);
         nb[i] = int32_t(key & dmask);
+        if (src) src[i] = int32_t(s);
         const int64_t prev = i ? int64_t(uk[i - 1] >> vb) : -1;
         for (int64_t v = prev + 1; v <= s; ++v) row[v] = i;
         if (i == m2 - 1)
@@ -152,7 +153,7 @@ __global__ void k_csr_from_keys(const uint64_t* __restrict__ uk, const int64_t* 
 }
 
 void csr_build(Context* ctx, const int64_t* pairs, int64_t k, int64_t n, int64_t* row,
-               int32_t* nb, int32_t* eu, int32_t* ev, int64_t* m_out) {
+               int32_t* nb, int32_t* src, int32_t* eu, int32_t* ev, int64_t* m_out) {
     require(n >= 0 && k >= 0, "negative size");
     require(n < (int64_t(1) << 31), "vertex ids must fit int32 (n < 2^31)");
     TCB_CUDA(cudaMemsetAsync(row, 0, sizeof(int64_t) * (n + 1), ctx->stream));
@@ -184,7 +185,7 @@ void csr_build(Context* ctx, const int64_t* pairs, int64_t k, int64_t n, int64_t
         },
         d_m2);
     TCB_LAUNCH(ctx, k_csr_from_keys, grid_for(ctx, nk, 256), 256, 0, (const uint64_t*)uniq,
-               (const int64_t*)d_m2, n, vb, row, nb);
+               (const int64_t*)d_m2, n, vb, row, nb, src);
     if (eu && ev) {
         // graph.py:108-110: u<v pairs in lexicographic order = forward keys in order
         const uint64_t dmask = (uint64_t(1) << vb) - 1;
@@ -210,6 +211,24 @@ void csr_build(Context* ctx, const int64_t* pairs, int64_t k, int64_t n, int64_t
     TCB_CUDA(cudaMemcpyAsync(&m2, d_m2, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     TCB_CUDA(cudaStreamSynchronize(ctx->stream));
     *m_out = m2 / 2;
+}
+
+// ---------------------------------------------------------------------------
+// per-entry row ids (COO rows) from the offsets: warp per row
+
+__global__ void k_csr_rows(const int64_t* __restrict__ row, int64_t n, int32_t* __restrict__ src) {
+    const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (int64_t v = gw; v < n; v += nw) {
+        const int64_t b = row[v], e = row[v + 1];
+        for (int64_t p = b + lane; p < e; p += 32) src[p] = int32_t(v);
+    }
+}
+
+void csr_rows(Context* ctx, const int64_t* row, int64_t n, int32_t* src) {
+    if (n == 0) return;
+    TCB_LAUNCH(ctx, k_csr_rows, grid_for(ctx, n * 32, 256), 256, 0, row, n, src);
 }
 
 // ---------------------------------------------------------------------------

@@ -94,28 +94,42 @@ class Graph:
 
 @dataclass
 class DeviceGraph:
-    """The same CSR resident in HBM: int64 row offsets, int32 neighbours and
-    the u<v edge arrays (torch tensors on one CUDA device)."""
+    """The same CSR resident in HBM (torch tensors on one CUDA device):
+    int64 row offsets, int32 neighbours, and ``src`` — the int32 row id of
+    every entry (COO rows).  ``src`` has the footprint of the reference's
+    edge_u/edge_v pair, whose entries are exactly the src < neighbour ones in
+    order; those arrays are derived on demand (``edge_arrays``)."""
 
     n: int
     m: int
     row_offsets: "object"   # torch.int64 [n+1]
     neighbors: "object"     # torch.int32 [2m]
-    edge_u: "object"        # torch.int32 [m]
-    edge_v: "object"        # torch.int32 [m]
+    src: "object"           # torch.int32 [2m]
 
     @property
     def device(self):
         return self.row_offsets.device
 
+    def edge_arrays(self):
+        """Graph.edge_u/edge_v (u<v, lexicographic) as int32 device tensors."""
+        import torch
+        ctx = _lib.context(self.device.index)
+        eu = torch.empty(max(self.m, 1), dtype=torch.int32, device=self.device)
+        ev = torch.empty(max(self.m, 1), dtype=torch.int32, device=self.device)
+        ctx.check(ctx.lib.tcb_csr_edges(ctx.h, _lib.ptr(self.row_offsets),
+                                        _lib.ptr(self.neighbors), self.n, self.m,
+                                        _lib.ptr(eu), _lib.ptr(ev)))
+        return eu[: self.m], ev[: self.m]
+
     def to_host(self) -> Graph:
+        eu, ev = self.edge_arrays()
         g = Graph(
             n=self.n,
             m=self.m,
             row_offsets=_freeze(self.row_offsets.cpu().numpy()),
             neighbors=_freeze(self.neighbors.cpu().numpy()),
-            edge_u=_freeze(self.edge_u.cpu().numpy()),
-            edge_v=_freeze(self.edge_v.cpu().numpy()),
+            edge_u=_freeze(eu.cpu().numpy()),
+            edge_v=_freeze(ev.cpu().numpy()),
         )
         object.__setattr__(g, "_device", self)
         return g
@@ -123,7 +137,7 @@ class DeviceGraph:
     @property
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size()
-                   for t in (self.row_offsets, self.neighbors, self.edge_u, self.edge_v))
+                   for t in (self.row_offsets, self.neighbors, self.src))
 
 
 def _check_vertex_count(n: int):
@@ -150,15 +164,13 @@ def normalize_device(n: int, pairs) -> DeviceGraph:
     k = pairs.shape[0]
     row = torch.empty(n + 1, dtype=torch.int64, device=dev)
     nb = torch.empty(max(2 * k, 1), dtype=torch.int32, device=dev)
-    eu = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
-    ev = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    src = torch.empty(max(2 * k, 1), dtype=torch.int32, device=dev)
     m = _lib.ctypes.c_int64(0)
     ctx.check(ctx.lib.tcb_csr_build(ctx.h, _lib.ptr(pairs), k, n, _lib.ptr(row),
-                                    _lib.ptr(nb), _lib.ptr(eu), _lib.ptr(ev),
+                                    _lib.ptr(nb), _lib.ptr(src), None, None,
                                     _lib.ctypes.byref(m)))
     m = int(m.value)
-    return DeviceGraph(n=n, m=m, row_offsets=row, neighbors=nb[: 2 * m],
-                       edge_u=eu[:m], edge_v=ev[:m])
+    return DeviceGraph(n=n, m=m, row_offsets=row, neighbors=nb[: 2 * m], src=src[: 2 * m])
 
 
 def normalize(el: EdgeList) -> Graph:
@@ -168,22 +180,22 @@ def normalize(el: EdgeList) -> Graph:
 
 
 def device_graph(g, device=None) -> DeviceGraph:
-    """The DeviceGraph behind a Graph (uploads once and caches it)."""
+    """The DeviceGraph behind a Graph (uploads the CSR once, expands the row
+    ids on the device, caches the result on the Graph)."""
     import torch
     if isinstance(g, DeviceGraph):
         return g
     dg = g._device
     if dg is not None and (device is None or dg.device == torch.device(device)):
         return dg
-    dev = torch.device(device) if device is not None else torch.device("cuda")
+    ctx = _lib.context(torch.device(device).index if device is not None else None)
+    dev = torch.device("cuda", ctx.device)
     _check_vertex_count(g.n)
-    dg = DeviceGraph(
-        n=g.n, m=g.m,
-        row_offsets=torch.from_numpy(np.ascontiguousarray(g.row_offsets, dtype=np.int64)).to(dev),
-        neighbors=torch.from_numpy(np.ascontiguousarray(g.neighbors, dtype=np.int32)).to(dev),
-        edge_u=torch.from_numpy(np.ascontiguousarray(g.edge_u, dtype=np.int32)).to(dev),
-        edge_v=torch.from_numpy(np.ascontiguousarray(g.edge_v, dtype=np.int32)).to(dev),
-    )
+    row = torch.from_numpy(np.ascontiguousarray(g.row_offsets, dtype=np.int64)).to(dev)
+    nb = torch.from_numpy(np.ascontiguousarray(g.neighbors, dtype=np.int32)).to(dev)
+    src = torch.empty(max(2 * g.m, 1), dtype=torch.int32, device=dev)
+    ctx.check(ctx.lib.tcb_csr_rows(ctx.h, _lib.ptr(row), g.n, _lib.ptr(src)))
+    dg = DeviceGraph(n=g.n, m=g.m, row_offsets=row, neighbors=nb, src=src[: 2 * g.m])
     object.__setattr__(g, "_device", dg)
     return dg
 

@@ -47,8 +47,8 @@ def bfs_levels(dg: DeviceGraph):
     comps = ctypes.c_int64(0)
     ml = ctypes.c_int64(0)
     ctx.check(ctx.lib.tcb_bfs_levels(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
-                                     _lib.ptr(dg.edge_u), _lib.ptr(dg.edge_v), dg.n, dg.m,
-                                     _lib.ptr(level), ctypes.byref(comps), ctypes.byref(ml)))
+                                     _lib.ptr(dg.src), dg.n, dg.m, _lib.ptr(level),
+                                     ctypes.byref(comps), ctypes.byref(ml)))
     return level[: dg.n], int(comps.value), int(ml.value)
 
 
@@ -61,8 +61,8 @@ def cover_select(dg: DeviceGraph, level):
     cu = torch.empty(max(dg.m, 1), dtype=torch.int32, device=dg.device)
     cv = torch.empty(max(dg.m, 1), dtype=torch.int32, device=dg.device)
     k = ctypes.c_int64(0)
-    ctx.check(ctx.lib.tcb_cover_select(ctx.h, _lib.ptr(level), _lib.ptr(dg.edge_u),
-                                       _lib.ptr(dg.edge_v), dg.m, _lib.ptr(cu), _lib.ptr(cv),
+    ctx.check(ctx.lib.tcb_cover_select(ctx.h, _lib.ptr(level), _lib.ptr(dg.src),
+                                       _lib.ptr(dg.neighbors), dg.m, _lib.ptr(cu), _lib.ptr(cv),
                                        ctypes.byref(k)))
     k = int(k.value)
     return cu[:k], cv[:k]
@@ -97,8 +97,8 @@ def cetc(dg: DeviceGraph, keep_level: bool = False, keep_cover: bool = False) ->
         cv = torch.empty(max(dg.m, 1), dtype=torch.int32, device=dg.device)
     r = _lib.TcbResult()
     ctx.check(ctx.lib.tcb_cetc(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
-                               _lib.ptr(dg.edge_u), _lib.ptr(dg.edge_v), dg.n, dg.m,
-                               _lib.ptr(level), _lib.ptr(cu), _lib.ptr(cv), ctypes.byref(r)))
+                               _lib.ptr(dg.src), dg.n, dg.m, _lib.ptr(level), _lib.ptr(cu),
+                               _lib.ptr(cv), ctypes.byref(r)))
     d = r.as_dict()
     return CetcResult(
         level=level[: dg.n] if level is not None else None,
@@ -114,8 +114,8 @@ def cetc_shard(dg: DeviceGraph, shard: int, nshards: int) -> CetcResult:
     ctx = _lib.context(dg.device.index)
     r = _lib.TcbResult()
     ctx.check(ctx.lib.tcb_cetc_shard(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
-                                     _lib.ptr(dg.edge_u), _lib.ptr(dg.edge_v), dg.n, dg.m,
-                                     shard, nshards, ctypes.byref(r)))
+                                     _lib.ptr(dg.src), dg.n, dg.m, shard, nshards,
+                                     ctypes.byref(r)))
     return CetcResult(**r.as_dict())
 
 
