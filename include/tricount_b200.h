@@ -85,6 +85,11 @@ TCB_API int64_t tcb_launch_count(tcb_context* ctx);
  * for the last fused call (tcb_cetc / tcb_cetc_shard / tcb_cetc_host). */
 TCB_API int tcb_set_timing(tcb_context* ctx, int enabled);
 TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n);
+/* Intersection work-split knobs (0 = built-in default): owners with degree
+ * <= warp_tier_max_degree (max 1024) use the per-warp tier; larger owners
+ * are staged <= cta_stage_max ids (4..4096) per CTA pass.  Results do not
+ * depend on them; tests shrink them to drive every code path. */
+TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_stage_max);
 
 /* ---- input synthesis (rmat.py:45-72) ---------------------------------- */
 /* generate_rmat: edge_factor*2^scale pairs into d_pairs[2*total] (u,v

@@ -48,7 +48,8 @@ def load_library(path: Path | None = None):
     with _lib_lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        import os
+        p = Path(path or os.environ.get("TCB_LIBRARY") or LIB_PATH)
         if not p.exists():
             raise RuntimeError(
                 f"libtricount_b200.so not found at {p}; build it with "
@@ -68,6 +69,7 @@ def load_library(path: Path | None = None):
             "tcb_last_error": ([vp], ctypes.c_char_p),
             "tcb_launch_count": ([vp], i64),
             "tcb_set_timing": ([vp, i32], i32),
+            "tcb_set_tuning": ([vp, i32, i32], i32),
             "tcb_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), i32], i32),
             "tcb_rmat_generate": ([vp, i32, i64, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, u64, u64, u64, u64, vp, vp], i32),
@@ -144,6 +146,11 @@ class Context:
 
     def set_timing(self, on: bool):
         self.check(self.lib.tcb_set_timing(self.h, int(bool(on))))
+
+    def set_tuning(self, warp_tier_max_degree: int = 0, cta_stage_max: int = 0):
+        """Intersection work-split knobs (0 = defaults); results are unchanged."""
+        self.check(self.lib.tcb_set_tuning(self.h, int(warp_tier_max_degree),
+                                           int(cta_stage_max)))
 
     def stage_times(self) -> dict:
         arr = (ctypes.c_float * len(STAGES))()

@@ -160,6 +160,14 @@ TCB_API int tcb_set_timing(tcb_context* ctx, int enabled) {
     return guarded(ctx, [&] { ctx->timing = enabled != 0; });
 }
 
+TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_stage_max) {
+    return guarded(ctx, [&] {
+        require(warp_tier_max_degree >= 0 && cta_stage_max >= 0, "negative tuning value");
+        ctx->tune_wt = warp_tier_max_degree;
+        ctx->tune_hc = cta_stage_max;
+    });
+}
+
 TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n) {
     return guarded(ctx, [&] {
         require(ms_out != nullptr, "ms_out is null");

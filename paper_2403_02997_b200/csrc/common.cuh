@@ -87,6 +87,8 @@ struct Context {
     cudaEvent_t ev[16] = {};
     float stage_ms[TCB_NSTAGES] = {};
     int bfs_coop_blocks = 0;
+    int tune_wt = 0;   // intersection: warp-tier max owner degree (0 = default)
+    int tune_hc = 0;   // intersection: ids staged per CTA pass (0 = default)
 
     void* ws(Slot s, size_t bytes) {
         if (bytes == 0) bytes = 16;
@@ -140,6 +142,23 @@ inline int grid_for(const Context* ctx, int64_t items, int block, int per_sm = 8
 
 // ---------------------------------------------------------------------------
 // device helpers
+
+// Device-side invariant checks, compiled in only for the debug library
+// (make debug -> lib/libtricount_b200_checked.so; TCB_LIBRARY selects it).
+#ifdef TCB_CHECKS
+#include <cstdio>
+#define TCB_DASSERT(c)                                                              \
+    do {                                                                            \
+        if (!(c)) {                                                                 \
+            printf("TCB_DASSERT %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #c, int(blockIdx.x), int(threadIdx.x));                          \
+        }                                                                           \
+    } while (0)
+#else
+#define TCB_DASSERT(c) \
+    do {               \
+    } while (0)
+#endif
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ unsigned lanemask_lt() {

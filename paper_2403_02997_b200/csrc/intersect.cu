@@ -8,31 +8,34 @@
 //
 // The reference merges both full lists per edge: W = sum_S (d(u)+d(v))
 // element steps (2.4e12 at RMAT-24).  Here each horizontal edge is owned by
-// its higher-degree endpoint x (ties: lower id).  x's list is staged ONCE in
-// shared memory and every partner y's list (the shorter one) is streamed past
-// it: sum_S min(d(u), d(v)) probes (10x fewer at RMAT-24) plus
-// sum over owners of d(x) inserts (<1% of that).
+// its higher-degree endpoint x (ties: lower id).  x's list is staged in a
+// shared-memory hash set and every partner y's list (the shorter one) is
+// streamed past it: sum_S min(d(u), d(v)) probes (10x fewer at RMAT-24).
 //
 //  1. owner_select: ordered compaction over the CSR entries (x, y) keeping
 //     level[x]==level[y] && owns(x, y).  Entries are in row order, so each
 //     owner's partners come out contiguous: P[seg_beg[x], seg_end[x]).
-//  2. make_items: owners with d(x) <= WT become warp items (x, p0, p1) with
-//     <= PW partners; larger owners become CTA items with <= PC partners.
-//  3. k_isect_warp: one warp per item; per-warp bucketed hash of N(x).
-//  4. k_isect_cta: one CTA per item.  d(x) <= HC: bucketed hash of N(x)
-//     (load <= 1/4).  d(x) > HC (hubs): N(x) is staged as a bitmap of one id
-//     range of R ids at a time; every partner keeps a cursor into its own list
-//     across ranges, so each partner element is read once per item.
+//  2. split points: the id space is cut into F equal ranges; split[v][r] is
+//     the position in N(v) of the first id in range r (one flat pass over
+//     the entries).  An owner whose list exceeds the table is staged one
+//     group of ranges at a time, and every partner's matching slice is read
+//     from the table — no per-partner searches.
+//  3. make_items: owners with d(x) <= WT -> warp items (x, p0, p1), <= PW
+//     partners each; others -> CTA items (x, p0, p1, group), <= PC partners.
+//  4. k_isect_warp: one warp per item; per-warp hash set of N(x).
+//  5. k_isect_cta: one CTA per item; the group's slice of N(x) (<= HC ids,
+//     load <= 1/4) staged; the partners' slices are flattened into one element
+//     stream (block scan of lengths) that warps consume in CHUNK-element
+//     grabs with 8 loads in flight per lane.
 //
 // Hash entries carry the apex's level relation to the owner in bit 31
 // (same level -> c2 candidate), so hits need no level gather.  Buckets are 4
-// entries (one LDS.128 per probe); linear probing over buckets.  Partners are
-// handed to warps dynamically; a long partner list is streamed by the whole
-// warp with 4 loads in flight per lane, short ones are flattened across lanes
-// (warp scan of lengths + shuffle search).  Tallies reduce per warp into one
-// 64-bit atomic each.
+// entries (one LDS.128 per probe); linear probing over buckets.  Tallies
+// reduce per warp into one 64-bit atomic each.
 #include "common.cuh"
 #include "scan.cuh"
+
+#include <cstdlib>
 
 namespace tcb {
 
@@ -40,15 +43,14 @@ constexpr int WT = 1024;              // warp tier: owner degree <= WT
 constexpr int W_SLOTS = 2 * WT;       // per-warp table: load <= 1/2
 constexpr int W_WARPS = 8;
 constexpr int PW = 64;                // partners per warp item
-constexpr int C_THREADS = 1024;
-constexpr int C_WARPS = C_THREADS / 32;
-constexpr int HC = 8192;              // CTA hash tier: owner degree <= HC
-constexpr int C_SLOTS = 4 * HC;       // load <= 1/4 (128 KB)
-constexpr int R_BITS = 20;            // hub tier: id range per bitmap pass
-constexpr int R_WORDS = (1 << R_BITS) / 32;  // 128 KB
-constexpr int C_TAB_WORDS = C_SLOTS > R_WORDS ? C_SLOTS : R_WORDS;
-constexpr int PC = 2048;              // partners per CTA item
-constexpr int LONG_LIST = 64;         // partner lists streamed by a whole warp
+constexpr int C_THREADS = 512;        // 2 CTAs per SM
+constexpr int HC = 4096;              // staged ids per CTA item
+constexpr int C_SLOTS = 4 * HC;       // load <= 1/4 (64 KB)
+constexpr int PC = 2 * C_THREADS;     // partners per CTA item (2 per thread in the scan)
+constexpr int CHUNK = 256;            // stream elements per warp grab (8 per lane)
+constexpr int LOG_F = 5;
+constexpr int F = 1 << LOG_F;         // id ranges for split points
+constexpr int LONG_LIST = 64;         // warp tier: lists streamed by a whole warp
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t SAME = 0x80000000u;
 
@@ -69,7 +71,7 @@ struct BucketHash {
         shift = 32 - lb;
     }
     __device__ __forceinline__ unsigned bucket(int key) const {
-        return shift >= 32 ? 0u : ((unsigned(key) * 0x9E3779B1u) >> shift);
+        return (unsigned(key) * 0x9E3779B1u) >> shift;
     }
     __device__ __forceinline__ void insert(int key, bool same) const {
         const uint32_t e = uint32_t(key) | (same ? SAME : 0u);
@@ -85,6 +87,7 @@ struct BucketHash {
     __device__ __forceinline__ int find(int key) const {
         unsigned b = bucket(key);
         while (true) {
+            TCB_DASSERT(b <= bmask);
             const uint4 v = reinterpret_cast<const uint4*>(tab)[b];
             const uint32_t k = uint32_t(key);
             if ((v.x & ~SAME) == k) return 1 + (v.x >> 31);
@@ -121,55 +124,36 @@ struct Tally {
     }
 };
 
-// Membership test against whichever staged structure the item uses.
-struct HashProbe {
-    BucketHash h;
-    __device__ __forceinline__ int operator()(int w) const { return h.find(w); }
-};
-struct BitmapProbe {
-    const uint32_t* bits;
-    const int32_t* level;
-    int lo, lx;
-    __device__ __forceinline__ int operator()(int w) const {
-        const unsigned off = unsigned(w - lo);
-        if (off >= (1u << R_BITS)) return 0;  // element of a skipped (empty) range
-        if (!((bits[off >> 5] >> (off & 31)) & 1u)) return 0;
-        return level[w] == lx ? 2 : 1;
-    }
-};
+// ---------------------------------------------------------------------------
+// warp tier helpers: one long list with the whole warp (4 loads in flight per
+// lane); a batch of <= 32 lists flattened across lanes.
 
-// Stream one long list [s, s+d) with the whole warp, 4 loads in flight/lane.
-template <typename Probe>
 __device__ __forceinline__ void probe_long(const int32_t* __restrict__ nb, int64_t s, int d,
-                                           int vmax, const Probe& probe, Tally& tl) {
+                                           int vmax, const BucketHash& h, Tally& tl) {
     const int lane = int(lane_id());
     int i = lane;
     for (; i + 96 < d; i += 128) {
         const int w0 = nb[s + i], w1 = nb[s + i + 32], w2 = nb[s + i + 64], w3 = nb[s + i + 96];
-        tl.add(probe(w0), w0, vmax);
-        tl.add(probe(w1), w1, vmax);
-        tl.add(probe(w2), w2, vmax);
-        tl.add(probe(w3), w3, vmax);
+        tl.add(h.find(w0), w0, vmax);
+        tl.add(h.find(w1), w1, vmax);
+        tl.add(h.find(w2), w2, vmax);
+        tl.add(h.find(w3), w3, vmax);
     }
     for (; i < d; i += 32) {
         const int w = nb[s + i];
-        tl.add(probe(w), w, vmax);
+        tl.add(h.find(w), w, vmax);
     }
 }
 
-// Batch of <= 32 partner lists (lane j: [ys_j, ys_j + yd_j), tie vertex vmax_j).
-// Long lists go one at a time through probe_long; the short remainder is
-// flattened across the lanes.
-template <typename Probe>
 __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int64_t ys, int yd,
-                                            int vmax, const Probe& probe, Tally& tl) {
+                                            int vmax, const BucketHash& h, Tally& tl) {
     const unsigned lane = lane_id();
     unsigned longs = __ballot_sync(0xffffffffu, yd >= LONG_LIST);
     while (longs) {
         const int k = __ffs(longs) - 1;
         longs &= longs - 1;
         probe_long(nb, __shfl_sync(0xffffffffu, ys, k), __shfl_sync(0xffffffffu, yd, k),
-                   __shfl_sync(0xffffffffu, vmax, k), probe, tl);
+                   __shfl_sync(0xffffffffu, vmax, k), h, tl);
     }
     if (yd >= LONG_LIST) yd = 0;
     const int incl = warp_inclusive_scan(yd);
@@ -187,7 +171,7 @@ __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int6
         const int vm = __shfl_sync(0xffffffffu, vmax, k);
         if (i < total) {
             const int w = nb[ysk + (i - exk)];
-            tl.add(probe(w), w, vm);
+            tl.add(h.find(w), w, vm);
         }
     }
 }
@@ -222,13 +206,33 @@ __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restri
 }
 
 // ---------------------------------------------------------------------------
-// 2. work items
+// 2. split points: split[v*(F+1) + r] = first position (relative to row[v])
+//    of an id >= r << rshift; split[.][0] = 0, split[.][F] = d(v).
+
+__global__ void k_split_points(const int64_t* __restrict__ row, const int32_t* __restrict__ src,
+                               const int32_t* __restrict__ nb, int64_t nnz, int rshift,
+                               int* __restrict__ split) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
+        const int v = src[e];
+        const int64_t rb = row[v];
+        const int r = nb[e] >> rshift;
+        int* sv = split + int64_t(v) * (F + 1);
+        const int prev = e == rb ? -1 : (nb[e - 1] >> rshift);
+        for (int q = prev + 1; q <= r; ++q) sv[q] = int(e - rb);
+        if (e == row[v + 1] - 1)
+            for (int q = r + 1; q <= F; ++q) sv[q] = int(e + 1 - rb);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 3. work items
 
 __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __restrict__ seg_beg,
-                             const int64_t* __restrict__ seg_end, int64_t n,
-                             longlong4* __restrict__ witems, longlong4* __restrict__ citems,
-                             unsigned long long* nw, unsigned long long* nc, int shard,
-                             int nshards) {
+                             const int64_t* __restrict__ seg_end, const int* __restrict__ split,
+                             int64_t n, longlong4* __restrict__ witems,
+                             longlong4* __restrict__ citems, unsigned long long* nw,
+                             unsigned long long* nc, int shard, int nshards, int wt, int hc) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += stride) {
         if (nshards > 1 && int(x % nshards) != shard) continue;  // owners shard by id
@@ -236,20 +240,40 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         if (d == 0) continue;
         const int64_t s = seg_beg[x], e = seg_end[x];
         if (e <= s) continue;
-        const int64_t per = d <= WT ? PW : PC;
-        const int64_t cnt = (e - s + per - 1) / per;
-        unsigned long long base = atomicAdd(d <= WT ? nw : nc, (unsigned long long)cnt);
-        longlong4* out = d <= WT ? witems : citems;
-        for (int64_t i = 0; i < cnt; ++i) {
-            const int64_t p0 = s + i * per;
-            const int64_t p1 = p0 + per < e ? p0 + per : e;
-            out[base + i] = make_longlong4(x, p0, p1, 0);
+        if (d <= wt) {
+            const int64_t cnt = (e - s + PW - 1) / PW;
+            unsigned long long base = atomicAdd(nw, (unsigned long long)cnt);
+            for (int64_t i = 0; i < cnt; ++i) {
+                const int64_t p0 = s + i * PW;
+                witems[base + i] = make_longlong4(x, p0, min(p0 + PW, e), 0);
+            }
+            continue;
         }
+        // fewest range groups G (power of two <= F) whose slices all fit HC
+        const int* sx = split + x * (F + 1);
+        int lg = 0;
+        if (d > hc) {
+            for (lg = 1; lg < LOG_F; ++lg) {
+                const int step = F >> lg;
+                int mx = 0;
+                for (int q = 0; q < F; q += step) mx = max(mx, sx[q + step] - sx[q]);
+                if (mx <= hc) break;
+            }
+        }
+        const int G = 1 << lg;
+        const int64_t per = (e - s + PC - 1) / PC;
+        unsigned long long base = atomicAdd(nc, (unsigned long long)(per * G));
+        for (int g = 0; g < G; ++g)
+            for (int64_t i = 0; i < per; ++i) {
+                const int64_t p0 = s + i * PC;
+                citems[base + g * per + i] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
+        TCB_DASSERT(sx[0] == 0 && sx[F] == int(d));
+            }
     }
 }
 
 // ---------------------------------------------------------------------------
-// 3. warp tier
+// 4. warp tier
 
 __global__ void __launch_bounds__(W_WARPS * 32)
     k_isect_warp(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
@@ -275,11 +299,11 @@ __global__ void __launch_bounds__(W_WARPS * 32)
         const int xd = int(row[x + 1] - xb);
         const int lx = level[x];
         const int slots = max(16, 2 << ceil_log2_dev(xd));
-        HashProbe probe;
-        probe.h.setup(tab, slots);
+        BucketHash h;
+        h.setup(tab, slots);
         for (int i = lane; i < xd; i += 32) {
             const int w = nb[xb + i];
-            probe.h.insert(w, level[w] == lx);
+            h.insert(w, level[w] == lx);
         }
         __syncwarp();
         for (int64_t pb = item.y; pb < item.z; pb += 32) {
@@ -292,7 +316,7 @@ __global__ void __launch_bounds__(W_WARPS * 32)
                 yd = int(row[y + 1] - ys);
                 vmax = max(x, y);
             }
-            probe_batch(nb, ys, yd, vmax, probe, tl);
+            probe_batch(nb, ys, yd, vmax, h, tl);
         }
         __syncwarp();
         for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
@@ -302,134 +326,204 @@ __global__ void __launch_bounds__(W_WARPS * 32)
 }
 
 // ---------------------------------------------------------------------------
-// 4. CTA tier
+// 5. CTA tier
 
-__global__ void __launch_bounds__(C_THREADS, 1)
+// Warps consume the flattened stream of partner slices in CHUNK grabs;
+// element i belongs to partner k with s_off[k] <= i < s_off[k+1].
+__device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, const int64_t* s_ys,
+                                              const int* s_off, const int* s_vm, int np,
+                                              int* s_next, const BucketHash& h, Tally& tl,
+                                              int dbg = 0) {
+    const int total = s_off[np];
+    TCB_DASSERT(np >= 1 && np <= PC && total >= 0);
+    const int lane = int(lane_id());
+    while (true) {
+        int c0 = 0;
+        if (lane == 0) c0 = atomicAdd(s_next, CHUNK);
+        c0 = __shfl_sync(0xffffffffu, c0, 0);
+        if (c0 >= total) break;
+        const int c1 = min(total, c0 + CHUNK);
+        const int i0 = c0 + lane;
+        int lo = 0, hi = np;  // invariant s_off[lo] <= i0 < s_off[hi] (when i0 < total)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_off[mid] <= i0) lo = mid; else hi = mid;
+        }
+        int k = lo;
+        TCB_DASSERT(k >= 0 && k < np);
+        int next = s_off[k + 1];
+        int64_t base = s_ys[k] - s_off[k];
+        int vm = s_vm[k];
+        int w[CHUNK / 32], vmj[CHUNK / 32];
+#pragma unroll
+        for (int j = 0; j < CHUNK / 32; ++j) {
+            const int i = i0 + 32 * j;
+            w[j] = -1;
+            if (i < c1) {
+                while (next <= i) {
+                    TCB_DASSERT(k + 1 < np);
+                    ++k;
+                    next = s_off[k + 1];
+                    base = s_ys[k] - s_off[k];
+                    vm = s_vm[k];
+                }
+                w[j] = (dbg & 16) ? int(base + i) & 0x7fffffff : nb[base + i];
+#ifdef TCB_CHECKS
+                if (base + i < 0 || base + i >= (int64_t(1) << 31))
+                    printf("BAD idx base=%lld i=%d k=%d np=%d off=%d ys=%lld\n", (long long)base, i, k,
+                           np, s_off[k], (long long)s_ys[k]);
+#endif
+            }
+            vmj[j] = vm;
+        }
+#pragma unroll
+        for (int j = 0; j < CHUNK / 32; ++j)
+            if (w[j] >= 0) {
+                int r;
+                if (dbg & 4) {
+                    const uint4 v = reinterpret_cast<const uint4*>(h.tab)[h.bucket(w[j])];
+                    r = ((v.x & ~SAME) == uint32_t(w[j])) ? 1 : 0;
+                } else {
+                    r = h.find(w[j]);
+                }
+                if (!(dbg & 8)) tl.add(r, w[j], vmj[j]);
+            }
+    }
+}
+
+// Exclusive block scan of the per-partner lengths (thread t holds partners
+// 2t, 2t+1) into s_off[0..np]; s_off[np] = stream length.
+__device__ __forceinline__ void scan_lengths(int* s_off, int np, int64_t* s_tmp) {
+    __syncthreads();  // lengths were written with a different thread->partner map
+    const int t = threadIdx.x;
+    const int a = 2 * t < np ? s_off[2 * t] : 0;
+    const int b = 2 * t + 1 < np ? s_off[2 * t + 1] : 0;
+    int64_t tot;
+    const int64_t ex = block_exclusive_scan<C_THREADS>(int64_t(a + b), s_tmp, tot);
+    if (2 * t < np) s_off[2 * t] = int(ex);
+    if (2 * t + 1 < np) s_off[2 * t + 1] = int(ex + a);
+    if (t == 0) s_off[np] = int(tot);
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(C_THREADS, 2)
     k_isect_cta(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                 const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                 const int32_t* __restrict__ P, const int32_t* __restrict__ level,
-                unsigned long long* fetch, DevCounters* C) {
+                const int* __restrict__ split, unsigned long long* fetch, DevCounters* C,
+                int hc, int dbg) {
     extern __shared__ uint4 smem4[];
-    uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);    // C_TAB_WORDS
-    int* cursor = reinterpret_cast<int*>(tab + C_TAB_WORDS);  // PC
+    uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS
+    int64_t* s_ys = reinterpret_cast<int64_t*>(tab + C_SLOTS);    // PC
+    int* s_off = reinterpret_cast<int*>(s_ys + PC);               // PC + 1
+    int* s_vm = s_off + PC + 1;                                   // PC
+    int* s_end = s_vm + PC;                                       // PC (sub-chunk cursors)
+    __shared__ int64_t s_tmp[C_THREADS / 32 + 1];
     __shared__ unsigned long long s_item;
     __shared__ int s_next;
-    const unsigned lane = lane_id();
     const unsigned long long nitems = *nitems_p;
     Tally tl;
     while (true) {
-        if (threadIdx.x == 0) {
-            s_item = atomicAdd(fetch, 1ull);
-            s_next = 0;
-        }
+        if (threadIdx.x == 0) s_item = atomicAdd(fetch, 1ull);
         __syncthreads();
         const unsigned long long it = s_item;
         if (it >= nitems) break;
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int64_t xb = row[x], xe = row[x + 1];
-        const int xd = int(xe - xb);
+        const int lg = int(item.w >> 8), g = int(item.w & 255);
+        const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;  // ranges [q0, q1)
+        const int64_t xrow = row[x];
+        const int* sx = split + int64_t(x) * (F + 1);
+        const int64_t xs = xrow + (lg ? sx[q0] : 0);
+        const int64_t xe = lg ? xrow + sx[q1] : row[x + 1];
         const int lx = level[x];
         const int np = int(item.z - item.y);
-        if (xd <= HC) {
-            // ---- hash tier: whole N(x) staged once
-            const int slots = 4 << ceil_log2_dev(xd);
-            HashProbe probe;
-            probe.h.setup(tab, slots);
+        // partner slices for ranges [q0, q1) (the whole list when lg == 0)
+        for (int t = threadIdx.x; t < np; t += C_THREADS) {
+            const int y = P[item.y + t];
+            const int64_t yb = row[y];
+            int a = 0, b;
+            if (lg) {
+                const int* sy = split + int64_t(y) * (F + 1);
+                a = sy[q0];
+                b = sy[q1];
+            } else {
+                b = int(row[y + 1] - yb);
+            }
+            s_ys[t] = yb + a;
+            TCB_DASSERT(0 <= a && a <= b && b <= int(row[y + 1] - yb));
+            s_end[t] = b - a;  // slice length; consumed below
+            s_vm[t] = max(x, y);
+        }
+        // stage the owner slice in sub-chunks of hc ids (one pass unless the
+        // slice still exceeds hc with every range split — the largest hubs)
+        for (int64_t cb = xs; cb < xe; cb += hc) {
+            const int len = int(min(int64_t(hc), xe - cb));
+            TCB_DASSERT(len >= 1 && len <= HC && xs >= row[x] && xe <= row[x + 1]);
+            const bool single = (cb == xs) && (cb + len >= xe);
+            const int slots = 4 << ceil_log2_dev(max(len, 4));
+            BucketHash h;
+            h.setup(tab, slots);
+            TCB_DASSERT(slots <= C_SLOTS && np <= PC);
             for (int i = threadIdx.x; i < slots; i += C_THREADS) tab[i] = EMPTY;
+            if (threadIdx.x == 0) s_next = 0;
             __syncthreads();
-            for (int i = threadIdx.x; i < xd; i += C_THREADS) {
-                const int w = nb[xb + i];
-                probe.h.insert(w, level[w] == lx);
-            }
-            __syncthreads();
-            while (true) {  // warps grab 32-partner batches
-                int q0 = 0;
-                if (lane == 0) q0 = atomicAdd(&s_next, 32);
-                q0 = __shfl_sync(0xffffffffu, q0, 0);
-                if (q0 >= np) break;
-                const int q = q0 + int(lane);
-                int64_t ys = 0;
-                int yd = 0, vmax = 0;
-                if (q < np) {
-                    const int y = P[item.y + q];
-                    ys = row[y];
-                    yd = int(row[y + 1] - ys);
-                    vmax = max(x, y);
+            if (!(dbg & 2))
+                for (int i = threadIdx.x; i < len; i += C_THREADS) {
+                    const int w = nb[cb + i];
+                    h.insert(w, level[w] == lx);
                 }
-                probe_batch(nb, ys, yd, vmax, probe, tl);
-            }
-        } else {
-            // ---- hub tier: one id range [lo, lo + 2^R_BITS) of N(x) at a time
-            for (int i = threadIdx.x; i < np; i += C_THREADS) cursor[i] = 0;
-            int64_t xc = xb;  // first entry of N(x) in the current range
-            while (xc < xe) {
-                const int lo = nb[xc] & ~((1 << R_BITS) - 1);
-                const int64_t hi_excl = int64_t(lo) + (1 << R_BITS);
-                // end of this range within N(x): gallop + binary search
-                int64_t a = xc, step = 1;
-                while (a + step - 1 < xe && nb[a + step - 1] < hi_excl) {
-                    a += step;
-                    step <<= 1;
-                }
-                int64_t bnd = a + step - 1 < xe ? a + step - 1 : xe;
-                while (a < bnd) {
-                    const int64_t mid = (a + bnd) >> 1;
-                    if (nb[mid] < hi_excl) a = mid + 1; else bnd = mid;
-                }
-                const int64_t xr = a;
-                const bool last = xr >= xe;
-                for (int i = threadIdx.x; i < R_WORDS; i += C_THREADS) tab[i] = 0u;
-                __syncthreads();
-                for (int64_t i = xc + threadIdx.x; i < xr; i += C_THREADS) {
-                    const unsigned off = unsigned(nb[i] - lo);
-                    atomicOr(&tab[off >> 5], 1u << (off & 31));
-                }
-                if (threadIdx.x == 0) s_next = 0;
-                __syncthreads();
-                BitmapProbe probe{tab, level, lo, lx};
-                while (true) {
-                    int q0 = 0;
-                    if (lane == 0) q0 = atomicAdd(&s_next, 32);
-                    q0 = __shfl_sync(0xffffffffu, q0, 0);
-                    if (q0 >= np) break;
-                    const int q = q0 + int(lane);
-                    int64_t ys = 0;
-                    int yd = 0, vmax = 0;
-                    if (q < np) {
-                        const int y = P[item.y + q];
-                        const int64_t yb = row[y], ye = row[y + 1];
-                        vmax = max(x, y);
-                        ys = yb + cursor[q];
-                        int64_t end = ye;
-                        if (!last) {  // first position with value >= hi_excl
-                            int64_t l2 = ys, st = 1;
-                            while (l2 + st - 1 < ye && nb[l2 + st - 1] < hi_excl) {
-                                l2 += st;
-                                st <<= 1;
-                            }
-                            int64_t h2 = l2 + st - 1 < ye ? l2 + st - 1 : ye;
-                            while (l2 < h2) {
-                                const int64_t mid = (l2 + h2) >> 1;
-                                if (nb[mid] < hi_excl) l2 = mid + 1; else h2 = mid;
-                            }
-                            end = l2;
+            if (single) {
+                for (int t = threadIdx.x; t < np; t += C_THREADS) s_off[t] = s_end[t];
+            } else {
+                // sub-chunk [vlo, vhi] of the owner slice: each partner's
+                // matching part starts where its previous part ended
+                const int vhi = nb[cb + len - 1];
+                const bool last = cb + len >= xe;
+                for (int t = threadIdx.x; t < np; t += C_THREADS) {
+                    int64_t a = s_ys[t];
+                    const int64_t e = a + s_end[t];
+                    int64_t lo = a, hi = e;
+                    if (!last)
+                        while (lo < hi) {
+                            const int64_t mid = (lo + hi) >> 1;
+                            if (nb[mid] <= vhi) lo = mid + 1; else hi = mid;
                         }
-                        yd = int(end - ys);
-                        cursor[q] = int(end - yb);
-                    }
-                    probe_batch(nb, ys, yd, vmax, probe, tl);
+                    else
+                        lo = e;
+                    s_off[t] = int(lo - a);
+                }
+            }
+            scan_lengths(s_off, np, s_tmp);  // ends with __syncthreads
+            if (!(dbg & 1)) stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, h, tl, dbg);
+            __syncthreads();
+            if (!single) {  // advance partner starts past this sub-chunk
+                for (int t = threadIdx.x; t < np; t += C_THREADS) {
+                    const int used = s_off[t + 1] - s_off[t];
+                    s_ys[t] += used;
+                    s_end[t] -= used;
                 }
                 __syncthreads();
-                xc = xr;
             }
         }
+        // an item whose owner slice is empty runs no sub-chunk: without this
+        // barrier thread 0 could overwrite s_item before all threads read it
         __syncthreads();
     }
     tl.flush(C);
 }
 
 // ---------------------------------------------------------------------------
+
+// TCB_DBG bit flags disable parts of the CTA tier (checked builds only)
+static int debug_flags() {
+#ifdef TCB_CHECKS
+    const char* e = getenv("TCB_DBG");
+    return e ? atoi(e) : 0;
+#else
+    return 0;
+#endif
+}
 
 struct IsectKernels {
     int warp_blocks = 0, cta_blocks = 0;
@@ -444,7 +538,12 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     int2* vinfo = ctx->wsT<int2>(WS_MISC, n);
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
-    const int64_t wcap = n + m / PW + 1, ccap = 2 * m / WT + 1 + m / PC + 1;
+    int* split = ctx->wsT<int>(WS_COVER_V, size_t(n) * (F + 1));
+    // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
+    const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
+    const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
+    const int64_t wcap = n + m / PW + 1;
+    const int64_t ccap = (2 * m / (wt + 1) + 2 + m / PC) * F;
     longlong4* items = ctx->wsT<longlong4>(WS_BINS, wcap + ccap);
     longlong4* witems = items;
     longlong4* citems = items + wcap;
@@ -453,16 +552,21 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     unsigned long long* fw = &C->scratch[7];
     unsigned long long* fc = &C->scratch[8];
     int64_t* d_ncover = reinterpret_cast<int64_t*>(&C->ncover);
+    const int rshift = max(0, bits_for(n) - LOG_F);
 
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo);
     owner_select(ctx, row, src, nb, vinfo, nnz, P, seg, seg + n, d_ncover);
     ctx->record(3);
+    TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, row, src, nb, nnz, rshift,
+               split);
     TCB_LAUNCH(ctx, k_make_items, grid_for(ctx, n, 256), 256, 0, row, (const int64_t*)seg,
-               (const int64_t*)(seg + n), n, witems, citems, nw, nc, shard, nshards);
+               (const int64_t*)(seg + n), (const int*)split, n, witems, citems, nw, nc, shard,
+               nshards, wt, hc);
 
     IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
-    const size_t csm = size_t(C_TAB_WORDS) * sizeof(uint32_t) + size_t(PC) * sizeof(int);
+    const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(PC) * sizeof(int64_t) +
+                       size_t(3 * PC + 1) * sizeof(int);
     if (K.warp_blocks == 0) {
         TCB_CUDA(cudaFuncSetAttribute(k_isect_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(wsm)));
@@ -476,7 +580,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         K.cta_blocks = b * ctx->num_sms;
     }
     TCB_LAUNCH(ctx, k_isect_cta, K.cta_blocks, C_THREADS, csm, (const longlong4*)citems,
-               (const unsigned long long*)nc, row, nb, (const int32_t*)P, level, fc, C);
+               (const unsigned long long*)nc, row, nb, (const int32_t*)P, level,
+               (const int*)split, fc, C, hc, debug_flags());
     TCB_LAUNCH(ctx, k_isect_warp, K.warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
                (const unsigned long long*)nw, row, nb, (const int32_t*)P, level, fw, C);
 }

@@ -129,3 +129,31 @@ def test_config_parity_large(name):
     if name not in config_goldens():
         pytest.skip(f"no golden for {name}")
     _check_config(name)
+
+
+@pytest.mark.parametrize("tuning", [(4, 4), (4, 8), (16, 64), (1024, 16), (0, 0)])
+def test_every_intersection_path_small(tuning):
+    """Shrunk thresholds push small owners through the CTA tier, its range
+    groups and the sub-chunk path; counts must not change."""
+    ctx = tb._lib.context()
+    ctx.set_tuning(*tuning)
+    try:
+        for case in SMALL_CASES:
+            g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+            r = tb.cetc(tb.device_graph(g))
+            assert (r.triangles, r.c1, r.c2) == (case.T, case.c1, case.c2), case.name
+    finally:
+        ctx.set_tuning(0, 0)
+
+
+@pytest.mark.parametrize("tuning", [(64, 64), (16, 512)])
+def test_every_intersection_path_rmat16(tuning):
+    gold = config_goldens()["rmat16"]
+    dg = C.build_device_graph("rmat16")
+    ctx = tb._lib.context()
+    ctx.set_tuning(*tuning)
+    try:
+        r = tb.cetc(dg)
+    finally:
+        ctx.set_tuning(0, 0)
+    assert (r.triangles, r.c1, r.c2) == (gold["T"], gold["c1"], gold["c2"])
