@@ -83,9 +83,21 @@ struct BucketHash {
             b = (b + 1) & bmask;
         }
     }
-    // 0 = miss, 1 = hit other level, 2 = hit same level
+    // 0 = miss, 1 = hit other level, 2 = hit same level.  The first bucket
+    // is resolved without branches; the loop runs only when that bucket is
+    // full and does not hold the key (rare at load <= 1/4).
     __device__ __forceinline__ int find(int key) const {
         unsigned b = bucket(key);
+        {
+            const uint4 v = reinterpret_cast<const uint4*>(tab)[b];
+            const uint32_t k = uint32_t(key);
+            const bool m0 = ((v.x ^ k) << 1) == 0u, m1 = ((v.y ^ k) << 1) == 0u;
+            const bool m2 = ((v.z ^ k) << 1) == 0u, m3 = ((v.w ^ k) << 1) == 0u;
+            const uint32_t e = m0 ? v.x : (m1 ? v.y : (m2 ? v.z : v.w));
+            const bool hit = m0 | m1 | m2 | m3;
+            if (hit || v.w == EMPTY) return hit ? 1 + int(e >> 31) : 0;
+            b = (b + 1) & bmask;
+        }
         while (true) {
             TCB_DASSERT(b <= bmask);
             const uint4 v = reinterpret_cast<const uint4*>(tab)[b];
@@ -104,13 +116,10 @@ struct Tally {
     unsigned long long c1 = 0, c2 = 0, t = 0;
     // r: 1 = apex on another level, 2 = apex on the owner's level
     __device__ __forceinline__ void add(int r, int w, int vmax) {
-        if (r == 1) {
-            c1++;
-            t++;
-        } else if (r == 2) {
-            c2++;
-            t += (w > vmax);
-        }
+        const unsigned other = r == 1, same = r == 2;
+        c1 += other;
+        c2 += same;
+        t += other | (same & unsigned(w > vmax));
     }
     __device__ __forceinline__ void flush(DevCounters* C) {
         c1 = warp_sum(c1);
