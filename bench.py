@@ -246,11 +246,9 @@ def main():
         flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
 
     def step():
-        if world > 1:
+        if world > 1:  # owner-sharded intersection + one 24-byte all-reduce
             r = tb.ops.cetc_shard(dg, rank, world)
-            t = torch.tensor([r.triangles, r.c1, r.c2], dtype=torch.int64, device=dev)
-            dist.all_reduce(t)
-            return r, t.tolist()
+            return r, list(tb.dist.reduce_counts(r.triangles, r.c1, r.c2, device=dev))
         r = tb.cetc(dg)
         return r, [r.triangles, r.c1, r.c2]
 
@@ -378,8 +376,9 @@ def main():
         import oracle
         row = dg.row_offsets.cpu().numpy()
         nb = dg.neighbors.cpu().numpy()
-        eu = dg.edge_u.cpu().numpy()
-        ev = dg.edge_v.cpu().numpy()
+        eu_d, ev_d = dg.edge_arrays()
+        eu, ev = eu_d.cpu().numpy(), ev_d.cpu().numpy()
+        del eu_d, ev_d
         line["cpu_baseline"] = cpu_sample(dg.n, row, nb, eu, ev, args.cpu_seconds,
                                           oracle.max_threads())
     if rank == 0:

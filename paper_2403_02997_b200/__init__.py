@@ -32,6 +32,7 @@ from .sequential import SEQUENTIAL_IDS, count_sequential, tc_cetc
 from .parallel import PARALLEL_IDS, ParallelConfig, tc_cetc_sm, tc_par
 from .ops import CetcResult, cetc, cetc_host, cetc_shard
 from . import ops
+from . import dist
 from . import configs
 
 __version__ = "0.1.0"

@@ -1,0 +1,104 @@
+"""Multi-rank path on CPU (gloo, world size 2) and on one GPU (shards run one
+after another, no rank waits on another).
+
+The CPU test restates the sharded intersection with numpy on the oracle's
+levels: each rank counts the cover edges whose owner maps to it, and
+reduce_counts sums the partials with a real all-reduce.  It pins the owner /
+shard rule (every cover edge counted by exactly one rank) and the reduction.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from conftest import SMALL_CASES
+from paper_2403_02997_b200 import dist as tdist
+
+CASES = [c for c in SMALL_CASES if c.name in ("karate", "rmat10_42", "k8", "er60_915", "rmat7_9")]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _partials(case, rank, world):
+    level, _, _, _ = oracle.bfs_levels(case.row, case.nb, case.n)
+    deg = np.diff(case.row)
+    cov = oracle.cover_select(level, case.eu, case.ev)
+    c1 = c2 = t = 0
+    if len(cov):
+        u, v = cov[:, 0], cov[:, 1]
+        own = tdist.owner_of(u, v, deg[u], deg[v])
+        mine = tdist.shard_of(own, world) == rank
+        for a, b in cov[mine]:
+            common = np.intersect1d(case.nb[case.row[a]:case.row[a + 1]],
+                                    case.nb[case.row[b]:case.row[b + 1]])
+            for w in common:
+                if level[w] != level[a]:
+                    c1 += 1
+                    t += 1
+                else:
+                    c2 += 1
+                    t += int(w > b)
+    return t, c1, c2
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        for case in CASES:
+            part = _partials(case, rank, world)
+            res[case.name] = (part, tdist.reduce_counts(*part))
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_shards_sum_to_reference():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for case in CASES:
+        parts = [out[r][case.name][0] for r in range(world)]
+        reduced = [out[r][case.name][1] for r in range(world)]
+        assert reduced[0] == reduced[1] == (case.T, case.c1, case.c2), case.name
+        assert sum(p[0] for p in parts) == case.T
+
+
+def test_owner_rule():
+    u = np.array([1, 5, 3]); v = np.array([2, 4, 9])
+    du = np.array([3, 7, 2]); dv = np.array([3, 1, 5])
+    assert tdist.owner_of(u, v, du, dv).tolist() == [1, 5, 9]
+    assert tdist.shard_of(np.array([4, 5]), 2).tolist() == [0, 1]
+
+
+def test_reduce_counts_single_process_passthrough():
+    assert tdist.reduce_counts(7, 4, 9) == (7, 4, 9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_gpu_shards_sum_to_total(world):
+    import paper_2403_02997_b200 as tb
+    for case in CASES:
+        g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+        dg = tb.device_graph(g)
+        parts = [tb.ops.cetc_shard(dg, r, world) for r in range(world)]
+        assert sum(p.triangles for p in parts) == case.T, case.name
+        assert sum(p.c1 for p in parts) == case.c1
+        assert sum(p.c2 for p in parts) == case.c2
+        assert all(p.ncover == len(case.cover) for p in parts)

@@ -34,7 +34,9 @@ def launches(path):
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 unit = d.get("Metric Unit", "")
                 v = float(d["Metric Value"].replace(",", ""))
-                us = v / 1e3 if unit == "nsecond" else (v * 1e3 if unit == "msecond" else v)
+                scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+                         "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+                us = v * scale.get(unit, 1e-3)
                 out.append((int(d["ID"]), d["Kernel Name"], us))
     tot = sum(x[2] for x in out)
     agg = {}
