@@ -262,7 +262,22 @@ def main():
     H = full.c1 + full.c2
     ncover = full.ncover
     expect = [full.triangles, full.c1, full.c2]
-    del du, dv, deg, full
+    # bytes the CTA-tier kernel must move (owners with d > WT = 1024): every
+    # partner slice streamed once (4 B/id), partner id + 2 offsets per cover
+    # edge (20 B), and the owner's list staged once per item (<= 1024 partners)
+    cu, cv = full.cover_u.long(), full.cover_v.long()
+    own_u = (du > dv) | ((du == dv) & (cu < cv))
+    d_own = torch.where(own_u, du, dv)
+    owner = torch.where(own_u, cu, cv)
+    cta = d_own > 1024
+    W_min_cta = int(torch.minimum(du, dv)[cta].sum().item())
+    S_cta = int(cta.sum().item())
+    staged = 0
+    if S_cta:
+        own_ids, per_owner = torch.unique(owner[cta], return_counts=True)
+        staged = int((deg[own_ids] * ((per_owner + 1023) // 1024)).sum().item())
+    b_cta = 4 * W_min_cta + 20 * S_cta + 4 * staged
+    del du, dv, deg, full, cu, cv, own_u, d_own, owner, cta
 
     for _ in range(args.warmup):
         if flush is not None:
@@ -334,27 +349,33 @@ def main():
         del row_h, nb_h
 
     peak, peak_kind = hbm_peak()
-    # roofline of the dominant kernel (intersection): SURVEY.md §8(d)
-    # B_int = 4 W + 24 |S| + 4 H algorithmic bytes per launch
+    # roofline of the dominant kernel, k_isect_cta (the CTA tier of the
+    # intersection), timed alone with CUDA events on its launch stream
+    t_cta = stages["isect_cta"] * 1e-3
+    achieved = b_cta / t_cta / 1e9 if t_cta > 0 else None
+    # SURVEY.md §8(d)'s merge-equivalent bytes for the whole intersection
+    # stage (both lists streamed per cover edge) — above P by construction
     b_int = 4 * W + 24 * ncover + 4 * H
     t_int = stages["intersect"] * 1e-3
-    achieved = b_int / t_int / 1e9 if t_int > 0 else None
     b_bfs = 8 * (dg.n + 1) + 16 * dg.m + 4 * dg.n
     t_bfs = (stages["components"] + stages["bfs"]) * 1e-3
     traffic = None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(cfg.name, {}).get("intersect_dram_bytes")
+            traffic = json.loads(prof.read_text()).get(cfg.name, {}).get("k_isect_cta_dram_bytes")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_intersect (per-cover-edge intersection)",
+    roofline = {"bound": "hbm", "kernel": "k_isect_cta",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "peak_kind": peak_kind,
-                "algorithmic_bytes": b_int,
-                "formula": "4*W + 24*|S| + 4*(c1+c2), W = sum_S (d(u)+d(v))",
-                "t_ms": stages["intersect"],
+                "peak_kind": peak_kind, "algorithmic_bytes": b_cta,
+                "formula": "4*sum_{S_cta} min(d(u),d(v)) + 20*|S_cta| + 4*staged owner ids",
+                "t_ms": stages["isect_cta"],
+                "survey_8d_intersect_stage": {
+                    "bytes": b_int, "t_ms": stages["intersect"],
+                    "effective_GBps": b_int / t_int / 1e9 if t_int > 0 else None,
+                    "formula": "4*W + 24*|S| + 4*(c1+c2), W = sum_S (d(u)+d(v))"},
                 "bfs": {"achieved": b_bfs / t_bfs / 1e9 if t_bfs > 0 else None,
                         "bytes": b_bfs, "t_ms": stages["components"] + stages["bfs"],
                         "formula": "8(n+1) + 16m + 4n"}}

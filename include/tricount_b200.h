@@ -56,7 +56,8 @@ enum {
     TCB_STAGE_INTERSECT = 3,   /* per-cover-edge |N(u) ∩ N(v)| + level dedup   */
     TCB_STAGE_H2D = 4,         /* host-buffer entry: uploads + row expansion   */
     TCB_STAGE_D2H = 5,         /* host-buffer entry: downloads                 */
-    TCB_NSTAGES = 6
+    TCB_STAGE_ISECT_CTA = 6,   /* the dominant kernel alone (CTA tier)          */
+    TCB_NSTAGES = 7
 };
 
 typedef struct tcb_context tcb_context;

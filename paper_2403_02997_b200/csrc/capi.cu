@@ -62,12 +62,19 @@ void collect_stage_times(Context* ctx) {
         TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[s], ctx->ev[s + 1]));
         ctx->stage_ms[TCB_STAGE_COMPONENTS + s] = ms;
     }
+    ctx->stage_ms[TCB_STAGE_ISECT_CTA] = 0.f;
+    if (ctx->isect_events) {
+        float ms = 0.f;
+        TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[5], ctx->ev[6]));
+        ctx->stage_ms[TCB_STAGE_ISECT_CTA] = ms;
+    }
 }
 
 // fused path on device-resident arrays; leaves results in ctx->d_counters
 void cetc_device(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
                  int64_t n, int64_t m, int32_t* level, int shard = 0, int nshards = 1) {
     TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
+    ctx->isect_events = false;
     if (n == 0) return;
     bfs_levels(ctx, row, nb, src, n, m, level, false);  // events 0, 1, 2
     if (m == 0) {
@@ -75,7 +82,8 @@ void cetc_device(Context* ctx, const int64_t* row, const int32_t* nb, const int3
         ctx->record(4);
         return;
     }
-    cetc_intersect_owner(ctx, row, nb, src, level, n, m, shard, nshards);  // event 3 inside
+    cetc_intersect_owner(ctx, row, nb, src, level, n, m, shard, nshards);  // events 3, 5, 6
+    ctx->isect_events = true;
     ctx->record(4);
 }
 

@@ -89,6 +89,7 @@ struct Context {
     int bfs_coop_blocks = 0;
     int tune_wt = 0;   // intersection: warp-tier max owner degree (0 = default)
     int tune_hc = 0;   // intersection: ids staged per CTA pass (0 = default)
+    bool isect_events = false;  // events 5/6 bracket the CTA-tier kernel
 
     void* ws(Slot s, size_t bytes) {
         if (bytes == 0) bytes = 16;

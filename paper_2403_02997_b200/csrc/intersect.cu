@@ -588,9 +588,11 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         K.warp_blocks = a * ctx->num_sms;
         K.cta_blocks = b * ctx->num_sms;
     }
+    ctx->record(5);
     TCB_LAUNCH(ctx, k_isect_cta, K.cta_blocks, C_THREADS, csm, (const longlong4*)citems,
                (const unsigned long long*)nc, row, nb, (const int32_t*)P, level,
                (const int*)split, fc, C, hc, debug_flags());
+    ctx->record(6);
     TCB_LAUNCH(ctx, k_isect_warp, K.warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
                (const unsigned long long*)nw, row, nb, (const int32_t*)P, level, fw, C);
 }
