@@ -338,11 +338,15 @@ __global__ void __launch_bounds__(W_WARPS * 32)
 // 5. CTA tier
 
 // Warps consume the flattened stream of partner slices in CHUNK grabs;
-// element i belongs to partner k with s_off[k] <= i < s_off[k+1].
+// element i belongs to partner k with s_off[k] <= i < s_off[k+1].  The
+// partner of a chunk's first element is found with two 32-way ballots over
+// s_off (np <= 1024); a chunk that lies inside one slice (the common case:
+// slices average hundreds of ids) takes a warp-uniform fast path with
+// coalesced loads and no per-element partner bookkeeping.
 __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, const int64_t* s_ys,
                                               const int* s_off, const int* s_vm, int np,
-                                              int* s_next, const BucketHash& h, Tally& tl,
-                                              int dbg = 0) {
+                                              int* s_next, const BucketHash& h, Tally& tl) {
+    constexpr int J = CHUNK / 32;
     const int total = s_off[np];
     TCB_DASSERT(np >= 1 && np <= PC && total >= 0);
     const int lane = int(lane_id());
@@ -352,51 +356,71 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (c0 >= total) break;
         const int c1 = min(total, c0 + CHUNK);
-        const int i0 = c0 + lane;
-        int lo = 0, hi = np;  // invariant s_off[lo] <= i0 < s_off[hi] (when i0 < total)
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_off[mid] <= i0) lo = mid; else hi = mid;
+        // k0 = largest k with s_off[k] <= c0  (s_off[0] = 0 <= c0)
+        int k0;
+        {
+            const int j = lane * 32;
+            const unsigned b1 = __ballot_sync(0xffffffffu, j < np && s_off[j] <= c0);
+            const int kb = 31 - __clz(b1);
+            const int j2 = kb * 32 + lane;
+            const unsigned b2 = __ballot_sync(0xffffffffu, j2 < np && s_off[j2] <= c0);
+            k0 = kb * 32 + 31 - __clz(b2);
         }
-        int k = lo;
-        TCB_DASSERT(k >= 0 && k < np);
-        int next = s_off[k + 1];
-        int64_t base = s_ys[k] - s_off[k];
-        int vm = s_vm[k];
-        int w[CHUNK / 32], vmj[CHUNK / 32];
+        TCB_DASSERT(k0 >= 0 && k0 < np);
+        uint32_t o1 = 0, o2 = 0, ot = 0;  // per-chunk tallies (<= J per lane)
+        if (s_off[k0 + 1] >= c1) {
+            // fast path: one partner slice
+            const int64_t base = s_ys[k0] - s_off[k0];
+            const int vm = s_vm[k0];
+            int w[J];
 #pragma unroll
-        for (int j = 0; j < CHUNK / 32; ++j) {
-            const int i = i0 + 32 * j;
-            w[j] = -1;
-            if (i < c1) {
-                while (next <= i) {
-                    TCB_DASSERT(k + 1 < np);
-                    ++k;
-                    next = s_off[k + 1];
-                    base = s_ys[k] - s_off[k];
-                    vm = s_vm[k];
-                }
-                w[j] = (dbg & 16) ? int(base + i) & 0x7fffffff : nb[base + i];
-#ifdef TCB_CHECKS
-                if (base + i < 0 || base + i >= (int64_t(1) << 31))
-                    printf("BAD idx base=%lld i=%d k=%d np=%d off=%d ys=%lld\n", (long long)base, i, k,
-                           np, s_off[k], (long long)s_ys[k]);
-#endif
+            for (int j = 0; j < J; ++j) {
+                const int i = c0 + lane + 32 * j;
+                w[j] = i < c1 ? nb[base + i] : -1;
             }
-            vmj[j] = vm;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                if (w[j] < 0) continue;
+                const int r = h.find(w[j]);
+                o1 += r == 1;
+                o2 += r == 2;
+                ot += (r == 1) | ((r == 2) & (w[j] > vm));
+            }
+        } else {
+            // chunk crosses slices: every lane walks forward from k0
+            int k = k0;
+            int next = s_off[k + 1];
+            int64_t base = s_ys[k] - s_off[k];
+            int vm = s_vm[k];
+            int w[J], vmj[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int i = c0 + lane + 32 * j;
+                w[j] = -1;
+                if (i < c1) {
+                    while (next <= i) {
+                        TCB_DASSERT(k + 1 < np);
+                        ++k;
+                        next = s_off[k + 1];
+                        base = s_ys[k] - s_off[k];
+                        vm = s_vm[k];
+                    }
+                    w[j] = nb[base + i];
+                }
+                vmj[j] = vm;
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                if (w[j] < 0) continue;
+                const int r = h.find(w[j]);
+                o1 += r == 1;
+                o2 += r == 2;
+                ot += (r == 1) | ((r == 2) & (w[j] > vmj[j]));
+            }
         }
-#pragma unroll
-        for (int j = 0; j < CHUNK / 32; ++j)
-            if (w[j] >= 0) {
-                int r;
-                if (dbg & 4) {
-                    const uint4 v = reinterpret_cast<const uint4*>(h.tab)[h.bucket(w[j])];
-                    r = ((v.x & ~SAME) == uint32_t(w[j])) ? 1 : 0;
-                } else {
-                    r = h.find(w[j]);
-                }
-                if (!(dbg & 8)) tl.add(r, w[j], vmj[j]);
-            }
+        tl.c1 += o1;
+        tl.c2 += o2;
+        tl.t += ot;
     }
 }
 
@@ -504,7 +528,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
                 }
             }
             scan_lengths(s_off, np, s_tmp);  // ends with __syncthreads
-            if (!(dbg & 1)) stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, h, tl, dbg);
+            if (!(dbg & 1)) stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, h, tl);
             __syncthreads();
             if (!single) {  // advance partner starts past this sub-chunk
                 for (int t = threadIdx.x; t < np; t += C_THREADS) {
