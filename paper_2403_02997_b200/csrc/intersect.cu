@@ -367,24 +367,34 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
             k0 = kb * 32 + 31 - __clz(b2);
         }
         TCB_DASSERT(k0 >= 0 && k0 < np);
-        uint32_t o1 = 0, o2 = 0, ot = 0;  // per-chunk tallies (<= J per lane)
+        // per-chunk tallies: hits, same-level hits, same-level hits with w > vmax
+        uint32_t nh = 0, ns = 0, nt = 0;
         if (s_off[k0 + 1] >= c1) {
             // fast path: one partner slice
-            const int64_t base = s_ys[k0] - s_off[k0];
+            const int32_t* p = nb + (s_ys[k0] - s_off[k0]) + c0 + lane;
             const int vm = s_vm[k0];
             int w[J];
+            if (c1 - c0 == CHUNK) {
 #pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const int i = c0 + lane + 32 * j;
-                w[j] = i < c1 ? nb[base + i] : -1;
-            }
+                for (int j = 0; j < J; ++j) w[j] = p[32 * j];
 #pragma unroll
-            for (int j = 0; j < J; ++j) {
-                if (w[j] < 0) continue;
-                const int r = h.find(w[j]);
-                o1 += r == 1;
-                o2 += r == 2;
-                ot += (r == 1) | ((r == 2) & (w[j] > vm));
+                for (int j = 0; j < J; ++j) {
+                    const int r = h.find(w[j]);
+                    nh += r != 0;
+                    ns += r >> 1;
+                    nt += (r >> 1) & (w[j] > vm);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < J; ++j) w[j] = c0 + lane + 32 * j < c1 ? p[32 * j] : -1;
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    if (w[j] < 0) continue;
+                    const int r = h.find(w[j]);
+                    nh += r != 0;
+                    ns += r >> 1;
+                    nt += (r >> 1) & (w[j] > vm);
+                }
             }
         } else {
             // chunk crosses slices: every lane walks forward from k0
@@ -413,14 +423,14 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
             for (int j = 0; j < J; ++j) {
                 if (w[j] < 0) continue;
                 const int r = h.find(w[j]);
-                o1 += r == 1;
-                o2 += r == 2;
-                ot += (r == 1) | ((r == 2) & (w[j] > vmj[j]));
+                nh += r != 0;
+                ns += r >> 1;
+                nt += (r >> 1) & (w[j] > vmj[j]);
             }
         }
-        tl.c1 += o1;
-        tl.c2 += o2;
-        tl.t += ot;
+        tl.c1 += nh - ns;
+        tl.c2 += ns;
+        tl.t += nh - ns + nt;
     }
 }
 
