@@ -56,8 +56,9 @@ enum {
     TCB_STAGE_INTERSECT = 3,   /* per-cover-edge |N(u) ∩ N(v)| + level dedup   */
     TCB_STAGE_H2D = 4,         /* host-buffer entry: uploads + row expansion   */
     TCB_STAGE_D2H = 5,         /* host-buffer entry: downloads                 */
-    TCB_STAGE_ISECT_CTA = 6,   /* the dominant kernel alone (CTA tier)          */
-    TCB_NSTAGES = 7
+    TCB_STAGE_ISECT_CTA = 6,   /* CTA tiers of the intersection (hub + hash)    */
+    TCB_STAGE_ISECT_HUB = 7,   /* the hub-bitmap kernel alone                   */
+    TCB_NSTAGES = 8
 };
 
 typedef struct tcb_context tcb_context;

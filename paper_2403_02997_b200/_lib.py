@@ -21,7 +21,7 @@ TCB_ERR_NOMEM = 3
 TCB_ERR_ASSERT = 4
 TCB_ERR_INTERNAL = 5
 
-STAGES = ("components", "bfs", "select", "intersect", "h2d", "d2h", "isect_cta")
+STAGES = ("components", "bfs", "select", "intersect", "h2d", "d2h", "isect_cta", "isect_hub")
 
 
 class TcbResult(ctypes.Structure):

@@ -63,10 +63,13 @@ void collect_stage_times(Context* ctx) {
         ctx->stage_ms[TCB_STAGE_COMPONENTS + s] = ms;
     }
     ctx->stage_ms[TCB_STAGE_ISECT_CTA] = 0.f;
+    ctx->stage_ms[TCB_STAGE_ISECT_HUB] = 0.f;
     if (ctx->isect_events) {
         float ms = 0.f;
         TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[5], ctx->ev[6]));
         ctx->stage_ms[TCB_STAGE_ISECT_CTA] = ms;
+        TCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[5], ctx->ev[7]));
+        ctx->stage_ms[TCB_STAGE_ISECT_HUB] = ms;
     }
 }
 

@@ -623,6 +623,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         K.cta_blocks = b * ctx->num_sms;
     }
     ctx->record(5);
+    ctx->record(7);  // no separate hub kernel in this design: hub stage = 0
     TCB_LAUNCH(ctx, k_isect_cta, K.cta_blocks, C_THREADS, csm, (const longlong4*)citems,
                (const unsigned long long*)nc, row, nb, (const int32_t*)P, level,
                (const int*)split, fc, C, hc, debug_flags());
