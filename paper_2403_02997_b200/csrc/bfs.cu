@@ -60,27 +60,84 @@ __global__ void k_cc_init(const int64_t* __restrict__ row, const int32_t* __rest
     }
 }
 
+// Union the trees of u and v, hooking the larger root under the smaller one
+// (so every tree's root stays its minimum id).  Lock-free: a failed CAS means
+// the root moved; continue from what it points to now.
+__device__ __forceinline__ void hook(int u, int v, int* parent) {
+    int ustat = find_root(u, parent);
+    int vstat = find_root(v, parent);
+    while (ustat != vstat) {
+        if (ustat < vstat) {
+            int ret = atomicCAS(&parent[vstat], vstat, ustat);
+            if (ret == vstat) break;
+            vstat = find_root(ret, parent);
+        } else {
+            int ret = atomicCAS(&parent[ustat], ustat, vstat);
+            if (ret == ustat) break;
+            ustat = find_root(ret, parent);
+        }
+    }
+}
+
 // one hook per undirected edge: the CSR entries (u, v) with u < v
 __global__ void k_cc_hook(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
                           int64_t nnz, int* parent) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
         const int u = src[e], v = nb[e];
-        if (v < u) continue;
-        int ustat = find_root(u, parent);
-        int vstat = find_root(v, parent);
-        while (ustat != vstat) {
-            // hook the larger root under the smaller one
-            if (ustat < vstat) {
-                int ret = atomicCAS(&parent[vstat], vstat, ustat);
-                if (ret == vstat) break;
-                vstat = find_root(ret, parent);
-            } else {
-                int ret = atomicCAS(&parent[ustat], ustat, vstat);
-                if (ret == ustat) break;
-                ustat = find_root(ret, parent);
-            }
-        }
+        if (v > u) hook(u, v, parent);
+    }
+}
+
+// ---- Afforest-style sampling: hook every vertex to its first CC_SAMPLE
+// neighbours, compress, find the dominant root from a fixed sample, and give
+// the full neighbour lists only to vertices outside that tree.  Any edge with
+// one end outside the dominant tree is still hooked from that end, so the
+// result equals the full union-find whatever tree is chosen.
+
+constexpr int CC_SAMPLE = 2;
+constexpr int CC_VOTES = 1024;
+
+__global__ void k_cc_sample(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
+                            int64_t n, int r, int* parent) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        const int64_t p = row[v] + r;
+        if (p < row[v + 1]) hook(int(v), nb[p], parent);
+    }
+}
+
+__global__ void k_cc_compress(int64_t n, int* parent) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+        parent[v] = find_root(int(v), parent);
+}
+
+// most frequent root among CC_VOTES fixed, spread-out vertices (one block)
+__global__ void __launch_bounds__(CC_VOTES) k_cc_vote(int64_t n, const int* parent, int* giant) {
+    __shared__ int roots[CC_VOTES];
+    __shared__ unsigned long long best;
+    const int t = threadIdx.x;
+    const int64_t v = (int64_t(t) * 2654435761ll + 12345) % n;
+    roots[t] = parent[v];
+    if (t == 0) best = 0;
+    __syncthreads();
+    int cnt = 0;
+    for (int j = 0; j < CC_VOTES; ++j) cnt += roots[j] == roots[t];
+    atomicMax(&best, (unsigned long long)cnt << 32 | unsigned(roots[t]));
+    __syncthreads();
+    if (t == 0) *giant = int(best & 0xffffffffu);
+}
+
+// remaining neighbours (index >= CC_SAMPLE) of vertices outside the dominant tree
+__global__ void k_cc_rest(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
+                          int64_t n, const int* __restrict__ giant_p, int* parent) {
+    const int giant = *giant_p;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        const int64_t b = row[v] + CC_SAMPLE, e = row[v + 1];
+        if (b >= e || find_root(int(v), parent) == giant) continue;
+        for (int64_t p = b; p < e; ++p) hook(int(v), nb[p], parent);
     }
 }
 
@@ -249,8 +306,16 @@ void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32
     int* parent = ctx->wsT<int>(WS_COMP, n);
     ctx->record(0);
     TCB_LAUNCH(ctx, k_cc_init, grid_for(ctx, n, 256), 256, 0, row, nb, n, parent);
-    if (m > 0)
-        TCB_LAUNCH(ctx, k_cc_hook, grid_for(ctx, 2 * m, 256), 256, 0, src, nb, 2 * m, parent);
+    if (m > 0) {
+        (void)src;
+        int* giant = reinterpret_cast<int*>(&C->scratch[11]);
+        for (int r = 0; r < CC_SAMPLE; ++r)
+            TCB_LAUNCH(ctx, k_cc_sample, grid_for(ctx, n, 256), 256, 0, row, nb, n, r, parent);
+        TCB_LAUNCH(ctx, k_cc_compress, grid_for(ctx, n, 256), 256, 0, n, parent);
+        TCB_LAUNCH(ctx, k_cc_vote, 1, CC_VOTES, 0, n, (const int*)parent, giant);
+        TCB_LAUNCH(ctx, k_cc_rest, grid_for(ctx, n, 256), 256, 0, row, nb, n, (const int*)giant,
+                   parent);
+    }
     int32_t* qa = ctx->wsT<int32_t>(WS_QUEUE_A, n);
     int32_t* qb = ctx->wsT<int32_t>(WS_QUEUE_B, n);
     TCB_LAUNCH(ctx, k_bfs_seed, grid_for(ctx, n, 256), 256, 0, row, n, parent, level, qa, C);
