@@ -147,7 +147,7 @@ __global__ void k_bfs_seed(const int64_t* __restrict__ row, int64_t n, int* pare
                            int32_t* __restrict__ level, int32_t* __restrict__ queue,
                            DevCounters* C) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    unsigned long long roots = 0, deg0 = 0;
+    unsigned long long roots = 0, deg0 = 0, dmax0 = 0;
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
         const int64_t v = base + threadIdx.x;
         bool is_root = false, seed = false;
@@ -165,11 +165,15 @@ __global__ void k_bfs_seed(const int64_t* __restrict__ row, int64_t n, int* pare
         if (seed) {
             queue[slot] = int32_t(v);
             deg0 += deg;
+            dmax0 = max(dmax0, (unsigned long long)deg);
         }
     }
     roots = warp_sum(roots);
     deg0 = warp_sum(deg0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax0 = max(dmax0, __shfl_xor_sync(0xffffffffu, dmax0, o));
     if (lane_id() == 0) {
+        if (dmax0) atomicMax(&C->deg_max[0], dmax0);
         if (roots) atomicAdd(&C->components, roots);
         if (deg0) atomicAdd(&C->deg_sum[0], deg0);
     }
@@ -178,27 +182,63 @@ __global__ void k_bfs_seed(const int64_t* __restrict__ row, int64_t n, int* pare
 // ---------------------------------------------------------------------------
 // cooperative multi-source BFS
 
-constexpr int BFS_BLOCK = 256;
+constexpr int BFS_BLOCK = 512;
 constexpr int64_t BFS_ALPHA = 14;  // top-down -> bottom-up when m_f > m_u / ALPHA
 constexpr int64_t BFS_BETA = 24;   // bottom-up -> top-down when n_f < n / BETA
+constexpr int BFS_HEAVY = 256;     // top-down: longer lists are split into chunks
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
     return *(volatile const unsigned long long*)p;
 }
 
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Claim and enqueue the unvisited vertices among nb[p] for p in [b, e)
+// handled by this warp (lanes stride by 32).
+__device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
+                                          const int32_t* __restrict__ nb, int64_t b, int64_t e,
+                                          int32_t* level, int next_level, int32_t* nxt,
+                                          unsigned long long* qlen, unsigned long long& my_deg,
+                                          unsigned long long& my_dmax) {
+    const unsigned lane = lane_id();
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+        const int64_t p = p0 + lane;
+        bool claim = false;
+        int w = 0;
+        if (p < e) {
+            w = nb[p];
+            if (level[w] == -1 && atomicCAS(&level[w], -1, next_level) == -1) claim = true;
+        }
+        unsigned long long slot = warp_append(claim, qlen);
+        if (claim) {
+            nxt[slot] = w;
+            const unsigned long long d = row[w + 1] - row[w];
+            my_deg += d;
+            my_dmax = max(my_dmax, d);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(BFS_BLOCK)
     k_bfs_coop(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
-               int32_t* level, int32_t* qa, int32_t* qb, DevCounters* C, int64_t dir_edges) {
+               int32_t* level, int32_t* qa, int32_t* qb, int2* chunks, DevCounters* C,
+               int64_t dir_edges) {
     cg::grid_group grid = cg::this_grid();
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const int64_t gwarp = gtid >> 5;
     const int64_t nwarps = gthreads >> 5;
     const unsigned lane = lane_id();
+    __shared__ long long s_bc[3];  // per-block broadcast of the level counters
 
     int L = 0;
     int64_t nf = int64_t(ld_volatile_u64(&C->q_len[0]));
     int64_t mf = int64_t(ld_volatile_u64(&C->deg_sum[0]));
+    int64_t dmax = int64_t(ld_volatile_u64(&C->deg_max[0]));
     int64_t mu = dir_edges - mf;  // directed entries of not-yet-visited vertices
     bool td = true;
     int32_t* cur = qa;
@@ -206,32 +246,46 @@ __global__ void __launch_bounds__(BFS_BLOCK)
     int max_level = 0;
 
     while (nf > 0) {
-        const int sn = (L + 1) % 3;
+        const int sc = L % 3, sn = (L + 1) % 3;
         // Slot (L+2)%3 is written by step L+1 (after the next barrier) and was
-        // last read right after barrier L-2, so clear it during this step.
+        // last read right after barrier L-1, so clear it during this step.
         if (gtid == 0) {
-            C->q_len[(L + 2) % 3] = 0;
-            C->deg_sum[(L + 2) % 3] = 0;
+            const int sr = (L + 2) % 3;
+            C->q_len[sr] = 0;
+            C->deg_sum[sr] = 0;
+            C->deg_max[sr] = 0;
+            C->nchunks[sr] = 0;
         }
-        unsigned long long my_deg = 0;
+        unsigned long long my_deg = 0, my_dmax = 0;
         if (td) {
-            // top-down: warp per frontier vertex, lanes stride its neighbour list
+            // top-down: warp per frontier vertex; lists longer than BFS_HEAVY
+            // are cut into chunks that all warps share after a barrier
+            const bool heavy = dmax > BFS_HEAVY;
             for (int64_t i = gwarp; i < nf; i += nwarps) {
                 const int u = cur[i];
                 const int64_t b = row[u], e = row[u + 1];
-                for (int64_t p0 = b; p0 < e; p0 += 32) {
-                    const int64_t p = p0 + lane;
-                    bool claim = false;
-                    int w = 0;
-                    if (p < e) {
-                        w = nb[p];
-                        if (level[w] == -1 && atomicCAS(&level[w], -1, L + 1) == -1) claim = true;
-                    }
-                    unsigned long long slot = warp_append(claim, &C->q_len[sn]);
-                    if (claim) {
-                        nxt[slot] = w;
-                        my_deg += row[w + 1] - row[w];
-                    }
+                if (heavy && e - b > BFS_HEAVY) {
+                    const int nch = int((e - b + BFS_HEAVY - 1) / BFS_HEAVY);
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(&C->nchunks[sc], (unsigned long long)nch);
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    for (int k = lane; k < nch; k += 32)
+                        chunks[base + k] = make_int2(u, k * BFS_HEAVY);
+                    continue;
+                }
+                td_expand(row, nb, b, e, level, L + 1, nxt, &C->q_len[sn], my_deg, my_dmax);
+            }
+            if (heavy) {
+                grid.sync();
+                if (threadIdx.x == 0) s_bc[0] = (long long)ld_volatile_u64(&C->nchunks[sc]);
+                __syncthreads();
+                const int64_t nch = s_bc[0];
+                __syncthreads();
+                for (int64_t c = gwarp; c < nch; c += nwarps) {
+                    const int2 ch = chunks[c];
+                    const int64_t b = row[ch.x] + ch.y;
+                    const int64_t e = min(row[ch.x + 1], b + BFS_HEAVY);
+                    td_expand(row, nb, b, e, level, L + 1, nxt, &C->q_len[sn], my_deg, my_dmax);
                 }
             }
         } else {
@@ -250,6 +304,7 @@ __global__ void __launch_bounds__(BFS_BLOCK)
                     if (found) {
                         level[v] = L + 1;
                         my_deg += e - b;
+                        my_dmax = max(my_dmax, (unsigned long long)(e - b));
                     }
                 }
                 unsigned cnt = __popc(__ballot_sync(0xffffffffu, found));
@@ -257,12 +312,33 @@ __global__ void __launch_bounds__(BFS_BLOCK)
             }
         }
         my_deg = warp_sum(my_deg);
-        if (lane == 0 && my_deg) atomicAdd(&C->deg_sum[sn], my_deg);
+        my_dmax = warp_max_u64(my_dmax);
+        if (lane == 0) {
+            if (my_deg) atomicAdd(&C->deg_sum[sn], my_deg);
+            if (my_dmax) atomicMax(&C->deg_max[sn], my_dmax);
+        }
 
         grid.sync();
 
-        const int64_t nf_next = int64_t(ld_volatile_u64(&C->q_len[sn]));
-        const int64_t mf_next = int64_t(ld_volatile_u64(&C->deg_sum[sn]));
+        if (threadIdx.x == 0) {
+            s_bc[0] = (long long)ld_volatile_u64(&C->q_len[sn]);
+            s_bc[1] = (long long)ld_volatile_u64(&C->deg_sum[sn]);
+            s_bc[2] = (long long)ld_volatile_u64(&C->deg_max[sn]);
+        }
+        __syncthreads();
+        const int64_t nf_next = s_bc[0];
+        const int64_t mf_next = s_bc[1];
+        dmax = s_bc[2];
+        __syncthreads();
+#ifdef TCB_CHECKS
+        if (gtid == 0 && (L < 40 || (L & 255) == 0)) {
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            printf("BFS L=%d mode=%s nf=%lld nf_next=%lld mf_next=%lld dmax=%lld t_ns=%llu\n", L,
+                   td ? "TD" : "BU", (long long)nf, (long long)nf_next, (long long)mf_next,
+                   (long long)dmax, now);
+        }
+#endif
         if (nf_next > 0) max_level = L + 1;
         mu -= mf_next;
         bool next_td;
@@ -329,8 +405,9 @@ void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32
             ctx->bfs_coop_blocks = per_sm * ctx->num_sms;
         }
         int64_t dir_edges = 2 * m;
-        void* args[] = {(void*)&row, (void*)&nb, (void*)&n, (void*)&level,
-                        (void*)&qa,  (void*)&qb, (void*)&C, (void*)&dir_edges};
+        int2* chunks = ctx->wsT<int2>(WS_MISC, 2 * m / BFS_HEAVY + n + 1);
+        void* args[] = {(void*)&row, (void*)&nb,     (void*)&n, (void*)&level,    (void*)&qa,
+                        (void*)&qb,  (void*)&chunks, (void*)&C, (void*)&dir_edges};
         TCB_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_coop, dim3(ctx->bfs_coop_blocks),
                                              dim3(BFS_BLOCK), args, 0, ctx->stream));
         ctx->launches++;

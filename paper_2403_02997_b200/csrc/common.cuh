@@ -70,6 +70,8 @@ struct DevCounters {
     // BFS rotating slots
     unsigned long long q_len[3];
     unsigned long long deg_sum[3];
+    unsigned long long deg_max[3];       // largest degree in the next frontier
+    unsigned long long nchunks[3];       // heavy-vertex chunks queued this level
     unsigned long long scratch[16];
 };
 
