@@ -51,6 +51,7 @@ constexpr int CHUNK = 256;            // stream elements per warp grab (8 per la
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int LONG_LIST = 64;         // warp tier: lists streamed by a whole warp
+constexpr int TINY = 16;              // thread tier: owner degree <= TINY
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t SAME = 0x80000000u;
 
@@ -240,8 +241,10 @@ __global__ void k_split_points(const int64_t* __restrict__ row, const int32_t* _
 __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __restrict__ seg_beg,
                              const int64_t* __restrict__ seg_end, const int* __restrict__ split,
                              int64_t n, longlong4* __restrict__ witems,
-                             longlong4* __restrict__ citems, unsigned long long* nw,
-                             unsigned long long* nc, int shard, int nshards, int wt, int hc) {
+                             longlong4* __restrict__ citems, longlong4* __restrict__ titems,
+                             unsigned long long* nw, unsigned long long* nc,
+                             unsigned long long* nt, int shard, int nshards, int wt, int hc,
+                             int tiny) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += stride) {
         if (nshards > 1 && int(x % nshards) != shard) continue;  // owners shard by id
@@ -249,6 +252,11 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         if (d == 0) continue;
         const int64_t s = seg_beg[x], e = seg_end[x];
         if (e <= s) continue;
+        if (d <= tiny) {  // <= TINY partners, each with <= TINY ids
+            const unsigned long long slot = atomicAdd(nt, 1ull);
+            titems[slot] = make_longlong4(x, s, e, 0);
+            continue;
+        }
         if (d <= wt) {
             const int64_t cnt = (e - s + PW - 1) / PW;
             unsigned long long base = atomicAdd(nw, (unsigned long long)cnt);
@@ -279,6 +287,54 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         TCB_DASSERT(sx[0] == 0 && sx[F] == int(d));
             }
     }
+}
+
+// ---------------------------------------------------------------------------
+// 3b. thread tier: one thread per tiny owner (d(x) <= TINY, so every partner
+//     has <= TINY ids too).  N(x) sits in registers; each partner id is
+//     compared with all of it; the level is gathered only on a hit.
+
+__global__ void __launch_bounds__(256)
+    k_isect_tiny(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
+                 const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
+                 const int32_t* __restrict__ P, const int32_t* __restrict__ level,
+                 DevCounters* C) {
+    const int64_t nitems = int64_t(*nitems_p);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    uint32_t nh = 0, ns = 0, ntie = 0;
+    for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < nitems; it += stride) {
+        const longlong4 item = items[it];
+        const int x = int(item.x);
+        const int64_t xb = row[x];
+        const int xd = int(row[x + 1] - xb);
+        const int lx = level[x];
+        int a[TINY];
+#pragma unroll
+        for (int i = 0; i < TINY; ++i) a[i] = i < xd ? nb[xb + i] : -1;
+        for (int64_t p = item.y; p < item.z; ++p) {
+            const int y = P[p];
+            const int64_t yb = row[y];
+            const int yd = int(row[y + 1] - yb);
+            const int vmax = max(x, y);
+            for (int j = 0; j < yd; ++j) {
+                const int w = nb[yb + j];
+                bool hit = false;
+#pragma unroll
+                for (int i = 0; i < TINY; ++i) hit |= a[i] == w;
+                if (hit) {
+                    const bool same = level[w] == lx;
+                    nh += 1;
+                    ns += same;
+                    ntie += same & (w > vmax);
+                }
+            }
+        }
+    }
+    Tally tl;
+    tl.c1 = nh - ns;
+    tl.c2 = ns;
+    tl.t = nh - ns + ntie;
+    tl.flush(C);
 }
 
 // ---------------------------------------------------------------------------
@@ -585,11 +641,14 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
     const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
     const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
+    const int tiny = min(TINY, wt);
     const int64_t wcap = n + m / PW + 1;
     const int64_t ccap = (2 * m / (wt + 1) + 2 + m / PC) * F;
-    longlong4* items = ctx->wsT<longlong4>(WS_BINS, wcap + ccap);
+    longlong4* items = ctx->wsT<longlong4>(WS_BINS, wcap + ccap + n + 1);
     longlong4* witems = items;
     longlong4* citems = items + wcap;
+    longlong4* titems = citems + ccap;
+    unsigned long long* nt = &C->scratch[9];
     unsigned long long* nw = &C->scratch[5];
     unsigned long long* nc = &C->scratch[6];
     unsigned long long* fw = &C->scratch[7];
@@ -603,8 +662,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, row, src, nb, nnz, rshift,
                split);
     TCB_LAUNCH(ctx, k_make_items, grid_for(ctx, n, 256), 256, 0, row, (const int64_t*)seg,
-               (const int64_t*)(seg + n), (const int*)split, n, witems, citems, nw, nc, shard,
-               nshards, wt, hc);
+               (const int64_t*)(seg + n), (const int*)split, n, witems, citems, titems, nw, nc,
+               nt, shard, nshards, wt, hc, tiny);
 
     IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
@@ -630,6 +689,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     ctx->record(6);
     TCB_LAUNCH(ctx, k_isect_warp, K.warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
                (const unsigned long long*)nw, row, nb, (const int32_t*)P, level, fw, C);
+    TCB_LAUNCH(ctx, k_isect_tiny, ctx->num_sms * 8, 256, 0, (const longlong4*)titems,
+               (const unsigned long long*)nt, row, nb, (const int32_t*)P, level, C);
 }
 
 }  // namespace tcb
