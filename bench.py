@@ -262,14 +262,14 @@ def main():
     H = full.c1 + full.c2
     ncover = full.ncover
     expect = [full.triangles, full.c1, full.c2]
-    # bytes the CTA-tier kernel must move (owners with d > WT = 1024): every
+    # bytes the CTA-tier kernel must move (owners with d > WT = 512): every
     # partner slice streamed once (4 B/id), partner id + 2 offsets per cover
     # edge (20 B), and the owner's list staged once per item (<= 1024 partners)
     cu, cv = full.cover_u.long(), full.cover_v.long()
     own_u = (du > dv) | ((du == dv) & (cu < cv))
     d_own = torch.where(own_u, du, dv)
     owner = torch.where(own_u, cu, cv)
-    cta = d_own > 1024
+    cta = d_own > 512
     W_min_cta = int(torch.minimum(du, dv)[cta].sum().item())
     S_cta = int(cta.sum().item())
     staged = 0

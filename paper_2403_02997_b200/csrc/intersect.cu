@@ -39,15 +39,29 @@
 
 namespace tcb {
 
-constexpr int WT = 1024;              // warp tier: owner degree <= WT
+// Tier thresholds and tile sizes.  The TCB_* macros exist so tools/variants.py
+// can A/B alternatives in one GPU session; the defaults are the measured best.
+#ifndef TCB_WT
+#define TCB_WT 512
+#endif
+#ifndef TCB_HC
+#define TCB_HC 4096
+#endif
+#ifndef TCB_CHUNK
+#define TCB_CHUNK 256
+#endif
+#ifndef TCB_PW
+#define TCB_PW 64
+#endif
+constexpr int WT = TCB_WT;            // warp tier: owner degree <= WT
 constexpr int W_SLOTS = 2 * WT;       // per-warp table: load <= 1/2
 constexpr int W_WARPS = 8;
-constexpr int PW = 64;                // partners per warp item
+constexpr int PW = TCB_PW;            // partners per warp item
 constexpr int C_THREADS = 512;        // 2 CTAs per SM
-constexpr int HC = 4096;              // staged ids per CTA item
+constexpr int HC = TCB_HC;            // staged ids per CTA item
 constexpr int C_SLOTS = 4 * HC;       // load <= 1/4 (64 KB)
 constexpr int PC = 2 * C_THREADS;     // partners per CTA item (2 per thread in the scan)
-constexpr int CHUNK = 256;            // stream elements per warp grab (8 per lane)
+constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (8 per lane)
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int LONG_LIST = 64;         // warp tier: lists streamed by a whole warp
