@@ -127,6 +127,69 @@ struct BucketHash {
     }
 };
 
+#ifndef TCB_CUCKOO
+#define TCB_CUCKOO 1
+#endif
+// 2-choice cuckoo set (A/B knob TCB_CUCKOO): a probe is two LDS.32 and two
+// compares with no loop.  Parallel insertion by atomicExch kick chains; a
+// chain longer than CUCKOO_KICKS reports failure and the caller falls back
+// to the bucket table (load <= 1/4 makes that vanishingly rare).
+constexpr int CUCKOO_KICKS = 64;
+
+struct CuckooHash {
+    uint32_t* tab;
+    int shift;
+    __device__ __forceinline__ void setup(uint32_t* t, int slots) {
+        tab = t;
+        shift = 32 - ceil_log2_dev(slots);
+    }
+    __device__ __forceinline__ unsigned h1(uint32_t k) const { return (k * 0x9E3779B1u) >> shift; }
+    __device__ __forceinline__ unsigned h2(uint32_t k) const {
+        const unsigned a = h1(k), b = (k * 0x7FEB352Du) >> shift;
+        return b == a ? a ^ 1u : b;
+    }
+    __device__ __forceinline__ bool insert(int key, bool same) const {
+        uint32_t e = uint32_t(key) | (same ? SAME : 0u);
+        unsigned pos = h1(uint32_t(key));
+        for (int it = 0; it < CUCKOO_KICKS; ++it) {
+            const uint32_t old = atomicExch(&tab[pos], e);
+            if (old == EMPTY) return true;
+            e = old;  // carry the evicted entry to its other slot
+            const uint32_t k = old & ~SAME;
+            const unsigned a = h1(k);
+            pos = pos == a ? h2(k) : a;
+        }
+        return false;
+    }
+    __device__ __forceinline__ int find(int key) const {
+        const uint32_t k = uint32_t(key);
+        const uint32_t e1 = tab[h1(k)], e2 = tab[h2(k)];
+        const bool m1 = ((e1 ^ k) << 1) == 0u, m2 = ((e2 ^ k) << 1) == 0u;
+        return (m1 | m2) ? 1 + int((m1 ? e1 : e2) >> 31) : 0;
+    }
+};
+
+#ifndef TCB_FILTER
+#define TCB_FILTER 0
+#endif
+// Optional 1-bit filter in front of the bucket table (A/B knob TCB_FILTER):
+// a clear bit settles a miss with one LDS.32 instead of a 16-byte bucket read.
+constexpr int FILT_BITS = 17;
+constexpr int FILT_WORDS = TCB_FILTER ? (1 << FILT_BITS) / 32 : 0;
+
+struct FilteredHash {
+    BucketHash h;
+    const uint32_t* filt;
+    __device__ __forceinline__ static unsigned fbit(int key) {
+        return (unsigned(key) * 0x85EBCA6Bu) >> (32 - FILT_BITS);
+    }
+    __device__ __forceinline__ int find(int key) const {
+        const unsigned b = fbit(key);
+        if (!((filt[b >> 5] >> (b & 31)) & 1u)) return 0;
+        return h.find(key);
+    }
+};
+
 struct Tally {
     unsigned long long c1 = 0, c2 = 0, t = 0;
     // r: 1 = apex on another level, 2 = apex on the owner's level
@@ -413,9 +476,10 @@ __global__ void __launch_bounds__(W_WARPS * 32)
 // s_off (np <= 1024); a chunk that lies inside one slice (the common case:
 // slices average hundreds of ids) takes a warp-uniform fast path with
 // coalesced loads and no per-element partner bookkeeping.
+template <typename Probe>
 __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, const int64_t* s_ys,
                                               const int* s_off, const int* s_vm, int np,
-                                              int* s_next, const BucketHash& h, Tally& tl) {
+                                              int* s_next, const Probe& h, Tally& tl) {
     constexpr int J = CHUNK / 32;
     const int total = s_off[np];
     TCB_DASSERT(np >= 1 && np <= PC && total >= 0);
@@ -531,9 +595,11 @@ __global__ void __launch_bounds__(C_THREADS, 2)
     int* s_off = reinterpret_cast<int*>(s_ys + PC);               // PC + 1
     int* s_vm = s_off + PC + 1;                                   // PC
     int* s_end = s_vm + PC;                                       // PC (sub-chunk cursors)
+    uint32_t* filt = reinterpret_cast<uint32_t*>(s_end + PC);     // FILT_WORDS
     __shared__ int64_t s_tmp[C_THREADS / 32 + 1];
     __shared__ unsigned long long s_item;
     __shared__ int s_next;
+    __shared__ int s_fail;
     const unsigned long long nitems = *nitems_p;
     Tally tl;
     while (true) {
@@ -579,12 +645,25 @@ __global__ void __launch_bounds__(C_THREADS, 2)
             h.setup(tab, slots);
             TCB_DASSERT(slots <= C_SLOTS && np <= PC);
             for (int i = threadIdx.x; i < slots; i += C_THREADS) tab[i] = EMPTY;
+            for (int i = threadIdx.x; i < FILT_WORDS; i += C_THREADS) filt[i] = 0u;
             if (threadIdx.x == 0) s_next = 0;
             __syncthreads();
+            CuckooHash ch;
+            ch.setup(tab, slots);
+            if (TCB_CUCKOO && threadIdx.x == 0) s_fail = 0;
+            if (TCB_CUCKOO) __syncthreads();
             if (!(dbg & 2))
                 for (int i = threadIdx.x; i < len; i += C_THREADS) {
                     const int w = nb[cb + i];
-                    h.insert(w, level[w] == lx);
+                    if (TCB_CUCKOO) {
+                        if (!ch.insert(w, level[w] == lx)) s_fail = 1;
+                    } else {
+                        h.insert(w, level[w] == lx);
+                    }
+                    if (TCB_FILTER) {
+                        const unsigned fb = FilteredHash::fbit(w);
+                        atomicOr(&filt[fb >> 5], 1u << (fb & 31));
+                    }
                 }
             if (single) {
                 for (int t = threadIdx.x; t < np; t += C_THREADS) s_off[t] = s_end[t];
@@ -608,7 +687,25 @@ __global__ void __launch_bounds__(C_THREADS, 2)
                 }
             }
             scan_lengths(s_off, np, s_tmp);  // ends with __syncthreads
-            if (!(dbg & 1)) stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, h, tl);
+            if (TCB_CUCKOO && s_fail) {  // rare: rebuild this sub-chunk as a bucket table
+                for (int i = threadIdx.x; i < slots; i += C_THREADS) tab[i] = EMPTY;
+                __syncthreads();
+                for (int i = threadIdx.x; i < len; i += C_THREADS) {
+                    const int w = nb[cb + i];
+                    h.insert(w, level[w] == lx);
+                }
+                __syncthreads();
+            }
+            if (!(dbg & 1)) {
+                if (TCB_CUCKOO && !s_fail) {
+                    stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, ch, tl);
+                } else if (TCB_FILTER) {
+                    FilteredHash fh{h, filt};
+                    stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, fh, tl);
+                } else {
+                    stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, h, tl);
+                }
+            }
             __syncthreads();
             if (!single) {  // advance partner starts past this sub-chunk
                 for (int t = threadIdx.x; t < np; t += C_THREADS) {
@@ -682,7 +779,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
     const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(PC) * sizeof(int64_t) +
-                       size_t(3 * PC + 1) * sizeof(int);
+                       size_t(3 * PC + 1) * sizeof(int) + size_t(FILT_WORDS) * sizeof(uint32_t);
     if (K.warp_blocks == 0) {
         TCB_CUDA(cudaFuncSetAttribute(k_isect_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(wsm)));
