@@ -48,13 +48,16 @@ namespace tcb {
 #define TCB_HC 4096
 #endif
 #ifndef TCB_CHUNK
-#define TCB_CHUNK 256
+#define TCB_CHUNK 512
 #endif
 #ifndef TCB_PW
 #define TCB_PW 64
 #endif
 constexpr int WT = TCB_WT;            // warp tier: owner degree <= WT
-constexpr int W_SLOTS = 2 * WT;       // per-warp table: load <= 1/2
+#ifndef TCB_WCUCKOO
+#define TCB_WCUCKOO 0
+#endif
+constexpr int W_SLOTS = (TCB_WCUCKOO ? 4 : 2) * WT;  // per-warp table: load <= 1/4 (1/2)
 constexpr int W_WARPS = 8;
 constexpr int PW = TCB_PW;            // partners per warp item
 constexpr int C_THREADS = 512;        // 2 CTAs per SM
@@ -215,8 +218,9 @@ struct Tally {
 // warp tier helpers: one long list with the whole warp (4 loads in flight per
 // lane); a batch of <= 32 lists flattened across lanes.
 
+template <typename Probe>
 __device__ __forceinline__ void probe_long(const int32_t* __restrict__ nb, int64_t s, int d,
-                                           int vmax, const BucketHash& h, Tally& tl) {
+                                           int vmax, const Probe& h, Tally& tl) {
     const int lane = int(lane_id());
     int i = lane;
     for (; i + 96 < d; i += 128) {
@@ -232,8 +236,9 @@ __device__ __forceinline__ void probe_long(const int32_t* __restrict__ nb, int64
     }
 }
 
+template <typename Probe>
 __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int64_t ys, int yd,
-                                            int vmax, const BucketHash& h, Tally& tl) {
+                                            int vmax, const Probe& h, Tally& tl) {
     const unsigned lane = lane_id();
     unsigned longs = __ballot_sync(0xffffffffu, yd >= LONG_LIST);
     while (longs) {
@@ -440,12 +445,28 @@ __global__ void __launch_bounds__(W_WARPS * 32)
         const int64_t xb = row[x];
         const int xd = int(row[x + 1] - xb);
         const int lx = level[x];
-        const int slots = max(16, 2 << ceil_log2_dev(xd));
+        const int slots = max(16, (TCB_WCUCKOO ? 4 : 2) << ceil_log2_dev(xd));
         BucketHash h;
         h.setup(tab, slots);
+        CuckooHash ch;
+        ch.setup(tab, slots);
+        bool ok = true;
         for (int i = lane; i < xd; i += 32) {
             const int w = nb[xb + i];
-            h.insert(w, level[w] == lx);
+            if (TCB_WCUCKOO)
+                ok &= ch.insert(w, level[w] == lx);
+            else
+                h.insert(w, level[w] == lx);
+        }
+        const bool cuckoo = TCB_WCUCKOO && __all_sync(0xffffffffu, ok);
+        if (TCB_WCUCKOO && !cuckoo) {  // rare: rebuild as a bucket table
+            __syncwarp();
+            for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
+            __syncwarp();
+            for (int i = lane; i < xd; i += 32) {
+                const int w = nb[xb + i];
+                h.insert(w, level[w] == lx);
+            }
         }
         __syncwarp();
         for (int64_t pb = item.y; pb < item.z; pb += 32) {
@@ -458,7 +479,10 @@ __global__ void __launch_bounds__(W_WARPS * 32)
                 yd = int(row[y + 1] - ys);
                 vmax = max(x, y);
             }
-            probe_batch(nb, ys, yd, vmax, h, tl);
+            if (cuckoo)
+                probe_batch(nb, ys, yd, vmax, ch, tl);
+            else
+                probe_batch(nb, ys, yd, vmax, h, tl);
         }
         __syncwarp();
         for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
