@@ -166,9 +166,9 @@ TCB_API int tcb_cetc(tcb_context* ctx, const int64_t* d_row_offsets,
 
 /* Multi-GPU shard of the fused path: full labeling and
  * selection on this device's replica; intersection for the owners
- * x with x % nshards == shard.  triangles/c1/c2 are this shard's partials
- * (sum over shards, e.g. one all-reduce); ncover/components/max_level are
- * global. */
+ * x with x % nshards == shard.  c1/c2 are this shard's partials (sum over
+ * shards, e.g. one all-reduce; then T = c1 + c2/3); triangles is -1 when
+ * nshards > 1; ncover/components/max_level are global. */
 TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
                            const int32_t* d_neighbors, const int32_t* d_src,
                            int64_t n, int64_t m, int shard, int nshards,

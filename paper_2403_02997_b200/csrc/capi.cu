@@ -95,14 +95,14 @@ void fill_result(Context* ctx, tcb_result* out, bool partial = false) {
     tcb_result r;
     r.c1 = int64_t(h.c1);
     r.c2 = int64_t(h.c2);
-    r.triangles = int64_t(h.t);
+    // T == c1 + c2/3 over the full cover set (intersect.cu Tally); a shard's
+    // partials carry c1/c2 only and T is formed after they are summed.
+    r.triangles = partial ? -1 : int64_t(h.c1 + h.c2 / 3);
     r.ncover = int64_t(h.ncover);
     r.components = int64_t(h.components);
     r.max_level = h.max_level;
     if (!partial && r.c2 % 3 != 0)  // parallel.py:127-128
         throw Error(TCB_ERR_ASSERT, "same-level apex tally must be divisible by 3");
-    if (!partial && r.triangles != r.c1 + r.c2 / 3)
-        throw Error(TCB_ERR_ASSERT, "T != c1 + c2/3: tie-break tally inconsistent");
     if (out) *out = r;
 }
 

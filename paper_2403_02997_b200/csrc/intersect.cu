@@ -133,40 +133,39 @@ struct BucketHash {
 #ifndef TCB_CUCKOO
 #define TCB_CUCKOO 1
 #endif
-// 2-choice cuckoo set (A/B knob TCB_CUCKOO): a probe is two LDS.32 and two
-// compares with no loop.  Parallel insertion by atomicExch kick chains; a
+// 2-choice cuckoo set over two half tables (A/B knob TCB_CUCKOO): a probe is
+// two LDS.32 and two compares with no loop.  Parallel insertion by atomicExch kick chains; a
 // chain longer than CUCKOO_KICKS reports failure and the caller falls back
 // to the bucket table (load <= 1/4 makes that vanishingly rare).
 constexpr int CUCKOO_KICKS = 64;
 
 struct CuckooHash {
-    uint32_t* tab;
-    int shift;
+    uint32_t* tab;   // table 1: tab[0, half); table 2: tab[half, 2 half)
+    uint32_t* tab2;
+    int shift;       // 32 - log2(half)
     __device__ __forceinline__ void setup(uint32_t* t, int slots) {
         tab = t;
-        shift = 32 - ceil_log2_dev(slots);
+        const int lh = ceil_log2_dev(slots) - 1;
+        tab2 = t + (1 << lh);
+        shift = 32 - lh;
     }
     __device__ __forceinline__ unsigned h1(uint32_t k) const { return (k * 0x9E3779B1u) >> shift; }
-    __device__ __forceinline__ unsigned h2(uint32_t k) const {
-        const unsigned a = h1(k), b = (k * 0x7FEB352Du) >> shift;
-        return b == a ? a ^ 1u : b;
-    }
+    __device__ __forceinline__ unsigned h2(uint32_t k) const { return (k * 0x7FEB352Du) >> shift; }
     __device__ __forceinline__ bool insert(int key, bool same) const {
         uint32_t e = uint32_t(key) | (same ? SAME : 0u);
-        unsigned pos = h1(uint32_t(key));
+        uint32_t* slot = tab + h1(uint32_t(key));
         for (int it = 0; it < CUCKOO_KICKS; ++it) {
-            const uint32_t old = atomicExch(&tab[pos], e);
+            const uint32_t old = atomicExch(slot, e);
             if (old == EMPTY) return true;
-            e = old;  // carry the evicted entry to its other slot
+            e = old;  // carry the evicted entry to its slot in the other table
             const uint32_t k = old & ~SAME;
-            const unsigned a = h1(k);
-            pos = pos == a ? h2(k) : a;
+            slot = slot < tab2 ? tab2 + h2(k) : tab + h1(k);
         }
         return false;
     }
     __device__ __forceinline__ int find(int key) const {
         const uint32_t k = uint32_t(key);
-        const uint32_t e1 = tab[h1(k)], e2 = tab[h2(k)];
+        const uint32_t e1 = tab[h1(k)], e2 = tab2[h2(k)];
         const bool m1 = ((e1 ^ k) << 1) == 0u, m2 = ((e2 ^ k) << 1) == 0u;
         return (m1 | m2) ? 1 + int((m1 ? e1 : e2) >> 31) : 0;
     }
@@ -193,23 +192,23 @@ struct FilteredHash {
     }
 };
 
+// c1/c2 tallies.  T is not tallied: a same-level triangle puts all three of
+// its edges in the cover set and is found once per edge, and the reference's
+// rule (w > max(u, v), _kernels.py:688-692) accepts exactly one of the three,
+// so over the full cover set T == c1 + c2/3 (formed in capi.cu fill_result).
 struct Tally {
-    unsigned long long c1 = 0, c2 = 0, t = 0;
-    // r: 1 = apex on another level, 2 = apex on the owner's level
-    __device__ __forceinline__ void add(int r, int w, int vmax) {
-        const unsigned other = r == 1, same = r == 2;
-        c1 += other;
-        c2 += same;
-        t += other | (same & unsigned(w > vmax));
+    unsigned long long c1 = 0, c2 = 0;
+    // r: 0 = miss, 1 = apex on another level, 2 = apex on the owner's level
+    __device__ __forceinline__ void add(int r) {
+        c1 += r == 1;
+        c2 += r >> 1;
     }
     __device__ __forceinline__ void flush(DevCounters* C) {
         c1 = warp_sum(c1);
         c2 = warp_sum(c2);
-        t = warp_sum(t);
         if (lane_id() == 0) {
             if (c1) atomicAdd(&C->c1, c1);
             if (c2) atomicAdd(&C->c2, c2);
-            if (t) atomicAdd(&C->t, t);
         }
     }
 };
@@ -220,32 +219,32 @@ struct Tally {
 
 template <typename Probe>
 __device__ __forceinline__ void probe_long(const int32_t* __restrict__ nb, int64_t s, int d,
-                                           int vmax, const Probe& h, Tally& tl) {
+                                           const Probe& h, Tally& tl) {
     const int lane = int(lane_id());
     int i = lane;
     for (; i + 96 < d; i += 128) {
         const int w0 = nb[s + i], w1 = nb[s + i + 32], w2 = nb[s + i + 64], w3 = nb[s + i + 96];
-        tl.add(h.find(w0), w0, vmax);
-        tl.add(h.find(w1), w1, vmax);
-        tl.add(h.find(w2), w2, vmax);
-        tl.add(h.find(w3), w3, vmax);
+        tl.add(h.find(w0));
+        tl.add(h.find(w1));
+        tl.add(h.find(w2));
+        tl.add(h.find(w3));
     }
     for (; i < d; i += 32) {
         const int w = nb[s + i];
-        tl.add(h.find(w), w, vmax);
+        tl.add(h.find(w));
     }
 }
 
 template <typename Probe>
 __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int64_t ys, int yd,
-                                            int vmax, const Probe& h, Tally& tl) {
+                                            const Probe& h, Tally& tl) {
     const unsigned lane = lane_id();
     unsigned longs = __ballot_sync(0xffffffffu, yd >= LONG_LIST);
     while (longs) {
         const int k = __ffs(longs) - 1;
         longs &= longs - 1;
-        probe_long(nb, __shfl_sync(0xffffffffu, ys, k), __shfl_sync(0xffffffffu, yd, k),
-                   __shfl_sync(0xffffffffu, vmax, k), h, tl);
+        probe_long(nb, __shfl_sync(0xffffffffu, ys, k), __shfl_sync(0xffffffffu, yd, k), h,
+                   tl);
     }
     if (yd >= LONG_LIST) yd = 0;
     const int incl = warp_inclusive_scan(yd);
@@ -260,11 +259,7 @@ __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int6
         }
         const int64_t ysk = __shfl_sync(0xffffffffu, ys, k);
         const int exk = __shfl_sync(0xffffffffu, incl - yd, k);
-        const int vm = __shfl_sync(0xffffffffu, vmax, k);
-        if (i < total) {
-            const int w = nb[ysk + (i - exk)];
-            tl.add(h.find(w), w, vm);
-        }
+        if (i < total) tl.add(h.find(nb[ysk + (i - exk)]));
     }
 }
 
@@ -383,7 +378,7 @@ __global__ void __launch_bounds__(256)
                  DevCounters* C) {
     const int64_t nitems = int64_t(*nitems_p);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    uint32_t nh = 0, ns = 0, ntie = 0;
+    uint32_t nh = 0, ns = 0;
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < nitems; it += stride) {
         const longlong4 item = items[it];
         const int x = int(item.x);
@@ -397,17 +392,14 @@ __global__ void __launch_bounds__(256)
             const int y = P[p];
             const int64_t yb = row[y];
             const int yd = int(row[y + 1] - yb);
-            const int vmax = max(x, y);
             for (int j = 0; j < yd; ++j) {
                 const int w = nb[yb + j];
                 bool hit = false;
 #pragma unroll
                 for (int i = 0; i < TINY; ++i) hit |= a[i] == w;
                 if (hit) {
-                    const bool same = level[w] == lx;
                     nh += 1;
-                    ns += same;
-                    ntie += same & (w > vmax);
+                    ns += level[w] == lx;
                 }
             }
         }
@@ -415,7 +407,6 @@ __global__ void __launch_bounds__(256)
     Tally tl;
     tl.c1 = nh - ns;
     tl.c2 = ns;
-    tl.t = nh - ns + ntie;
     tl.flush(C);
 }
 
@@ -472,17 +463,16 @@ __global__ void __launch_bounds__(W_WARPS * 32)
         for (int64_t pb = item.y; pb < item.z; pb += 32) {
             const int64_t j = pb + lane;
             int64_t ys = 0;
-            int yd = 0, vmax = 0;
+            int yd = 0;
             if (j < item.z) {
                 const int y = P[j];
                 ys = row[y];
                 yd = int(row[y + 1] - ys);
-                vmax = max(x, y);
             }
             if (cuckoo)
-                probe_batch(nb, ys, yd, vmax, ch, tl);
+                probe_batch(nb, ys, yd, ch, tl);
             else
-                probe_batch(nb, ys, yd, vmax, h, tl);
+                probe_batch(nb, ys, yd, h, tl);
         }
         __syncwarp();
         for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
@@ -502,7 +492,7 @@ __global__ void __launch_bounds__(W_WARPS * 32)
 // coalesced loads and no per-element partner bookkeeping.
 template <typename Probe>
 __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, const int64_t* s_ys,
-                                              const int* s_off, const int* s_vm, int np,
+                                              const int* s_off, int np,
                                               int* s_next, const Probe& h, Tally& tl) {
     constexpr int J = CHUNK / 32;
     const int total = s_off[np];
@@ -525,12 +515,11 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
             k0 = kb * 32 + 31 - __clz(b2);
         }
         TCB_DASSERT(k0 >= 0 && k0 < np);
-        // per-chunk tallies: hits, same-level hits, same-level hits with w > vmax
-        uint32_t nh = 0, ns = 0, nt = 0;
+        // per-chunk tallies: hits, same-level hits
+        uint32_t nh = 0, ns = 0;
         if (s_off[k0 + 1] >= c1) {
             // fast path: one partner slice
             const int32_t* p = nb + (s_ys[k0] - s_off[k0]) + c0 + lane;
-            const int vm = s_vm[k0];
             int w[J];
             if (c1 - c0 == CHUNK) {
 #pragma unroll
@@ -540,7 +529,6 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
                     const int r = h.find(w[j]);
                     nh += r != 0;
                     ns += r >> 1;
-                    nt += (r >> 1) & (w[j] > vm);
                 }
             } else {
 #pragma unroll
@@ -551,7 +539,6 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
                     const int r = h.find(w[j]);
                     nh += r != 0;
                     ns += r >> 1;
-                    nt += (r >> 1) & (w[j] > vm);
                 }
             }
         } else {
@@ -559,8 +546,7 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
             int k = k0;
             int next = s_off[k + 1];
             int64_t base = s_ys[k] - s_off[k];
-            int vm = s_vm[k];
-            int w[J], vmj[J];
+            int w[J];
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int i = c0 + lane + 32 * j;
@@ -571,11 +557,9 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
                         ++k;
                         next = s_off[k + 1];
                         base = s_ys[k] - s_off[k];
-                        vm = s_vm[k];
                     }
                     w[j] = nb[base + i];
                 }
-                vmj[j] = vm;
             }
 #pragma unroll
             for (int j = 0; j < J; ++j) {
@@ -583,12 +567,10 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
                 const int r = h.find(w[j]);
                 nh += r != 0;
                 ns += r >> 1;
-                nt += (r >> 1) & (w[j] > vmj[j]);
             }
         }
         tl.c1 += nh - ns;
         tl.c2 += ns;
-        tl.t += nh - ns + nt;
     }
 }
 
@@ -617,8 +599,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS
     int64_t* s_ys = reinterpret_cast<int64_t*>(tab + C_SLOTS);    // PC
     int* s_off = reinterpret_cast<int*>(s_ys + PC);               // PC + 1
-    int* s_vm = s_off + PC + 1;                                   // PC
-    int* s_end = s_vm + PC;                                       // PC (sub-chunk cursors)
+    int* s_end = s_off + PC + 1;                                  // PC (sub-chunk cursors)
     uint32_t* filt = reinterpret_cast<uint32_t*>(s_end + PC);     // FILT_WORDS
     __shared__ int64_t s_tmp[C_THREADS / 32 + 1];
     __shared__ unsigned long long s_item;
@@ -656,7 +637,6 @@ __global__ void __launch_bounds__(C_THREADS, 2)
             s_ys[t] = yb + a;
             TCB_DASSERT(0 <= a && a <= b && b <= int(row[y + 1] - yb));
             s_end[t] = b - a;  // slice length; consumed below
-            s_vm[t] = max(x, y);
         }
         // stage the owner slice in sub-chunks of hc ids (one pass unless the
         // slice still exceeds hc with every range split — the largest hubs)
@@ -722,12 +702,12 @@ __global__ void __launch_bounds__(C_THREADS, 2)
             }
             if (!(dbg & 1)) {
                 if (TCB_CUCKOO && !s_fail) {
-                    stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, ch, tl);
+                    stream_chunks(nb, s_ys, s_off, np, &s_next, ch, tl);
                 } else if (TCB_FILTER) {
                     FilteredHash fh{h, filt};
-                    stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, fh, tl);
+                    stream_chunks(nb, s_ys, s_off, np, &s_next, fh, tl);
                 } else {
-                    stream_chunks(nb, s_ys, s_off, s_vm, np, &s_next, h, tl);
+                    stream_chunks(nb, s_ys, s_off, np, &s_next, h, tl);
                 }
             }
             __syncthreads();
@@ -803,7 +783,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
     const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(PC) * sizeof(int64_t) +
-                       size_t(3 * PC + 1) * sizeof(int) + size_t(FILT_WORDS) * sizeof(uint32_t);
+                       size_t(2 * PC + 1) * sizeof(int) + size_t(FILT_WORDS) * sizeof(uint32_t);
     if (K.warp_blocks == 0) {
         TCB_CUDA(cudaFuncSetAttribute(k_isect_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(wsm)));

@@ -29,22 +29,26 @@ def shard_of(owner, world: int):
     return owner % world
 
 
-def reduce_counts(t: int, c1: int, c2: int, group=None, device=None):
-    """Sum per-rank (T, c1, c2) partials with one all-reduce.  NCCL needs the
-    tensor on the rank's GPU; gloo takes it on the CPU."""
+def reduce_counts(c1: int, c2: int, group=None, device=None):
+    """Sum per-rank (c1, c2) partials with one all-reduce and form
+    T = c1 + c2/3 (every same-level triangle is found once per cover edge,
+    three times in all; the reference's w > max(u, v) rule keeps one of them).
+    NCCL needs the tensor on the rank's GPU; gloo takes it on the CPU.
+    Returns (T, c1, c2)."""
     import torch
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
-        return int(t), int(c1), int(c2)
-    if device is None:
-        device = (torch.device("cuda", torch.cuda.current_device())
-                  if dist.get_backend(group) == "nccl" else torch.device("cpu"))
-    buf = torch.tensor([t, c1, c2], dtype=torch.int64, device=device)
-    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
-    T, C1, C2 = (int(x) for x in buf.tolist())
+        C1, C2 = int(c1), int(c2)
+    else:
+        if device is None:
+            device = (torch.device("cuda", torch.cuda.current_device())
+                      if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+        buf = torch.tensor([c1, c2], dtype=torch.int64, device=device)
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        C1, C2 = (int(x) for x in buf.tolist())
     if C2 % 3:
-        raise AssertionError("same-level apex tally must be divisible by 3")
-    return T, C1, C2
+        raise AssertionError("same-level apex tally must be divisible by 3")  # parallel.py:127-128
+    return C1 + C2 // 3, C1, C2
 
 
 def tc_cetc_distributed(dg, group=None) -> int:
@@ -57,5 +61,5 @@ def tc_cetc_distributed(dg, group=None) -> int:
         return cetc(dg).triangles
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     r = cetc_shard(dg, rank, world)
-    T, _, _ = reduce_counts(r.triangles, r.c1, r.c2, group=group)
+    T, _, _ = reduce_counts(r.c1, r.c2, group=group)
     return T

@@ -110,7 +110,8 @@ def cetc(dg: DeviceGraph, keep_level: bool = False, keep_cover: bool = False) ->
 def cetc_shard(dg: DeviceGraph, shard: int, nshards: int) -> CetcResult:
     """One rank's share of the fused path: replicated
     labeling/selection, intersection over slice `shard` of `nshards`.
-    triangles/c1/c2 are partials; sum them across shards."""
+    c1/c2 are partials (sum them across shards, then T = c1 + c2/3 —
+    dist.reduce_counts); triangles is -1 when nshards > 1."""
     ctx = _lib.context(dg.device.index)
     r = _lib.TcbResult()
     ctx.check(ctx.lib.tcb_cetc_shard(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),

@@ -61,7 +61,7 @@ def _worker(rank, world, port, out):
         res = {}
         for case in CASES:
             part = _partials(case, rank, world)
-            res[case.name] = (part, tdist.reduce_counts(*part))
+            res[case.name] = (part, tdist.reduce_counts(part[1], part[2]))
         out[rank] = res
     finally:
         dist.destroy_process_group()
@@ -87,7 +87,9 @@ def test_owner_rule():
 
 
 def test_reduce_counts_single_process_passthrough():
-    assert tdist.reduce_counts(7, 4, 9) == (7, 4, 9)
+    assert tdist.reduce_counts(4, 9) == (7, 4, 9)
+    with pytest.raises(AssertionError):
+        tdist.reduce_counts(4, 10)
 
 
 @pytest.mark.gpu
@@ -98,7 +100,8 @@ def test_gpu_shards_sum_to_total(world):
         g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
         dg = tb.device_graph(g)
         parts = [tb.ops.cetc_shard(dg, r, world) for r in range(world)]
-        assert sum(p.triangles for p in parts) == case.T, case.name
+        assert all(p.triangles == -1 for p in parts)  # T is formed after the sum
+        assert sum(p.c1 for p in parts) + sum(p.c2 for p in parts) // 3 == case.T, case.name
         assert sum(p.c1 for p in parts) == case.c1
         assert sum(p.c2 for p in parts) == case.c2
         assert all(p.ncover == len(case.cover) for p in parts)

@@ -1,6 +1,7 @@
 """Build and time library variants (compile-time -D knobs) in one GPU call.
 
     python tools/variants.py build  NAME="-DFOO=1 -DBAR=2" ...   # here
+    python tools/variants.py build-rev REV NAME                  # csrc at a git rev
     python tools/variants.py run CONFIG STEPS NAME...             # on the GPU box
 
 Variants go to paper_2403_02997_b200/lib/variants/ (git-ignored); `run`
@@ -21,12 +22,12 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          f"-I{ROOT / 'include'}"]
 
 
-def build(name: str, defs: str):
+def build(name: str, defs: str, csrc: Path = CSRC):
     obj = ROOT / "paper_2403_02997_b200" / "build" / f"obj_v_{name}"
     obj.mkdir(parents=True, exist_ok=True)
     OUT.mkdir(parents=True, exist_ok=True)
     procs, objs = [], []
-    for src in sorted(CSRC.glob("*.cu")):
+    for src in sorted(csrc.glob("*.cu")):
         o = obj / (src.stem + ".o")
         objs.append(str(o))
         procs.append(subprocess.Popen([NVCC, *FLAGS, *defs.split(), "-c", str(src), "-o", str(o)]))
@@ -50,7 +51,13 @@ def run(config: str, steps: int, names):
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "build":
+    if sys.argv[1] == "build-rev":
+        import tempfile
+        tmp = Path(tempfile.mkdtemp())
+        subprocess.run(f"git -C {ROOT} archive {sys.argv[2]} paper_2403_02997_b200/csrc include"
+                       f" | tar -x -C {tmp}", shell=True, check=True)
+        build(sys.argv[3], "", tmp / "paper_2403_02997_b200" / "csrc")
+    elif sys.argv[1] == "build":
         for spec in sys.argv[2:]:
             name, _, defs = spec.partition("=")
             build(name, defs.strip('"'))
