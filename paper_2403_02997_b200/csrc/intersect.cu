@@ -26,7 +26,7 @@
 //  5. k_isect_cta: one CTA per item; the group's slice of N(x) (<= HC ids,
 //     load <= 1/4) staged; the partners' slices are flattened into one element
 //     stream (block scan of lengths) that warps consume in CHUNK-element
-//     grabs with 8 loads in flight per lane.
+//     grabs (CHUNK / 32 loads in flight per lane).
 //
 // Hash entries carry the apex's level relation to the owner in bit 31
 // (same level -> c2 candidate), so hits need no level gather.  Buckets are 4
@@ -48,7 +48,7 @@ namespace tcb {
 #define TCB_HC 4096
 #endif
 #ifndef TCB_CHUNK
-#define TCB_CHUNK 512
+#define TCB_CHUNK 1024
 #endif
 #ifndef TCB_PW
 #define TCB_PW 64
@@ -64,7 +64,7 @@ constexpr int C_THREADS = 512;        // 2 CTAs per SM
 constexpr int HC = TCB_HC;            // staged ids per CTA item
 constexpr int C_SLOTS = 4 * HC;       // load <= 1/4 (64 KB)
 constexpr int PC = 2 * C_THREADS;     // partners per CTA item (2 per thread in the scan)
-constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (8 per lane)
+constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per lane)
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int LONG_LIST = 64;         // warp tier: lists streamed by a whole warp
@@ -484,6 +484,44 @@ __global__ void __launch_bounds__(W_WARPS * 32)
 // ---------------------------------------------------------------------------
 // 5. CTA tier
 
+// A chunk that crosses slice boundaries: each lane walks forward from the
+// chunk's first partner k0; a lane crosses a boundary in few of its J
+// elements.  FULL: the chunk holds CHUNK elements (no bounds checks).
+template <bool FULL, typename Probe>
+__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ nb, const int64_t* s_ys,
+                                            const int* s_off, int np, int k0, int c0, int c1,
+                                            const Probe& h, uint32_t& nh, uint32_t& ns) {
+    constexpr int J = CHUNK / 32;
+    int k = k0;
+    int next = s_off[k + 1];
+    const int32_t* q = nb + s_ys[k];
+    const int i0 = c0 + int(lane_id());
+    int w[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int i = i0 + 32 * j;
+        w[j] = -1;
+        if (FULL || i < c1) {
+            if (next <= i) {
+                do {
+                    TCB_DASSERT(k + 1 < np);
+                    ++k;
+                    next = s_off[k + 1];
+                } while (next <= i);
+                q = nb + s_ys[k];
+            }
+            w[j] = q[i];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        if (!FULL && w[j] < 0) continue;
+        const int r = h.find(w[j]);
+        nh += r != 0;
+        ns += r >> 1;
+    }
+}
+
 // Warps consume the flattened stream of partner slices in CHUNK grabs;
 // element i belongs to partner k with s_off[k] <= i < s_off[k+1].  The
 // partner of a chunk's first element is found with two 32-way ballots over
@@ -519,7 +557,7 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
         uint32_t nh = 0, ns = 0;
         if (s_off[k0 + 1] >= c1) {
             // fast path: one partner slice
-            const int32_t* p = nb + (s_ys[k0] - s_off[k0]) + c0 + lane;
+            const int32_t* p = nb + s_ys[k0] + c0 + lane;
             int w[J];
             if (c1 - c0 == CHUNK) {
 #pragma unroll
@@ -541,33 +579,10 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
                     ns += r >> 1;
                 }
             }
+        } else if (c1 - c0 == CHUNK) {
+            cross_chunk<true>(nb, s_ys, s_off, np, k0, c0, c1, h, nh, ns);
         } else {
-            // chunk crosses slices: every lane walks forward from k0
-            int k = k0;
-            int next = s_off[k + 1];
-            int64_t base = s_ys[k] - s_off[k];
-            int w[J];
-#pragma unroll
-            for (int j = 0; j < J; ++j) {
-                const int i = c0 + lane + 32 * j;
-                w[j] = -1;
-                if (i < c1) {
-                    while (next <= i) {
-                        TCB_DASSERT(k + 1 < np);
-                        ++k;
-                        next = s_off[k + 1];
-                        base = s_ys[k] - s_off[k];
-                    }
-                    w[j] = nb[base + i];
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < J; ++j) {
-                if (w[j] < 0) continue;
-                const int r = h.find(w[j]);
-                nh += r != 0;
-                ns += r >> 1;
-            }
+            cross_chunk<false>(nb, s_ys, s_off, np, k0, c0, c1, h, nh, ns);
         }
         tl.c1 += nh - ns;
         tl.c2 += ns;
@@ -575,16 +590,23 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
 }
 
 // Exclusive block scan of the per-partner lengths (thread t holds partners
-// 2t, 2t+1) into s_off[0..np]; s_off[np] = stream length.
-__device__ __forceinline__ void scan_lengths(int* s_off, int np, int64_t* s_tmp) {
+// 2t, 2t+1) into s_off[0..np]; s_off[np] = stream length.  s_ys[k] becomes
+// the stream base of partner k: stream element i of its slice is nb[s_ys[k] + i].
+__device__ __forceinline__ void scan_lengths(int* s_off, int64_t* s_ys, int np, int64_t* s_tmp) {
     __syncthreads();  // lengths were written with a different thread->partner map
     const int t = threadIdx.x;
     const int a = 2 * t < np ? s_off[2 * t] : 0;
     const int b = 2 * t + 1 < np ? s_off[2 * t + 1] : 0;
     int64_t tot;
     const int64_t ex = block_exclusive_scan<C_THREADS>(int64_t(a + b), s_tmp, tot);
-    if (2 * t < np) s_off[2 * t] = int(ex);
-    if (2 * t + 1 < np) s_off[2 * t + 1] = int(ex + a);
+    if (2 * t < np) {
+        s_off[2 * t] = int(ex);
+        s_ys[2 * t] -= ex;
+    }
+    if (2 * t + 1 < np) {
+        s_off[2 * t + 1] = int(ex + a);
+        s_ys[2 * t + 1] -= ex + a;
+    }
     if (t == 0) s_off[np] = int(tot);
     __syncthreads();
 }
@@ -690,7 +712,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
                     s_off[t] = int(lo - a);
                 }
             }
-            scan_lengths(s_off, np, s_tmp);  // ends with __syncthreads
+            scan_lengths(s_off, s_ys, np, s_tmp);  // ends with __syncthreads
             if (TCB_CUCKOO && s_fail) {  // rare: rebuild this sub-chunk as a bucket table
                 for (int i = threadIdx.x; i < slots; i += C_THREADS) tab[i] = EMPTY;
                 __syncthreads();
@@ -713,9 +735,8 @@ __global__ void __launch_bounds__(C_THREADS, 2)
             __syncthreads();
             if (!single) {  // advance partner starts past this sub-chunk
                 for (int t = threadIdx.x; t < np; t += C_THREADS) {
-                    const int used = s_off[t + 1] - s_off[t];
-                    s_ys[t] += used;
-                    s_end[t] -= used;
+                    s_ys[t] += s_off[t + 1];  // stream base -> next unread id
+                    s_end[t] -= s_off[t + 1] - s_off[t];
                 }
                 __syncthreads();
             }
