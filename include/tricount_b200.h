@@ -37,7 +37,7 @@ extern "C" {
 
 #define TCB_API __attribute__((visibility("default")))
 
-#define TCB_VERSION 2
+#define TCB_VERSION 3
 
 enum {
     TCB_OK = 0,
@@ -130,11 +130,32 @@ TCB_API int tcb_csr_edges(tcb_context* ctx, const int64_t* d_row_offsets,
 /* ---- BFS levels (_kernels.py:129-157 bfs_levels_k; bfs.py:76-94) ------ */
 /* Levels of a BFS over all components rooted at each component's lowest
  * id (the reference's root rule, _kernels.py:137-142).  d_level int32[n].
- * parent / TREE-vs-STRUT classes are not produced (FIFO-order dependent). */
+ * The FIFO parents are a separate call (tcb_bfs_parent) since the counting
+ * path does not need them. */
 TCB_API int tcb_bfs_levels(tcb_context* ctx, const int64_t* d_row_offsets,
                            const int32_t* d_neighbors, const int32_t* d_src,
                            int64_t n, int64_t m, int32_t* d_level,
                            int64_t* components_out, int64_t* max_level_out);
+
+/* ---- FIFO parents (_kernels.py:143-156; bfs_levels_k's `parent`) ------ */
+/* The parent the reference's FIFO BFS assigns (the first dequeued
+ * neighbour one level up), rebuilt level-synchronously from d_level and
+ * max_level (tcb_bfs_levels outputs).  d_parent_out int32[n], -1 at the
+ * component roots.  Synchronous. */
+TCB_API int tcb_bfs_parent(tcb_context* ctx, const int64_t* d_row_offsets,
+                           const int32_t* d_neighbors, int64_t n,
+                           const int32_t* d_level, int64_t max_level,
+                           int32_t* d_parent_out);
+
+/* ---- edge classes (bfs.py:83-87 in bfs_label) -------------------------- */
+/* Class of each canonical edge (edge_u/edge_v order: u < v, lexicographic)
+ * as int8 EdgeClass: 0 TREE (either endpoint is the other's parent),
+ * 2 HORIZONTAL (equal levels), else 1 STRUT.  d_class_out int8[m].
+ * Synchronous. */
+TCB_API int tcb_edge_classes(tcb_context* ctx, const int64_t* d_row_offsets,
+                             const int32_t* d_neighbors, const int32_t* d_src,
+                             int64_t n, int64_t m, const int32_t* d_level,
+                             const int32_t* d_parent, int8_t* d_class_out);
 
 /* ---- cover edges (bfs.py:97-106 cover_edges) -------------------------- */
 /* Horizontal edges (level[u]==level[v], u<v) in the reference's

@@ -77,6 +77,8 @@ def load_library(path: Path | None = None):
             "tcb_csr_rows": ([vp, vp, i64, vp], i32),
             "tcb_csr_edges": ([vp, vp, vp, i64, i64, vp, vp], i32),
             "tcb_bfs_levels": ([vp, vp, vp, vp, i64, i64, vp, pi64, pi64], i32),
+            "tcb_bfs_parent": ([vp, vp, vp, i64, vp, i64, vp], i32),
+            "tcb_edge_classes": ([vp, vp, vp, vp, i64, i64, vp, vp, vp], i32),
             "tcb_cover_select": ([vp, vp, vp, vp, i64, vp, vp, pi64], i32),
             "tcb_cetc_count": ([vp, vp, vp, vp, i64, vp, vp, i64, i64, pi64], i32),
             "tcb_cetc": ([vp, vp, vp, vp, i64, i64, vp, vp, vp,

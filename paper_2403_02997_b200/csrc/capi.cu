@@ -19,6 +19,10 @@ void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, int64_
                 int32_t*, bool);
 void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
                   int32_t*, int64_t*);
+void bfs_parent(Context*, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t,
+                int32_t*);
+void edge_classes(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
+                  const int32_t*, const int32_t*, int8_t*);
 void cetc_intersect(Context*, const int64_t*, const int32_t*, const int32_t*, const int32_t*,
                     const int32_t*, const int64_t*, int64_t, int64_t, int, int, int64_t);
 void cetc_intersect_owner(Context*, const int64_t*, const int32_t*, const int32_t*,
@@ -235,6 +239,31 @@ TCB_API int tcb_bfs_levels(tcb_context* ctx, const int64_t* d_row_offsets,
         fetch_counters(ctx);
         if (components_out) *components_out = int64_t(ctx->h_counters->components);
         if (max_level_out) *max_level_out = ctx->h_counters->max_level;
+    });
+}
+
+TCB_API int tcb_bfs_parent(tcb_context* ctx, const int64_t* d_row_offsets,
+                           const int32_t* d_neighbors, int64_t n, const int32_t* d_level,
+                           int64_t max_level, int32_t* d_parent_out) {
+    return guarded(ctx, [&] {
+        require(n >= 0, "negative size");
+        require(n == 0 || (d_row_offsets && d_level && d_parent_out), "null array");
+        bfs_parent(ctx, d_row_offsets, d_neighbors, n, d_level, max_level, d_parent_out);
+        sync(ctx);
+    });
+}
+
+TCB_API int tcb_edge_classes(tcb_context* ctx, const int64_t* d_row_offsets,
+                             const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
+                             int64_t m, const int32_t* d_level, const int32_t* d_parent,
+                             int8_t* d_class_out) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        require(m == 0 || (d_neighbors && d_src && d_level && d_parent && d_class_out),
+                "null array");
+        edge_classes(ctx, d_row_offsets, d_neighbors, d_src, n, m, d_level, d_parent,
+                     d_class_out);
+        sync(ctx);
     });
 }
 

@@ -52,6 +52,31 @@ def bfs_levels(dg: DeviceGraph):
     return level[: dg.n], int(comps.value), int(ml.value)
 
 
+def bfs_parent(dg: DeviceGraph, level, max_level: int):
+    """The FIFO parents of bfs_levels_k (_kernels.py:143-156): int32 tensor
+    [n], -1 at component roots (tcb_bfs_parent)."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    parent = torch.empty(max(dg.n, 1), dtype=torch.int32, device=dg.device)
+    ctx.check(ctx.lib.tcb_bfs_parent(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                     dg.n, _lib.ptr(level), int(max_level), _lib.ptr(parent)))
+    return parent[: dg.n]
+
+
+def edge_classes(dg: DeviceGraph, level, parent):
+    """bfs.py:83-87: int8 EdgeClass per canonical edge (tcb_edge_classes)."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    parent = parent.to(device=dg.device, dtype=torch.int32).contiguous()
+    out = torch.empty(max(dg.m, 1), dtype=torch.int8, device=dg.device)
+    ctx.check(ctx.lib.tcb_edge_classes(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                       _lib.ptr(dg.src), dg.n, dg.m, _lib.ptr(level),
+                                       _lib.ptr(parent), _lib.ptr(out)))
+    return out[: dg.m]
+
+
 def cover_select(dg: DeviceGraph, level):
     """bfs.py:97-106 cover_edges: horizontal u<v edges, lexicographic.
     Returns (cover_u, cover_v) int32 tensors."""

@@ -36,6 +36,8 @@ class SmallCase:
         self.eu = data[p + "edge_u"]
         self.ev = data[p + "edge_v"]
         self.level = data[p + "level"]
+        self.parent = data[p + "parent"]
+        self.edge_class = data[p + "edge_class"]
         self.components = int(data[p + "components"])
         self.max_level = int(data[p + "max_level"])
         self.cover = data[p + "cover"]

@@ -42,6 +42,8 @@ def test_labels_cover_counts_match_reference(case):
     lab = tb.bfs_label(g)
     assert lab.level.dtype == np.int64
     assert np.array_equal(lab.level, case.level)
+    assert lab.parent.dtype == np.int64 and np.array_equal(lab.parent, case.parent)
+    assert lab.edge_class.dtype == np.int8 and np.array_equal(lab.edge_class, case.edge_class)
     assert lab.components == case.components
     assert lab.max_level == case.max_level
     cov = tb.cover_edges(lab, g)
@@ -121,6 +123,34 @@ def _check_config(name):
 @pytest.mark.parametrize("name", ["er4096", "rmat16", "lattice2048"])
 def test_config_parity(name):
     _check_config(name)
+
+
+def _check_parent(name):
+    """FIFO parents and edge classes at config scale against the C oracle's
+    FIFO BFS (itself pinned to the reference on the golden cases)."""
+    import torch
+    dg = C.build_device_graph(name)
+    level, _, max_level = tb.ops.bfs_levels(dg)
+    parent = tb.ops.bfs_parent(dg, level, max_level)
+    classes = tb.ops.edge_classes(dg, level, parent)
+    row, nb = dg.row_offsets.cpu().numpy(), dg.neighbors.cpu().numpy()
+    o_level, o_parent, _, _ = oracle.bfs_levels(row, nb, dg.n)
+    assert np.array_equal(level.cpu().numpy(), o_level)
+    assert np.array_equal(parent.cpu().numpy().astype(np.int64), o_parent)
+    eu, ev = (t.cpu().numpy() for t in dg.edge_arrays())
+    assert np.array_equal(classes.cpu().numpy(), oracle.edge_classes(o_level, o_parent, eu, ev))
+    del torch
+
+
+@pytest.mark.parametrize("name", ["er4096", "rmat16", "lattice2048"])
+def test_config_parent_classes(name):
+    _check_parent(name)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["rmat22", "rmat24"])
+def test_config_parent_classes_large(name):
+    _check_parent(name)
 
 
 @pytest.mark.slow

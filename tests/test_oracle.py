@@ -28,6 +28,8 @@ def test_oracle_matches_reference_small(case):
     assert np.array_equal(eu, case.eu) and np.array_equal(ev, case.ev)
     out = oracle.run(case.n, row, nb, eu, ev, threads=2)
     assert np.array_equal(out["level"], case.level)
+    assert np.array_equal(out["parent"], case.parent)
+    assert np.array_equal(out["edge_class"], case.edge_class)
     assert out["components"] == case.components
     assert out["max_level"] == case.max_level
     assert np.array_equal(out["cover"], case.cover)
