@@ -195,6 +195,36 @@ TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
                            int64_t n, int64_t m, int shard, int nshards,
                            tcb_result* out);
 
+/* ---- CETC variants (sequential.py:170-183) ----------------------------- */
+/* Forward triangle count on device (tc_forward_k, _kernels.py:480; the
+ * forward branch of tc_cetc_fe): every edge is intersected once by its
+ * higher-ranked endpoint in (degree desc, id asc) order, which stages only
+ * its neighbours ranked above itself; each triangle is hit exactly once.  T
+ * is orientation-independent, so it equals the reference's id-ordered
+ * forward count. */
+TCB_API int tcb_forward_count(tcb_context* ctx, const int64_t* d_row_offsets,
+                              const int32_t* d_neighbors, const int32_t* d_src,
+                              int64_t n, int64_t m, int64_t* triangles_out);
+
+/* tc_cetc_fe (sequential.py:176-183): BFS levels, covering ratio
+ * |S| / m; below `threshold` (COVER_RATIO_THRESHOLD = 0.7) the cover-edge
+ * count, else the forward count.  out->ncover/components/max_level are
+ * filled either way; c1/c2 are -1 on the forward branch.
+ * *used_forward_out (nullable) = 1 when the forward branch ran. */
+TCB_API int tcb_cetc_fe(tcb_context* ctx, const int64_t* d_row_offsets,
+                        const int32_t* d_neighbors, const int32_t* d_src,
+                        int64_t n, int64_t m, double threshold, tcb_result* out,
+                        int32_t* used_forward_out);
+
+/* degree_order (graph.py:203-213, for CETC-Seq-D / -SD): the graph
+ * relabelled by non-increasing degree, ties by ascending old id, as a new
+ * CSR (d_row_out int64[n+1], d_neighbors_out / d_src_out int32[2m]).
+ * Synchronous. */
+TCB_API int tcb_degree_order(tcb_context* ctx, const int64_t* d_row_offsets,
+                             const int32_t* d_neighbors, const int32_t* d_src,
+                             int64_t n, int64_t m, int64_t* d_row_out,
+                             int32_t* d_neighbors_out, int32_t* d_src_out);
+
 /* Host-buffer entry, the call a binding of cetc_count_k's argument list
  * (row, nb, n; _kernels.py:669) makes: uploads the CSR, derives src, runs
  * the fused path, downloads the result (and levels as int64 when

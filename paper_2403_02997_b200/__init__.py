@@ -1,14 +1,16 @@
 """B200-native cover-edge triangle counting (arXiv 2403.02997).
 
 Drop-in for the reference package ``tricount``'s cover-edge path: the same
-entry points (``normalize``, ``bfs_label``, ``cover_edges``, ``tc_cetc``,
-``tc_cetc_sm``, the ``"CETC-Seq"``/``"CETC-SM"`` registry entries), backed by
+entry points (``normalize``, ``degree_order``, ``bfs_label``, ``cover_edges``,
+``tc_cetc``, ``tc_cetc_sm``, every ``CETC*`` registry entry), backed by
 hand-written sm_100a kernels behind the C ABI in include/tricount_b200.h.
 There is no CPU fallback: compute calls raise without the CUDA library/GPU.
 """
 from .graph import (
     DeviceGraph,
     EdgeList,
+    degree_order,
+    degree_order_device,
     Graph,
     ParseError,
     device_graph,
@@ -28,7 +30,18 @@ from .bfs import (
     enumerate_triangles,
     verify_cover,
 )
-from .sequential import SEQUENTIAL_IDS, count_sequential, tc_cetc
+from .sequential import (
+    COVER_RATIO_THRESHOLD,
+    SEQUENTIAL_IDS,
+    count_sequential,
+    tc_cetc,
+    tc_cetc_degree,
+    tc_cetc_fe,
+    tc_cetc_split,
+    tc_cetc_split_degree,
+    tc_cetc_split_recursive,
+    tc_forward_gpu,
+)
 from .parallel import PARALLEL_IDS, ParallelConfig, tc_cetc_sm, tc_par
 from .ops import CetcResult, cetc, cetc_host, cetc_shard
 from . import ops

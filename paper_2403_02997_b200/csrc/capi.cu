@@ -26,7 +26,11 @@ void edge_classes(Context*, const int64_t*, const int32_t*, const int32_t*, int6
 void cetc_intersect(Context*, const int64_t*, const int32_t*, const int32_t*, const int32_t*,
                     const int32_t*, const int64_t*, int64_t, int64_t, int, int, int64_t);
 void cetc_intersect_owner(Context*, const int64_t*, const int32_t*, const int32_t*,
-                          const int32_t*, int64_t, int64_t, int, int);
+                          const int32_t*, int64_t, int64_t, int, int, int);
+void degree_order(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
+                  int64_t*, int32_t*, int32_t*);
+void count_horizontal(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t,
+                      unsigned long long*);
 void rmat_generate(Context*, int, int64_t, double, double, double, uint64_t, uint64_t, uint64_t,
                    uint64_t, const int64_t*, int64_t*);
 
@@ -89,7 +93,7 @@ void cetc_device(Context* ctx, const int64_t* row, const int32_t* nb, const int3
         ctx->record(4);
         return;
     }
-    cetc_intersect_owner(ctx, row, nb, src, level, n, m, shard, nshards);  // events 3, 5, 6
+    cetc_intersect_owner(ctx, row, nb, src, level, n, m, shard, nshards, 0);  // events 3, 5, 6
     ctx->isect_events = true;
     ctx->record(4);
 }
@@ -313,6 +317,83 @@ TCB_API int tcb_cetc(tcb_context* ctx, const int64_t* d_row_offsets, const int32
         }
         fetch_counters(ctx);
         fill_result(ctx, out);
+    });
+}
+
+// Forward count on device (all edges intersected, owners stage their
+// higher-ranked neighbours; intersect.cu `staged`): T into *triangles_out.
+void forward_device(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
+                    int64_t n, int64_t m, int64_t* triangles_out) {
+    TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
+    if (n > 0 && m > 0) {
+        int32_t* zero = ctx->wsT<int32_t>(WS_LEVEL, n);  // one "level": every edge selected
+        TCB_CUDA(cudaMemsetAsync(zero, 0, sizeof(int32_t) * n, ctx->stream));
+        cetc_intersect_owner(ctx, row, nb, src, zero, n, m, 0, 1, 1);
+    }
+    fetch_counters(ctx);
+    if (ctx->h_counters->c1 != 0)
+        throw Error(TCB_ERR_ASSERT, "forward count: off-level tally must be zero");
+    *triangles_out = int64_t(ctx->h_counters->c2);
+}
+
+TCB_API int tcb_forward_count(tcb_context* ctx, const int64_t* d_row_offsets,
+                              const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
+                              int64_t m, int64_t* triangles_out) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        require(triangles_out != nullptr, "triangles_out is null");
+        forward_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, triangles_out);
+    });
+}
+
+TCB_API int tcb_cetc_fe(tcb_context* ctx, const int64_t* d_row_offsets,
+                        const int32_t* d_neighbors, const int32_t* d_src, int64_t n, int64_t m,
+                        double threshold, tcb_result* out, int32_t* used_forward_out) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
+        TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
+        bfs_levels(ctx, d_row_offsets, d_neighbors, d_src, n, m, level, false);
+        unsigned long long* d_h = &ctx->d_counters->scratch[12];
+        count_horizontal(ctx, d_src, d_neighbors, level, n > 0 ? m : 0, d_h);
+        fetch_counters(ctx);
+        const DevCounters h = *ctx->h_counters;
+        const double ratio = m ? double(h.scratch[12]) / double(m) : 0.0;  // sequential.py:179
+        tcb_result r{};
+        r.ncover = int64_t(h.scratch[12]);
+        r.components = int64_t(h.components);
+        r.max_level = h.max_level;
+        const bool fwd = !(ratio < threshold);
+        if (!fwd) {
+            cetc_intersect_owner(ctx, d_row_offsets, d_neighbors, d_src, level, n, m, 0, 1, 0);
+            fetch_counters(ctx);
+            const DevCounters& c = *ctx->h_counters;
+            if (c.c2 % 3 != 0)  // parallel.py:127-128
+                throw Error(TCB_ERR_ASSERT, "same-level apex tally must be divisible by 3");
+            r.c1 = int64_t(c.c1);
+            r.c2 = int64_t(c.c2);
+            r.triangles = r.c1 + r.c2 / 3;
+        } else {
+            int64_t t = 0;
+            forward_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, &t);
+            r.triangles = t;
+            r.c1 = r.c2 = -1;  // the forward branch has no cover-edge tallies
+        }
+        if (out) *out = r;
+        if (used_forward_out) *used_forward_out = fwd ? 1 : 0;
+    });
+}
+
+TCB_API int tcb_degree_order(tcb_context* ctx, const int64_t* d_row_offsets,
+                             const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
+                             int64_t m, int64_t* d_row_out, int32_t* d_neighbors_out,
+                             int32_t* d_src_out) {
+    return guarded(ctx, [&] {
+        require(n >= 0 && m >= 0, "negative size");
+        require(d_row_out && (m == 0 || (d_neighbors_out && d_src_out)), "null output");
+        degree_order(ctx, d_row_offsets, d_neighbors, d_src, n, m, d_row_out, d_neighbors_out,
+                     d_src_out);
+        sync(ctx);
     });
 }
 

@@ -213,6 +213,19 @@ struct Tally {
     }
 };
 
+// Forward mode (tcb_forward_count, the forward branch of CETC-Seq-FE): every
+// edge is intersected (the caller passes an all-zero level array, so every
+// edge is selected and every hit is "same level"), and an owner stages only
+// the neighbours ranked above it in (degree desc, id asc) order, the order
+// that makes x the owner of (x, y).  A triangle a > b > c in that order is
+// then hit once: at (b, c) with apex a.  T = the same-level tally.
+__device__ __forceinline__ bool staged(const int2* __restrict__ vinfo, int w, int x, int dx,
+                                       int fwd) {
+    if (!fwd) return true;
+    const int dw = vinfo[w].y;
+    return dw > dx || (dw == dx && w < x);
+}
+
 // ---------------------------------------------------------------------------
 // warp tier helpers: one long list with the whole warp (4 loads in flight per
 // lane); a batch of <= 32 lists flattened across lanes.
@@ -375,7 +388,7 @@ __global__ void __launch_bounds__(256)
     k_isect_tiny(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                  const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                  const int32_t* __restrict__ P, const int32_t* __restrict__ level,
-                 DevCounters* C) {
+                 DevCounters* C, const int2* __restrict__ vinfo, int fwd) {
     const int64_t nitems = int64_t(*nitems_p);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     uint32_t nh = 0, ns = 0;
@@ -397,7 +410,7 @@ __global__ void __launch_bounds__(256)
                 bool hit = false;
 #pragma unroll
                 for (int i = 0; i < TINY; ++i) hit |= a[i] == w;
-                if (hit) {
+                if (hit && staged(vinfo, w, x, xd, fwd)) {
                     nh += 1;
                     ns += level[w] == lx;
                 }
@@ -417,7 +430,8 @@ __global__ void __launch_bounds__(W_WARPS * 32)
     k_isect_warp(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                  const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                  const int32_t* __restrict__ P, const int32_t* __restrict__ level,
-                 unsigned long long* fetch, DevCounters* C) {
+                 unsigned long long* fetch, DevCounters* C, const int2* __restrict__ vinfo,
+                 int fwd) {
     extern __shared__ uint4 smem4[];
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
@@ -444,6 +458,7 @@ __global__ void __launch_bounds__(W_WARPS * 32)
         bool ok = true;
         for (int i = lane; i < xd; i += 32) {
             const int w = nb[xb + i];
+            if (!staged(vinfo, w, x, xd, fwd)) continue;
             if (TCB_WCUCKOO)
                 ok &= ch.insert(w, level[w] == lx);
             else
@@ -456,7 +471,7 @@ __global__ void __launch_bounds__(W_WARPS * 32)
             __syncwarp();
             for (int i = lane; i < xd; i += 32) {
                 const int w = nb[xb + i];
-                h.insert(w, level[w] == lx);
+                if (staged(vinfo, w, x, xd, fwd)) h.insert(w, level[w] == lx);
             }
         }
         __syncwarp();
@@ -616,7 +631,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
                 const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                 const int32_t* __restrict__ P, const int32_t* __restrict__ level,
                 const int* __restrict__ split, unsigned long long* fetch, DevCounters* C,
-                int hc, int dbg) {
+                int hc, int dbg, const int2* __restrict__ vinfo, int fwd) {
     extern __shared__ uint4 smem4[];
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS
     int64_t* s_ys = reinterpret_cast<int64_t*>(tab + C_SLOTS);    // PC
@@ -643,6 +658,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
         const int64_t xs = xrow + (lg ? sx[q0] : 0);
         const int64_t xe = lg ? xrow + sx[q1] : row[x + 1];
         const int lx = level[x];
+        const int dx = int(row[x + 1] - xrow);
         const int np = int(item.z - item.y);
         // partner slices for ranges [q0, q1) (the whole list when lg == 0)
         for (int t = threadIdx.x; t < np; t += C_THREADS) {
@@ -681,6 +697,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
             if (!(dbg & 2))
                 for (int i = threadIdx.x; i < len; i += C_THREADS) {
                     const int w = nb[cb + i];
+                    if (!staged(vinfo, w, x, dx, fwd)) continue;
                     if (TCB_CUCKOO) {
                         if (!ch.insert(w, level[w] == lx)) s_fail = 1;
                     } else {
@@ -718,7 +735,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
                 __syncthreads();
                 for (int i = threadIdx.x; i < len; i += C_THREADS) {
                     const int w = nb[cb + i];
-                    h.insert(w, level[w] == lx);
+                    if (staged(vinfo, w, x, dx, fwd)) h.insert(w, level[w] == lx);
                 }
                 __syncthreads();
             }
@@ -766,7 +783,8 @@ struct IsectKernels {
 static IsectKernels g_k[16];
 
 void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
-                          const int32_t* level, int64_t n, int64_t m, int shard, int nshards) {
+                          const int32_t* level, int64_t n, int64_t m, int shard, int nshards,
+                          int fwd) {
     if (n == 0 || m == 0) return;
     DevCounters* C = ctx->d_counters;
     const int64_t nnz = 2 * m;
@@ -821,12 +839,14 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     ctx->record(7);  // no separate hub kernel in this design: hub stage = 0
     TCB_LAUNCH(ctx, k_isect_cta, K.cta_blocks, C_THREADS, csm, (const longlong4*)citems,
                (const unsigned long long*)nc, row, nb, (const int32_t*)P, level,
-               (const int*)split, fc, C, hc, debug_flags());
+               (const int*)split, fc, C, hc, debug_flags(), (const int2*)vinfo, fwd);
     ctx->record(6);
     TCB_LAUNCH(ctx, k_isect_warp, K.warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
-               (const unsigned long long*)nw, row, nb, (const int32_t*)P, level, fw, C);
+               (const unsigned long long*)nw, row, nb, (const int32_t*)P, level, fw, C,
+               (const int2*)vinfo, fwd);
     TCB_LAUNCH(ctx, k_isect_tiny, ctx->num_sms * 8, 256, 0, (const longlong4*)titems,
-               (const unsigned long long*)nt, row, nb, (const int32_t*)P, level, C);
+               (const unsigned long long*)nt, row, nb, (const int32_t*)P, level, C,
+               (const int2*)vinfo, fwd);
 }
 
 }  // namespace tcb

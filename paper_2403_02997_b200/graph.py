@@ -173,6 +173,28 @@ def normalize_device(n: int, pairs) -> DeviceGraph:
     return DeviceGraph(n=n, m=m, row_offsets=row, neighbors=nb[: 2 * m], src=src[: 2 * m])
 
 
+def degree_order_device(dg: DeviceGraph) -> DeviceGraph:
+    """graph.py:203-213 on the GPU (tcb_degree_order): relabel by
+    non-increasing degree, ties by ascending old id."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    row = torch.empty(dg.n + 1, dtype=torch.int64, device=dg.device)
+    nb = torch.empty(max(2 * dg.m, 1), dtype=torch.int32, device=dg.device)
+    src = torch.empty(max(2 * dg.m, 1), dtype=torch.int32, device=dg.device)
+    ctx.check(ctx.lib.tcb_degree_order(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                       _lib.ptr(dg.src), dg.n, dg.m, _lib.ptr(row),
+                                       _lib.ptr(nb), _lib.ptr(src)))
+    return DeviceGraph(n=dg.n, m=dg.m, row_offsets=row, neighbors=nb[: 2 * dg.m],
+                       src=src[: 2 * dg.m])
+
+
+def degree_order(g: Graph) -> Graph:
+    """Relabel vertices by non-increasing degree, ties by ascending old id
+    (graph.py:203-213).  The result is isomorphic to ``g``; vertex 0 has
+    maximal degree."""
+    return degree_order_device(device_graph(g)).to_host()
+
+
 def normalize(el: EdgeList) -> Graph:
     """Canonicalize an EdgeList into a Graph (graph.py:177-194): self-loops
     dropped, duplicates collapsed, both directions stored, rows sorted."""

@@ -132,6 +132,28 @@ def cetc(dg: DeviceGraph, keep_level: bool = False, keep_cover: bool = False) ->
         **d)
 
 
+def forward_count(dg: DeviceGraph) -> int:
+    """Forward triangle count on the GPU (tcb_forward_count; the forward
+    branch of tc_cetc_fe, sequential.py:176-183)."""
+    ctx = _lib.context(dg.device.index)
+    t = ctypes.c_int64(0)
+    ctx.check(ctx.lib.tcb_forward_count(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                        _lib.ptr(dg.src), dg.n, dg.m, ctypes.byref(t)))
+    return int(t.value)
+
+
+def cetc_fe(dg: DeviceGraph, threshold: float = 0.7):
+    """tc_cetc_fe (sequential.py:176-183) fused on the GPU (tcb_cetc_fe).
+    Returns (CetcResult, used_forward); c1/c2 are -1 on the forward branch."""
+    ctx = _lib.context(dg.device.index)
+    r = _lib.TcbResult()
+    fwd = ctypes.c_int32(0)
+    ctx.check(ctx.lib.tcb_cetc_fe(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                  _lib.ptr(dg.src), dg.n, dg.m, float(threshold),
+                                  ctypes.byref(r), ctypes.byref(fwd)))
+    return CetcResult(**r.as_dict()), bool(fwd.value)
+
+
 def cetc_shard(dg: DeviceGraph, shard: int, nshards: int) -> CetcResult:
     """One rank's share of the fused path: replicated
     labeling/selection, intersection over slice `shard` of `nshards`.

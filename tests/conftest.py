@@ -45,6 +45,9 @@ class SmallCase:
         self.T = int(data[p + "T"])
         self.c1 = int(data[p + "c1"])
         self.c2 = int(data[p + "c2"])
+        self.deg_row = data[p + "deg_row_offsets"]
+        self.deg_nb = data[p + "deg_neighbors"]
+        self.fe_forward = bool(data[p + "fe_forward"])
 
     @property
     def m(self):

@@ -6,8 +6,9 @@ Run in the build container (where /root/reference exists):
     NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py configs [names...]
 
 ``small``   -> tests/golden/small_cases.npz: inputs and every hot-path output
-               (CSR, levels, components, max_level, cover set, T, c1, c2) of the
-               reference's own test graphs (tests/conftest.py fixtures, karate,
+               (CSR, levels, parents, edge classes, components, max_level,
+               cover set, T, c1, c2, the degree-ordered CSR, and which branch
+               CETC-Seq-FE takes) of the reference's own test graphs (tests/conftest.py fixtures, karate,
                and the edge cases of test_sequential.py / test_bfs.py).
 ``configs`` -> tests/golden/configs.json: per BASELINE config, sha256 digests
                of the reference's CSR, levels and cover set plus T, c1, c2,
@@ -120,6 +121,10 @@ def make_small():
         c1, c2 = _cetc_sm_counts(g, tc.ParallelConfig(workers=2))
         T = tc.tc_cetc(g)
         assert T == tc.tc_triples(g) == c1 + c2 // 3, name
+        for alg, fn in tc.SEQUENTIAL_IDS.items():  # every CETC id agrees
+            if alg.startswith("CETC"):
+                assert fn(g) == T, (name, alg)
+        gd = tc.degree_order(g)
         p = f"{name}/"
         out[p + "n"] = np.int64(n)
         out[p + "pairs"] = edges
@@ -137,6 +142,10 @@ def make_small():
         out[p + "T"] = np.int64(T)
         out[p + "c1"] = np.int64(c1)
         out[p + "c2"] = np.int64(c2)
+        out[p + "deg_row_offsets"] = gd.row_offsets
+        out[p + "deg_neighbors"] = gd.neighbors
+        ratio = lab.horizontal_count / g.m if g.m else 0.0  # sequential.py:179
+        out[p + "fe_forward"] = np.bool_(not ratio < tc.sequential.COVER_RATIO_THRESHOLD)
         names.append(name)
         print(f"{name}: n={n} m={g.m} T={T} c1={c1} c2={c2} cover={len(cov)}")
     out["_names"] = np.array(names)

@@ -59,6 +59,27 @@ def test_labels_cover_counts_match_reference(case):
 
 
 @pytest.mark.parametrize("case", SMALL_CASES, ids=SMALL_IDS)
+def test_cetc_family_and_forward(case):
+    """Every CETC id of the cetc-family group (bench.py:42-43), the GPU forward
+    count, the FE branch choice (sequential.py:176-183) and degree_order
+    (graph.py:203-213) against the reference's outputs."""
+    g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+    for alg, fn in tb.SEQUENTIAL_IDS.items():
+        assert fn(g) == case.T, alg
+    assert tb.count_sequential("CETC-Seq-FE", g) == case.T
+    assert tb.tc_forward_gpu(g) == case.T
+    r, used_forward = tb.ops.cetc_fe(tb.device_graph(g))
+    assert used_forward == case.fe_forward
+    assert r.triangles == case.T and r.ncover == len(case.cover)
+    if not used_forward:
+        assert (r.c1, r.c2) == (case.c1, case.c2)
+    gd = tb.degree_order(g)
+    assert gd.m == g.m
+    assert np.array_equal(gd.row_offsets, case.deg_row)
+    assert np.array_equal(gd.neighbors, case.deg_nb)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=SMALL_IDS)
 def test_host_buffer_entry(case):
     r = tb.cetc_host(case.row, case.nb, case.n, want_level=True)
     assert (r["triangles"], r["c1"], r["c2"]) == (case.T, case.c1, case.c2)
@@ -140,6 +161,29 @@ def _check_parent(name):
     eu, ev = (t.cpu().numpy() for t in dg.edge_arrays())
     assert np.array_equal(classes.cpu().numpy(), oracle.edge_classes(o_level, o_parent, eu, ev))
     del torch
+
+
+def _check_variants(name):
+    gold = config_goldens()[name]
+    dg = C.build_device_graph(name)
+    assert tb.ops.forward_count(dg) == gold["T"]
+    r, used_forward = tb.ops.cetc_fe(dg)
+    assert r.triangles == gold["T"]
+    assert used_forward == (gold["cover_count"] / dg.m >= tb.COVER_RATIO_THRESHOLD)
+    dd = tb.degree_order_device(dg)
+    rd = tb.cetc(dd)
+    assert rd.triangles == gold["T"] and dd.m == dg.m
+
+
+@pytest.mark.parametrize("name", ["er4096", "rmat16", "lattice2048"])
+def test_config_variants(name):
+    _check_variants(name)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["rmat22", "rmat24"])
+def test_config_variants_large(name):
+    _check_variants(name)
 
 
 @pytest.mark.parametrize("name", ["er4096", "rmat16", "lattice2048"])

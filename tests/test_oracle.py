@@ -35,6 +35,8 @@ def test_oracle_matches_reference_small(case):
     assert np.array_equal(out["cover"], case.cover)
     assert (out["T"], out["c1"], out["c2"]) == (case.T, case.c1, case.c2)
     assert oracle.cetc_count(row, nb, out["level"], case.n) == case.T
+    drow, dnb = oracle.degree_order(case.n, row, eu, ev)
+    assert np.array_equal(drow, case.deg_row) and np.array_equal(dnb, case.deg_nb)
     if case.n <= 80:
         assert oracle.brute_count(case.n, row, nb) == case.T
 
