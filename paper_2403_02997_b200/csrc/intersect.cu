@@ -104,6 +104,12 @@ struct BucketHash {
     // 0 = miss, 1 = hit other level, 2 = hit same level.  The first bucket
     // is resolved without branches; the loop runs only when that bucket is
     // full and does not hold the key (rare at load <= 1/4).
+    // hits: c_other += apex on another level, c_same += apex on the owner's level
+    __device__ __forceinline__ void count(int key, uint32_t& c_other, uint32_t& c_same) const {
+        const int r = find(key);
+        c_other += r == 1;
+        c_same += r >> 1;
+    }
     __device__ __forceinline__ int find(int key) const {
         unsigned b = bucket(key);
         {
@@ -138,19 +144,33 @@ struct BucketHash {
 // chain longer than CUCKOO_KICKS reports failure and the caller falls back
 // to the bucket table (load <= 1/4 makes that vanishingly rare).
 constexpr int CUCKOO_KICKS = 64;
+#ifndef TCB_H1FIRST
+#define TCB_H1FIRST 0
+#endif
+#ifndef TCB_FULLTAB
+#define TCB_FULLTAB 1
+#endif
 
 struct CuckooHash {
     uint32_t* tab;   // table 1: tab[0, half); table 2: tab[half, 2 half)
     uint32_t* tab2;
+    uint32_t a1, a2; // shared-window byte addresses of the two tables
     int shift;       // 32 - log2(half)
     __device__ __forceinline__ void setup(uint32_t* t, int slots) {
         tab = t;
         const int lh = ceil_log2_dev(slots) - 1;
         tab2 = t + (1 << lh);
         shift = 32 - lh;
+        a1 = uint32_t(__cvta_generic_to_shared(tab));
+        a2 = uint32_t(__cvta_generic_to_shared(tab2));
     }
     __device__ __forceinline__ unsigned h1(uint32_t k) const { return (k * 0x9E3779B1u) >> shift; }
     __device__ __forceinline__ unsigned h2(uint32_t k) const { return (k * 0x7FEB352Du) >> shift; }
+    __device__ __forceinline__ static uint32_t lds(uint32_t addr) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+        return v;
+    }
     __device__ __forceinline__ bool insert(int key, bool same) const {
         uint32_t e = uint32_t(key) | (same ? SAME : 0u);
         uint32_t* slot = tab + h1(uint32_t(key));
@@ -168,6 +188,27 @@ struct CuckooHash {
         const uint32_t e1 = tab[h1(k)], e2 = tab2[h2(k)];
         const bool m1 = ((e1 ^ k) << 1) == 0u, m2 = ((e2 ^ k) << 1) == 0u;
         return (m1 | m2) ? 1 + int((m1 ? e1 : e2) >> 31) : 0;
+    }
+    // A key sits in at most one slot, stored as key (other level) or
+    // key | SAME (owner's level): two equality tests per table entry and two
+    // predicated increments.  key >= 0 (EMPTY would match free slots).
+    __device__ __forceinline__ void count(int key, uint32_t& c_other, uint32_t& c_same) const {
+        const uint32_t k = uint32_t(key), ks = k | SAME;
+        const uint32_t e1 = lds(a1 + 4u * h1(k));
+#if TCB_H1FIRST
+        // Slots are never emptied and every insertion starts at h1, so an
+        // empty h1 slot means the key is absent; table 2 is read only by the
+        // lanes whose h1 slot holds another key (inactive lanes put no
+        // requests on the shared-memory banks).
+        uint32_t e2 = EMPTY;
+        const uint32_t need = (e1 != k) & (e1 != ks) & (e1 != EMPTY);
+        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p ld.shared.u32 %0, [%1]; }"
+                     : "+r"(e2) : "r"(a2 + 4u * h2(k)), "r"(need));
+#else
+        const uint32_t e2 = lds(a2 + 4u * h2(k));
+#endif
+        c_other += (e1 == k) | (e2 == k);
+        c_same += (e1 == ks) | (e2 == ks);
     }
 };
 
@@ -190,6 +231,11 @@ struct FilteredHash {
         if (!((filt[b >> 5] >> (b & 31)) & 1u)) return 0;
         return h.find(key);
     }
+    __device__ __forceinline__ void count(int key, uint32_t& c_other, uint32_t& c_same) const {
+        const int r = find(key);
+        c_other += r == 1;
+        c_same += r >> 1;
+    }
 };
 
 // c1/c2 tallies.  T is not tallied: a same-level triangle puts all three of
@@ -198,11 +244,6 @@ struct FilteredHash {
 // so over the full cover set T == c1 + c2/3 (formed in capi.cu fill_result).
 struct Tally {
     unsigned long long c1 = 0, c2 = 0;
-    // r: 0 = miss, 1 = apex on another level, 2 = apex on the owner's level
-    __device__ __forceinline__ void add(int r) {
-        c1 += r == 1;
-        c2 += r >> 1;
-    }
     __device__ __forceinline__ void flush(DevCounters* C) {
         c1 = warp_sum(c1);
         c2 = warp_sum(c2);
@@ -234,18 +275,18 @@ template <typename Probe>
 __device__ __forceinline__ void probe_long(const int32_t* __restrict__ nb, int64_t s, int d,
                                            const Probe& h, Tally& tl) {
     const int lane = int(lane_id());
+    uint32_t co = 0, cs = 0;
     int i = lane;
     for (; i + 96 < d; i += 128) {
         const int w0 = nb[s + i], w1 = nb[s + i + 32], w2 = nb[s + i + 64], w3 = nb[s + i + 96];
-        tl.add(h.find(w0));
-        tl.add(h.find(w1));
-        tl.add(h.find(w2));
-        tl.add(h.find(w3));
+        h.count(w0, co, cs);
+        h.count(w1, co, cs);
+        h.count(w2, co, cs);
+        h.count(w3, co, cs);
     }
-    for (; i < d; i += 32) {
-        const int w = nb[s + i];
-        tl.add(h.find(w));
-    }
+    for (; i < d; i += 32) h.count(nb[s + i], co, cs);
+    tl.c1 += co;
+    tl.c2 += cs;
 }
 
 template <typename Probe>
@@ -272,7 +313,12 @@ __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int6
         }
         const int64_t ysk = __shfl_sync(0xffffffffu, ys, k);
         const int exk = __shfl_sync(0xffffffffu, incl - yd, k);
-        if (i < total) tl.add(h.find(nb[ysk + (i - exk)]));
+        if (i < total) {
+            uint32_t co = 0, cs = 0;
+            h.count(nb[ysk + (i - exk)], co, cs);
+            tl.c1 += co;
+            tl.c2 += cs;
+        }
     }
 }
 
@@ -426,7 +472,7 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------
 // 4. warp tier
 
-__global__ void __launch_bounds__(W_WARPS * 32)
+__global__ void __launch_bounds__(W_WARPS * 32, 4)
     k_isect_warp(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                  const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                  const int32_t* __restrict__ P, const int32_t* __restrict__ level,
@@ -505,7 +551,7 @@ __global__ void __launch_bounds__(W_WARPS * 32)
 template <bool FULL, typename Probe>
 __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ nb, const int64_t* s_ys,
                                             const int* s_off, int np, int k0, int c0, int c1,
-                                            const Probe& h, uint32_t& nh, uint32_t& ns) {
+                                            const Probe& h, uint32_t& co, uint32_t& cs) {
     constexpr int J = CHUNK / 32;
     int k = k0;
     int next = s_off[k + 1];
@@ -531,9 +577,7 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ nb, cons
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         if (!FULL && w[j] < 0) continue;
-        const int r = h.find(w[j]);
-        nh += r != 0;
-        ns += r >> 1;
+        h.count(w[j], co, cs);
     }
 }
 
@@ -568,8 +612,8 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
             k0 = kb * 32 + 31 - __clz(b2);
         }
         TCB_DASSERT(k0 >= 0 && k0 < np);
-        // per-chunk tallies: hits, same-level hits
-        uint32_t nh = 0, ns = 0;
+        // per-chunk tallies: apexes on another level / on the owner's level
+        uint32_t co = 0, cs = 0;
         if (s_off[k0 + 1] >= c1) {
             // fast path: one partner slice
             const int32_t* p = nb + s_ys[k0] + c0 + lane;
@@ -578,29 +622,23 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
 #pragma unroll
                 for (int j = 0; j < J; ++j) w[j] = p[32 * j];
 #pragma unroll
-                for (int j = 0; j < J; ++j) {
-                    const int r = h.find(w[j]);
-                    nh += r != 0;
-                    ns += r >> 1;
-                }
+                for (int j = 0; j < J; ++j) h.count(w[j], co, cs);
             } else {
 #pragma unroll
                 for (int j = 0; j < J; ++j) w[j] = c0 + lane + 32 * j < c1 ? p[32 * j] : -1;
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
                     if (w[j] < 0) continue;
-                    const int r = h.find(w[j]);
-                    nh += r != 0;
-                    ns += r >> 1;
+                    h.count(w[j], co, cs);
                 }
             }
         } else if (c1 - c0 == CHUNK) {
-            cross_chunk<true>(nb, s_ys, s_off, np, k0, c0, c1, h, nh, ns);
+            cross_chunk<true>(nb, s_ys, s_off, np, k0, c0, c1, h, co, cs);
         } else {
-            cross_chunk<false>(nb, s_ys, s_off, np, k0, c0, c1, h, nh, ns);
+            cross_chunk<false>(nb, s_ys, s_off, np, k0, c0, c1, h, co, cs);
         }
-        tl.c1 += nh - ns;
-        tl.c2 += ns;
+        tl.c1 += co;
+        tl.c2 += cs;
     }
 }
 
@@ -626,7 +664,10 @@ __device__ __forceinline__ void scan_lengths(int* s_off, int64_t* s_ys, int np, 
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(C_THREADS, 2)
+#ifndef TCB_CTA_PER_SM
+#define TCB_CTA_PER_SM 2
+#endif
+__global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     k_isect_cta(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                 const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                 const int32_t* __restrict__ P, const int32_t* __restrict__ level,
@@ -682,7 +723,7 @@ __global__ void __launch_bounds__(C_THREADS, 2)
             const int len = int(min(int64_t(hc), xe - cb));
             TCB_DASSERT(len >= 1 && len <= HC && xs >= row[x] && xe <= row[x + 1]);
             const bool single = (cb == xs) && (cb + len >= xe);
-            const int slots = 4 << ceil_log2_dev(max(len, 4));
+            const int slots = TCB_FULLTAB ? C_SLOTS : 4 << ceil_log2_dev(max(len, 4));
             BucketHash h;
             h.setup(tab, slots);
             TCB_DASSERT(slots <= C_SLOTS && np <= PC);
