@@ -154,23 +154,15 @@ constexpr int CUCKOO_KICKS = 64;
 struct CuckooHash {
     uint32_t* tab;   // table 1: tab[0, half); table 2: tab[half, 2 half)
     uint32_t* tab2;
-    uint32_t a1, a2; // shared-window byte addresses of the two tables
     int shift;       // 32 - log2(half)
     __device__ __forceinline__ void setup(uint32_t* t, int slots) {
         tab = t;
         const int lh = ceil_log2_dev(slots) - 1;
         tab2 = t + (1 << lh);
         shift = 32 - lh;
-        a1 = uint32_t(__cvta_generic_to_shared(tab));
-        a2 = uint32_t(__cvta_generic_to_shared(tab2));
     }
     __device__ __forceinline__ unsigned h1(uint32_t k) const { return (k * 0x9E3779B1u) >> shift; }
     __device__ __forceinline__ unsigned h2(uint32_t k) const { return (k * 0x7FEB352Du) >> shift; }
-    __device__ __forceinline__ static uint32_t lds(uint32_t addr) {
-        uint32_t v;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-        return v;
-    }
     __device__ __forceinline__ bool insert(int key, bool same) const {
         uint32_t e = uint32_t(key) | (same ? SAME : 0u);
         uint32_t* slot = tab + h1(uint32_t(key));
@@ -193,19 +185,29 @@ struct CuckooHash {
     // key | SAME (owner's level): two equality tests per table entry and two
     // predicated increments.  key >= 0 (EMPTY would match free slots).
     __device__ __forceinline__ void count(int key, uint32_t& c_other, uint32_t& c_same) const {
+#ifdef TCB_NOPROBE  // measurement-only variant: stream without probing
+        c_other += uint32_t(key) == 0x7FFFFFFEu;
+        return;
+#endif
         const uint32_t k = uint32_t(key), ks = k | SAME;
-        const uint32_t e1 = lds(a1 + 4u * h1(k));
+#ifdef TCB_NOCONFLICT  // measurement-only: same loads at bank-conflict-free addresses
+        {
+            const uint32_t f1 = tab[(h1(k) & ~31u) | (threadIdx.x & 31)];
+            const uint32_t f2 = tab2[(h2(k) & ~31u) | (threadIdx.x & 31)];
+            c_other += (f1 == k) | (f2 == k);
+            c_same += (f1 == ks) | (f2 == ks);
+            return;
+        }
+#endif
+        const uint32_t e1 = tab[h1(k)];
 #if TCB_H1FIRST
         // Slots are never emptied and every insertion starts at h1, so an
         // empty h1 slot means the key is absent; table 2 is read only by the
-        // lanes whose h1 slot holds another key (inactive lanes put no
-        // requests on the shared-memory banks).
+        // lanes whose h1 slot holds another key.
         uint32_t e2 = EMPTY;
-        const uint32_t need = (e1 != k) & (e1 != ks) & (e1 != EMPTY);
-        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p ld.shared.u32 %0, [%1]; }"
-                     : "+r"(e2) : "r"(a2 + 4u * h2(k)), "r"(need));
+        if ((e1 != k) & (e1 != ks) & (e1 != EMPTY)) e2 = tab2[h2(k)];
 #else
-        const uint32_t e2 = lds(a2 + 4u * h2(k));
+        const uint32_t e2 = tab2[h2(k)];
 #endif
         c_other += (e1 == k) | (e2 == k);
         c_same += (e1 == ks) | (e2 == ks);
@@ -571,7 +573,11 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ nb, cons
                 } while (next <= i);
                 q = nb + s_ys[k];
             }
+#ifdef TCB_NOLOAD  // measurement-only variant: probe without streaming
+            w[j] = int((uint32_t(i) * 2654435761u) >> 8) + int(reinterpret_cast<uintptr_t>(q) & 1);
+#else
             w[j] = q[i];
+#endif
         }
     }
 #pragma unroll
@@ -619,8 +625,15 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
             const int32_t* p = nb + s_ys[k0] + c0 + lane;
             int w[J];
             if (c1 - c0 == CHUNK) {
+#ifdef TCB_NOLOAD
+#pragma unroll
+                for (int j = 0; j < J; ++j)
+                    w[j] = int((uint32_t(c0 + lane + 32 * j) * 2654435761u) >> 8) +
+                           int(reinterpret_cast<uintptr_t>(p) & 1);
+#else
 #pragma unroll
                 for (int j = 0; j < J; ++j) w[j] = p[32 * j];
+#endif
 #pragma unroll
                 for (int j = 0; j < J; ++j) h.count(w[j], co, cs);
             } else {
