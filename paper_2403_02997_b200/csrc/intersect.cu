@@ -384,23 +384,33 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
                              unsigned long long* nt, int shard, int nshards, int wt, int hc,
                              int tiny) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    // Multi-GPU (tcb_cetc_shard): partner block i of owner x belongs to
+    // shard (x + i) % nshards (dist.py shard_of mirrors this).  Blocks rather
+    // than whole owners, so a hub's work spreads over the ranks.
+    auto mine = [shard, nshards](int64_t x, int64_t i) {
+        return nshards <= 1 || int((x + i) % nshards) == shard;
+    };
     for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += stride) {
-        if (nshards > 1 && int(x % nshards) != shard) continue;  // owners shard by id
         const int64_t d = row[x + 1] - row[x];
         if (d == 0) continue;
         const int64_t s = seg_beg[x], e = seg_end[x];
         if (e <= s) continue;
         if (d <= tiny) {  // <= TINY partners, each with <= TINY ids
+            if (!mine(x, 0)) continue;
             const unsigned long long slot = atomicAdd(nt, 1ull);
             titems[slot] = make_longlong4(x, s, e, 0);
             continue;
         }
         if (d <= wt) {
             const int64_t cnt = (e - s + PW - 1) / PW;
-            unsigned long long base = atomicAdd(nw, (unsigned long long)cnt);
+            int64_t my = 0;
+            for (int64_t i = 0; i < cnt; ++i) my += mine(x, i);
+            if (my == 0) continue;
+            unsigned long long base = atomicAdd(nw, (unsigned long long)my);
             for (int64_t i = 0; i < cnt; ++i) {
+                if (!mine(x, i)) continue;
                 const int64_t p0 = s + i * PW;
-                witems[base + i] = make_longlong4(x, p0, min(p0 + PW, e), 0);
+                witems[base++] = make_longlong4(x, p0, min(p0 + PW, e), 0);
             }
             continue;
         }
@@ -415,14 +425,18 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
                 if (mx <= hc) break;
             }
         }
+        TCB_DASSERT(sx[0] == 0 && sx[F] == int(d));
         const int G = 1 << lg;
         const int64_t per = (e - s + PC - 1) / PC;
-        unsigned long long base = atomicAdd(nc, (unsigned long long)(per * G));
+        int64_t my = 0;
+        for (int64_t i = 0; i < per; ++i) my += mine(x, i);
+        if (my == 0) continue;
+        unsigned long long base = atomicAdd(nc, (unsigned long long)(my * G));
         for (int g = 0; g < G; ++g)
             for (int64_t i = 0; i < per; ++i) {
+                if (!mine(x, i)) continue;
                 const int64_t p0 = s + i * PC;
-                citems[base + g * per + i] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
-        TCB_DASSERT(sx[0] == 0 && sx[F] == int(d));
+                citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
             }
     }
 }

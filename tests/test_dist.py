@@ -39,7 +39,14 @@ def _partials(case, rank, world):
     if len(cov):
         u, v = cov[:, 0], cov[:, 1]
         own = tdist.owner_of(u, v, deg[u], deg[v])
-        mine = tdist.shard_of(own, world) == rank
+        partner = np.where(own == u, v, u)
+        # rank of each edge among its owner's cover edges, by partner id
+        order = np.lexsort((partner, own))
+        prank = np.empty(len(own), dtype=np.int64)
+        so = own[order]
+        starts = np.searchsorted(so, so, side="left")
+        prank[order] = np.arange(len(so)) - starts
+        mine = tdist.shard_of(own, prank, deg[own], world) == rank
         for a, b in cov[mine]:
             common = np.intersect1d(case.nb[case.row[a]:case.row[a + 1]],
                                     case.nb[case.row[b]:case.row[b + 1]])
@@ -83,7 +90,12 @@ def test_owner_rule():
     u = np.array([1, 5, 3]); v = np.array([2, 4, 9])
     du = np.array([3, 7, 2]); dv = np.array([3, 1, 5])
     assert tdist.owner_of(u, v, du, dv).tolist() == [1, 5, 9]
-    assert tdist.shard_of(np.array([4, 5]), 2).tolist() == [0, 1]
+    # tiny owners shard by id; warp-tier blocks of 64 and CTA-tier blocks of
+    # 1024 partners rotate over the ranks
+    own = np.array([4, 5, 7, 7, 7, 9, 9])
+    prank = np.array([0, 3, 0, 63, 64, 1023, 1024])
+    deg = np.array([8, 10, 100, 100, 100, 4000, 4000])
+    assert tdist.shard_of(own, prank, deg, 2).tolist() == [0, 1, 1, 1, 0, 1, 0]
 
 
 def test_reduce_counts_single_process_passthrough():
@@ -105,3 +117,7 @@ def test_gpu_shards_sum_to_total(world):
         assert sum(p.c1 for p in parts) == case.c1
         assert sum(p.c2 for p in parts) == case.c2
         assert all(p.ncover == len(case.cover) for p in parts)
+        # the device's item sharding is exactly dist.shard_of's rule
+        for r, p in enumerate(parts):
+            _, c1, c2 = _partials(case, r, world)
+            assert (p.c1, p.c2) == (c1, c2), (case.name, r)

@@ -39,3 +39,26 @@ streamed = (cnt * deg).sum().item()
 uniq = deg[cnt > 0].sum().item()
 print(f"  CTA tier: streamed ids {streamed:.4g}, distinct partner ids {uniq:.4g}, "
       f"reuse {streamed / max(uniq, 1):.1f}x, partners {(cnt > 0).sum().item()}")
+
+# multi-GPU balance: probe work per shard under owner sharding (x % N)
+# and under (owner, id-range group, 1024-partner block) item sharding
+ow = torch.where(own_u, u, v)
+for N in (2, 4, 8):
+    per_owner = torch.zeros(dg.n, dtype=torch.float64, device=ow.device)
+    per_owner.index_add_(0, ow, wmin.double())
+    owners = torch.arange(dg.n, device=ow.device)
+    shard_w = torch.zeros(N, dtype=torch.float64, device=ow.device)
+    shard_w.index_add_(0, owners % N, per_owner)
+    print(f"  N={N}: owner sharding  max/mean shard work = "
+          f"{(shard_w.max() / shard_w.mean()).item():.3f}")
+    # finer: each cover edge's block index within its owner (rank of the edge
+    # among the owner's partners // 1024) and range group g in [0, 32)
+    order = torch.argsort(ow, stable=True)
+    ow_s = ow[order]
+    first = torch.searchsorted(ow_s, ow_s, right=False)
+    blk = (torch.arange(len(ow_s), device=ow.device) - first) // 1024
+    wm_s = wmin[order].double()
+    key = (ow_s * 7 + blk) % N
+    sw2 = torch.zeros(N, dtype=torch.float64, device=ow.device)
+    sw2.index_add_(0, key, wm_s)
+    print(f"  N={N}: (owner, block) sharding max/mean = {(sw2.max() / sw2.mean()).item():.3f}")
