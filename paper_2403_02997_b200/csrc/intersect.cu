@@ -327,16 +327,36 @@ __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int6
 // ---------------------------------------------------------------------------
 // 1. owner-grouped selection
 
+// The owner predicate is evaluated once (two random vinfo gathers per
+// entry) into a bitmask, one ballot word per 32 entries; both scan passes
+// then read bits only.
+__global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
+                             const int2* __restrict__ vinfo, int64_t nnz, uint32_t* __restrict__ bits) {
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const unsigned lane = lane_id();
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < nnz;
+         base += gthreads) {
+        const int64_t e = base + lane;
+        bool keep = false;
+        if (e < nnz) {
+            const int x = src[e], y = nb[e];
+            const int2 a = vinfo[x], b = vinfo[y];
+            keep = a.x == b.x && (a.y > b.y || (a.y == b.y && x < y));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) bits[base >> 5] = m;
+    }
+}
+
 void owner_select(Context* ctx, const int64_t* row, const int32_t* src, const int32_t* nb,
                   const int2* vinfo, int64_t nnz, int32_t* P, int64_t* seg_beg, int64_t* seg_end,
                   int64_t* d_ncover) {
+    uint32_t* bits = ctx->wsT<uint32_t>(WS_QUEUE_A, (nnz + 31) / 32);
+    TCB_LAUNCH(ctx, k_owner_bits, grid_for(ctx, nnz, 256), 256, 0, src, nb, vinfo, nnz, bits);
+    const uint32_t* B = bits;
     scan_apply(
         ctx, nnz,
-        [src, nb, vinfo] __device__(int64_t e) -> int64_t {
-            const int x = src[e], y = nb[e];
-            const int2 a = vinfo[x], b = vinfo[y];
-            return (a.x == b.x && (a.y > b.y || (a.y == b.y && x < y))) ? 1 : 0;
-        },
+        [B] __device__(int64_t e) -> int64_t { return (B[e >> 5] >> (e & 31)) & 1u; },
         [src, nb, row, P, seg_beg, seg_end] __device__(int64_t e, int64_t pos, int64_t keep) {
             const int x = src[e];
             if (keep) P[pos] = nb[e];
