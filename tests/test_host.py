@@ -68,8 +68,13 @@ class TestParams:
             tb.tc_par("NOPE", None, tb.ParallelConfig())
 
     def test_registry_names(self):
-        assert "CETC-Seq" in tb.SEQUENTIAL_IDS
-        assert "CETC-SM" in tb.PARALLEL_IDS
+        # the reference's cetc-family group (bench.py:42-43): every id that
+        # starts with "CETC" in SEQUENTIAL_IDS (sequential.py:261-267) and
+        # PARALLEL_IDS (parallel.py:151)
+        assert sorted(tb.SEQUENTIAL_IDS) == sorted([
+            "CETC-Seq", "CETC-Seq-D", "CETC-Seq-FE", "CETC-Seq-S", "CETC-Seq-SD", "CETC-Seq-SR"])
+        assert list(tb.PARALLEL_IDS) == ["CETC-SM"]
+        assert tb.COVER_RATIO_THRESHOLD == 0.7
 
 
 class TestConfigs:
