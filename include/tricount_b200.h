@@ -105,6 +105,21 @@ TCB_API int tcb_rmat_generate(tcb_context* ctx, int scale, int64_t edge_factor,
                               uint64_t inc_hi, uint64_t inc_lo,
                               const int64_t* d_perm, int64_t* d_pairs);
 
+/* The reference's ER fixture recipe (tests/conftest.py:41-47 er_graph):
+ * default_rng(seed).random((n, n)) < p over the strict upper triangle, the
+ * (i, j) pairs in row-major order, bit-identical to numpy's.  (state, inc)
+ * as for tcb_rmat_generate.  d_pairs: int64[2 * n(n-1)/2] capacity;
+ * *k_out = pairs written.  n <= 65536.  Synchronous. */
+TCB_API int tcb_er_generate(tcb_context* ctx, int64_t n, double p,
+                            uint64_t state_hi, uint64_t state_lo,
+                            uint64_t inc_hi, uint64_t inc_lo,
+                            int64_t* d_pairs, int64_t* k_out);
+
+/* The side x side lattice config: ids r*side + c, edges
+ * (r,c)-(r,c+1), (r,c)-(r+1,c), (r,c)-(r+1,c+1), each family row-major.
+ * d_pairs: int64[2 * (2 side (side-1) + (side-1)^2)]. */
+TCB_API int tcb_lattice_generate(tcb_context* ctx, int64_t side, int64_t* d_pairs);
+
 /* ---- graph build (graph.py:177-194 normalize,
  *      graph.py:104-125 _graph_from_canonical_pairs) ------------------ */
 /* Drops self-loops, dedups, symmetrises, sorts adjacency lists.

@@ -73,6 +73,8 @@ def load_library(path: Path | None = None):
             "tcb_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), i32], i32),
             "tcb_rmat_generate": ([vp, i32, i64, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, u64, u64, u64, u64, vp, vp], i32),
+            "tcb_er_generate": ([vp, i64, ctypes.c_double, u64, u64, u64, u64, vp, pi64], i32),
+            "tcb_lattice_generate": ([vp, i64, vp], i32),
             "tcb_csr_build": ([vp, vp, i64, i64, vp, vp, vp, vp, vp, pi64], i32),
             "tcb_csr_rows": ([vp, vp, i64, vp], i32),
             "tcb_csr_edges": ([vp, vp, vp, i64, i64, vp, vp], i32),

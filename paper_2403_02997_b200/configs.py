@@ -13,9 +13,10 @@ with the shapes BASELINE.json names:
                  row-major ids; T = 2*2047^2 in closed form.
 * ``rmat22`` / ``rmat24`` — as rmat16 at scale 22 / 24.
 
-RMAT pairs are produced on the device by ``generate_rmat`` in this package
-(the PCG64 stream numpy's default_rng uses, reproduced bit-exactly); the
-id permutation and the ER draws are produced by numpy on the host.
+RMAT and ER pairs are produced on the device (the PCG64 stream numpy's
+default_rng uses, reproduced bit-exactly: tcb_rmat_generate,
+tcb_er_generate), as are the lattice's (tcb_lattice_generate); only the RMAT
+id permutation (numpy's sequential Fisher-Yates shuffle) comes from the host.
 """
 from __future__ import annotations
 
@@ -72,6 +73,38 @@ def er_pairs(n: int, p: float, seed: int) -> np.ndarray:
     return np.stack([iu[0][sel], iu[1][sel]], axis=1).astype(np.int64)
 
 
+def er_pairs_device(n: int, p: float, seed: int, device=None):
+    """er_pairs on the GPU (tcb_er_generate): torch int64 [k, 2]."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .rmat import _hi_lo, pcg64_seed_state
+    ctx = _lib.context(device)
+    dev = torch.device("cuda", ctx.device)
+    cap = max(1, n * (n - 1) // 2)
+    pairs = torch.empty((cap, 2), dtype=torch.int64, device=dev)
+    st, inc = pcg64_seed_state(seed)
+    k = ctypes.c_int64(0)
+    ctx.check(ctx.lib.tcb_er_generate(ctx.h, n, float(p), *_hi_lo(st), *_hi_lo(inc),
+                                      _lib.ptr(pairs), ctypes.byref(k)))
+    return pairs[: int(k.value)]
+
+
+def lattice_pairs_device(side: int, device=None):
+    """lattice_pairs on the GPU (tcb_lattice_generate): torch int64 [k, 2]."""
+    import torch
+
+    from . import _lib
+    ctx = _lib.context(device)
+    dev = torch.device("cuda", ctx.device)
+    k = 2 * side * (side - 1) + (side - 1) ** 2
+    pairs = torch.empty((max(k, 1), 2), dtype=torch.int64, device=dev)
+    ctx.check(ctx.lib.tcb_lattice_generate(ctx.h, side, _lib.ptr(pairs)))
+    return pairs[:k]
+
+
 def id_permutation(n: int, seed: int) -> np.ndarray:
     """The seeded vertex relabeling applied to RMAT endpoints: new = perm[old]."""
     return np.random.default_rng(seed).permutation(n).astype(np.int64)
@@ -96,9 +129,9 @@ def lattice_closed_form(side: int) -> dict:
 
 
 def build_device_graph(cfg: "Config | str", device=None):
-    """Materialise a config as a DeviceGraph: RMAT pairs generated in HBM
-    (PCG64 replay + id permutation), ER / lattice pairs from numpy, then the
-    device CSR build (tcb_csr_build)."""
+    """Materialise a config as a DeviceGraph: pairs generated in HBM (PCG64
+    replay for RMAT / ER, closed form for the lattice; RMAT ids permuted by
+    the host permutation), then the device CSR build (tcb_csr_build)."""
     import torch
 
     from .graph import normalize_device
@@ -112,9 +145,9 @@ def build_device_graph(cfg: "Config | str", device=None):
         pairs = rmat_pairs_device(RmatParams(scale=cfg.scale, edge_factor=cfg.edge_factor,
                                              seed=cfg.seed), perm=perm, device=dev.index)
     elif cfg.kind == "er":
-        pairs = torch.from_numpy(er_pairs(cfg.n, cfg.p, cfg.seed)).to(dev)
+        pairs = er_pairs_device(cfg.n, cfg.p, cfg.seed, device=dev.index)
     else:
-        pairs = torch.from_numpy(lattice_pairs(cfg.side)).to(dev)
+        pairs = lattice_pairs_device(cfg.side, device=dev.index)
     with torch.cuda.device(dev):
         dg = normalize_device(cfg.n, pairs)
     del pairs

@@ -33,6 +33,9 @@ void count_horizontal(Context*, const int32_t*, const int32_t*, const int32_t*, 
                       unsigned long long*);
 void rmat_generate(Context*, int, int64_t, double, double, double, uint64_t, uint64_t, uint64_t,
                    uint64_t, const int64_t*, int64_t*);
+void er_generate(Context*, int64_t, double, uint64_t, uint64_t, uint64_t, uint64_t, int64_t*,
+                 int64_t*);
+void lattice_generate(Context*, int64_t, int64_t*);
 
 namespace {
 
@@ -205,6 +208,23 @@ TCB_API int tcb_rmat_generate(tcb_context* ctx, int scale, int64_t edge_factor, 
         require(d_pairs != nullptr, "d_pairs is null");
         rmat_generate(ctx, scale, edge_factor, a, b, c, state_hi, state_lo, inc_hi, inc_lo,
                       d_perm, d_pairs);
+    });
+}
+
+TCB_API int tcb_er_generate(tcb_context* ctx, int64_t n, double p, uint64_t state_hi,
+                            uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                            int64_t* d_pairs, int64_t* k_out) {
+    return guarded(ctx, [&] {
+        require(k_out != nullptr, "k_out is null");
+        require(n < 2 || d_pairs, "null output");
+        er_generate(ctx, n, p, state_hi, state_lo, inc_hi, inc_lo, d_pairs, k_out);
+    });
+}
+
+TCB_API int tcb_lattice_generate(tcb_context* ctx, int64_t side, int64_t* d_pairs) {
+    return guarded(ctx, [&] {
+        require(d_pairs != nullptr || side <= 1, "null output");
+        lattice_generate(ctx, side, d_pairs);
     });
 }
 

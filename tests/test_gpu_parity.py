@@ -123,6 +123,19 @@ def test_csr_with_loops_and_duplicates_random():
         assert np.array_equal(g.edge_u, eu) and np.array_equal(g.edge_v, ev)
 
 
+@pytest.mark.parametrize("n,p,seed", [(2, 0.5, 0), (30, 0.25, 3), (48, 0.18, 205),
+                                       (4096, 16 / 4095, 1), (1000, 0.9, 7)])
+def test_device_er_recipe_matches_numpy(n, p, seed):
+    got = C.er_pairs_device(n, p, seed).cpu().numpy()
+    assert np.array_equal(got, C.er_pairs(n, p, seed))
+
+
+@pytest.mark.parametrize("side", [1, 2, 3, 17, 2048])
+def test_device_lattice_matches_host(side):
+    got = C.lattice_pairs_device(side).cpu().numpy()
+    assert np.array_equal(got, C.lattice_pairs(side))
+
+
 def _check_config(name):
     import torch
     gold = config_goldens()[name]
