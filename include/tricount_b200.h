@@ -249,6 +249,13 @@ TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
                           const int32_t* h_neighbors, int64_t n,
                           int64_t* h_level_out, tcb_result* out);
 
+/* The host-buffer entry for one rank of a multi-GPU run (tcb_cetc_shard's
+ * sharding): c1/c2 partials to be summed across ranks; triangles is -1
+ * when nshards > 1. */
+TCB_API int tcb_cetc_host_shard(tcb_context* ctx, const int64_t* h_row_offsets,
+                                const int32_t* h_neighbors, int64_t n,
+                                int shard, int nshards, tcb_result* out);
+
 #ifdef __cplusplus
 }
 #endif

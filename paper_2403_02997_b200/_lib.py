@@ -92,6 +92,7 @@ def load_library(path: Path | None = None):
                              ctypes.POINTER(TcbResult), ctypes.POINTER(ctypes.c_int32)], i32),
             "tcb_degree_order": ([vp, vp, vp, vp, i64, i64, vp, vp, vp], i32),
             "tcb_cetc_host": ([vp, vp, vp, i64, vp, ctypes.POINTER(TcbResult)], i32),
+            "tcb_cetc_host_shard": ([vp, vp, vp, i64, i32, i32, ctypes.POINTER(TcbResult)], i32),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)

@@ -434,11 +434,13 @@ TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
     });
 }
 
-TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
-                          const int32_t* h_neighbors, int64_t n, int64_t* h_level_out,
-                          tcb_result* out) {
+// host-buffer entries: upload the CSR, derive src, run the fused path (or a
+// shard of it), download the counters (and levels on request)
+static int host_entry(tcb_context* ctx, const int64_t* h_row_offsets, const int32_t* h_neighbors,
+                      int64_t n, int64_t* h_level_out, int shard, int nshards, tcb_result* out) {
     return guarded(ctx, [&] {
         require(n >= 0, "negative size");
+        require(nshards >= 1 && shard >= 0 && shard < nshards, "bad shard index");
         require(h_row_offsets != nullptr, "null row offsets");
         const int64_t nnz = h_row_offsets[n];
         require(nnz % 2 == 0, "CSR is not symmetric (odd entry count)");
@@ -455,7 +457,7 @@ TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
         csr_rows(ctx, row, n, src);
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[9], ctx->stream));
         int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
-        cetc_device(ctx, row, nb, src, n, m, level);
+        cetc_device(ctx, row, nb, src, n, m, level, shard, nshards);
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[10], ctx->stream));
         if (h_level_out && n > 0) {
             int64_t* l64 = ctx->wsT<int64_t>(WS_EDGE_V, n);
@@ -467,7 +469,7 @@ TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
                                  cudaMemcpyDeviceToHost, ctx->stream));
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[11], ctx->stream));
         sync(ctx);
-        fill_result(ctx, out);
+        fill_result(ctx, out, /*partial=*/nshards > 1);
         if (n > 0) collect_stage_times(ctx);
         if (ctx->timing) {
             float ms = 0.f;
@@ -477,6 +479,18 @@ TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
             ctx->stage_ms[TCB_STAGE_D2H] = ms;
         }
     });
+}
+
+TCB_API int tcb_cetc_host(tcb_context* ctx, const int64_t* h_row_offsets,
+                          const int32_t* h_neighbors, int64_t n, int64_t* h_level_out,
+                          tcb_result* out) {
+    return host_entry(ctx, h_row_offsets, h_neighbors, n, h_level_out, 0, 1, out);
+}
+
+TCB_API int tcb_cetc_host_shard(tcb_context* ctx, const int64_t* h_row_offsets,
+                                const int32_t* h_neighbors, int64_t n, int shard, int nshards,
+                                tcb_result* out) {
+    return host_entry(ctx, h_row_offsets, h_neighbors, n, nullptr, shard, nshards, out);
 }
 
 }  // extern "C"

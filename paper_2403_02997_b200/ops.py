@@ -187,3 +187,20 @@ def cetc_host(row_offsets: np.ndarray, neighbors: np.ndarray, n: int,
     if level is not None:
         d["level"] = level[:n]
     return d
+
+
+def cetc_host_shard(row_offsets: np.ndarray, neighbors: np.ndarray, n: int, shard: int,
+                    nshards: int, device: int | None = None) -> dict:
+    """One rank's host-buffer entry (tcb_cetc_host_shard): numpy CSR in,
+    c1/c2 partials out (sum them across ranks: dist.reduce_counts)."""
+    ctx = _lib.context(device)
+    row = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    nb = np.ascontiguousarray(neighbors, dtype=np.int32)
+    if len(row) != n + 1:
+        raise ValueError("row_offsets must have n+1 entries")
+    r = _lib.TcbResult()
+    ctx.check(ctx.lib.tcb_cetc_host_shard(
+        ctx.h, row.ctypes.data_as(ctypes.c_void_p),
+        nb.ctypes.data_as(ctypes.c_void_p) if len(nb) else ctypes.c_void_p(0), n,
+        int(shard), int(nshards), ctypes.byref(r)))
+    return r.as_dict()

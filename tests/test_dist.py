@@ -121,3 +121,7 @@ def test_gpu_shards_sum_to_total(world):
         for r, p in enumerate(parts):
             _, c1, c2 = _partials(case, r, world)
             assert (p.c1, p.c2) == (c1, c2), (case.name, r)
+        # the host-buffer entry of each rank gives the same partials
+        for r, p in enumerate(parts):
+            h = tb.ops.cetc_host_shard(case.row, case.nb, case.n, r, world)
+            assert (h["c1"], h["c2"], h["triangles"]) == (p.c1, p.c2, -1 if world > 1 else h["triangles"])
