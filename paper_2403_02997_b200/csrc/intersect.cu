@@ -20,18 +20,20 @@
 //     the entries).  An owner whose list exceeds the table is staged one
 //     group of ranges at a time, and every partner's matching slice is read
 //     from the table — no per-partner searches.
-//  3. make_items: owners with d(x) <= WT -> warp items (x, p0, p1), <= PW
-//     partners each; others -> CTA items (x, p0, p1, group), <= PC partners.
-//  4. k_isect_warp: one warp per item; per-warp hash set of N(x).
-//  5. k_isect_cta: one CTA per item; the group's slice of N(x) (<= HC ids,
-//     load <= 1/4) staged; the partners' slices are flattened into one element
-//     stream (block scan of lengths) that warps consume in CHUNK-element
-//     grabs (CHUNK / 32 loads in flight per lane).
+//  3. make_items: owners with d(x) <= TINY -> thread items; <= WT -> warp
+//     items (x, p0, p1), <= PW partners each; others -> CTA items
+//     (x, p0, p1, group), <= PC partners.  With nshards > 1 only this
+//     shard's partner blocks are listed (dist.py shard_of).
+//  4. k_isect_tiny / k_isect_warp: one thread / warp per item; the warp tier
+//     keeps a per-warp bucket hash of N(x) (4-entry buckets, LDS.128).
+//  5. k_isect_cta: one CTA per item; the group's slice of N(x) (<= HC ids)
+//     staged in a two-table cuckoo set; the partners' slices are flattened
+//     into one element stream (block scan of lengths) that warps consume in
+//     CHUNK-element grabs (CHUNK / 32 loads in flight per lane).
 //
 // Hash entries carry the apex's level relation to the owner in bit 31
-// (same level -> c2 candidate), so hits need no level gather.  Buckets are 4
-// entries (one LDS.128 per probe); linear probing over buckets.  Tallies
-// reduce per warp into one 64-bit atomic each.
+// (same level -> c2), so hits need no level gather.  Tallies reduce per warp
+// into one 64-bit atomic each.
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -54,10 +56,7 @@ namespace tcb {
 #define TCB_PW 64
 #endif
 constexpr int WT = TCB_WT;            // warp tier: owner degree <= WT
-#ifndef TCB_WCUCKOO
-#define TCB_WCUCKOO 0
-#endif
-constexpr int W_SLOTS = (TCB_WCUCKOO ? 4 : 2) * WT;  // per-warp table: load <= 1/4 (1/2)
+constexpr int W_SLOTS = 2 * WT;       // per-warp bucket table: load <= 1/2
 constexpr int W_WARPS = 8;
 constexpr int PW = TCB_PW;            // partners per warp item
 constexpr int C_THREADS = 512;        // 2 CTAs per SM
@@ -144,9 +143,6 @@ struct BucketHash {
 // chain longer than CUCKOO_KICKS reports failure and the caller falls back
 // to the bucket table (load <= 1/4 makes that vanishingly rare).
 constexpr int CUCKOO_KICKS = 64;
-#ifndef TCB_H1FIRST
-#define TCB_H1FIRST 0
-#endif
 #ifndef TCB_FULLTAB
 #define TCB_FULLTAB 1
 #endif
@@ -199,44 +195,9 @@ struct CuckooHash {
             return;
         }
 #endif
-        const uint32_t e1 = tab[h1(k)];
-#if TCB_H1FIRST
-        // Slots are never emptied and every insertion starts at h1, so an
-        // empty h1 slot means the key is absent; table 2 is read only by the
-        // lanes whose h1 slot holds another key.
-        uint32_t e2 = EMPTY;
-        if ((e1 != k) & (e1 != ks) & (e1 != EMPTY)) e2 = tab2[h2(k)];
-#else
-        const uint32_t e2 = tab2[h2(k)];
-#endif
+        const uint32_t e1 = tab[h1(k)], e2 = tab2[h2(k)];
         c_other += (e1 == k) | (e2 == k);
         c_same += (e1 == ks) | (e2 == ks);
-    }
-};
-
-#ifndef TCB_FILTER
-#define TCB_FILTER 0
-#endif
-// Optional 1-bit filter in front of the bucket table (A/B knob TCB_FILTER):
-// a clear bit settles a miss with one LDS.32 instead of a 16-byte bucket read.
-constexpr int FILT_BITS = 17;
-constexpr int FILT_WORDS = TCB_FILTER ? (1 << FILT_BITS) / 32 : 0;
-
-struct FilteredHash {
-    BucketHash h;
-    const uint32_t* filt;
-    __device__ __forceinline__ static unsigned fbit(int key) {
-        return (unsigned(key) * 0x85EBCA6Bu) >> (32 - FILT_BITS);
-    }
-    __device__ __forceinline__ int find(int key) const {
-        const unsigned b = fbit(key);
-        if (!((filt[b >> 5] >> (b & 31)) & 1u)) return 0;
-        return h.find(key);
-    }
-    __device__ __forceinline__ void count(int key, uint32_t& c_other, uint32_t& c_same) const {
-        const int r = find(key);
-        c_other += r == 1;
-        c_same += r >> 1;
     }
 };
 
@@ -532,29 +493,12 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
         const int64_t xb = row[x];
         const int xd = int(row[x + 1] - xb);
         const int lx = level[x];
-        const int slots = max(16, (TCB_WCUCKOO ? 4 : 2) << ceil_log2_dev(xd));
+        const int slots = max(16, 2 << ceil_log2_dev(xd));
         BucketHash h;
         h.setup(tab, slots);
-        CuckooHash ch;
-        ch.setup(tab, slots);
-        bool ok = true;
         for (int i = lane; i < xd; i += 32) {
             const int w = nb[xb + i];
-            if (!staged(vinfo, w, x, xd, fwd)) continue;
-            if (TCB_WCUCKOO)
-                ok &= ch.insert(w, level[w] == lx);
-            else
-                h.insert(w, level[w] == lx);
-        }
-        const bool cuckoo = TCB_WCUCKOO && __all_sync(0xffffffffu, ok);
-        if (TCB_WCUCKOO && !cuckoo) {  // rare: rebuild as a bucket table
-            __syncwarp();
-            for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
-            __syncwarp();
-            for (int i = lane; i < xd; i += 32) {
-                const int w = nb[xb + i];
-                if (staged(vinfo, w, x, xd, fwd)) h.insert(w, level[w] == lx);
-            }
+            if (staged(vinfo, w, x, xd, fwd)) h.insert(w, level[w] == lx);
         }
         __syncwarp();
         for (int64_t pb = item.y; pb < item.z; pb += 32) {
@@ -566,10 +510,7 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
                 ys = row[y];
                 yd = int(row[y + 1] - ys);
             }
-            if (cuckoo)
-                probe_batch(nb, ys, yd, ch, tl);
-            else
-                probe_batch(nb, ys, yd, h, tl);
+            probe_batch(nb, ys, yd, h, tl);
         }
         __syncwarp();
         for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
@@ -725,7 +666,6 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     int64_t* s_ys = reinterpret_cast<int64_t*>(tab + C_SLOTS);    // PC
     int* s_off = reinterpret_cast<int*>(s_ys + PC);               // PC + 1
     int* s_end = s_off + PC + 1;                                  // PC (sub-chunk cursors)
-    uint32_t* filt = reinterpret_cast<uint32_t*>(s_end + PC);     // FILT_WORDS
     __shared__ int64_t s_tmp[C_THREADS / 32 + 1];
     __shared__ unsigned long long s_item;
     __shared__ int s_next;
@@ -775,7 +715,6 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
             h.setup(tab, slots);
             TCB_DASSERT(slots <= C_SLOTS && np <= PC);
             for (int i = threadIdx.x; i < slots; i += C_THREADS) tab[i] = EMPTY;
-            for (int i = threadIdx.x; i < FILT_WORDS; i += C_THREADS) filt[i] = 0u;
             if (threadIdx.x == 0) s_next = 0;
             __syncthreads();
             CuckooHash ch;
@@ -790,10 +729,6 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         if (!ch.insert(w, level[w] == lx)) s_fail = 1;
                     } else {
                         h.insert(w, level[w] == lx);
-                    }
-                    if (TCB_FILTER) {
-                        const unsigned fb = FilteredHash::fbit(w);
-                        atomicOr(&filt[fb >> 5], 1u << (fb & 31));
                     }
                 }
             if (single) {
@@ -830,9 +765,6 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
             if (!(dbg & 1)) {
                 if (TCB_CUCKOO && !s_fail) {
                     stream_chunks(nb, s_ys, s_off, np, &s_next, ch, tl);
-                } else if (TCB_FILTER) {
-                    FilteredHash fh{h, filt};
-                    stream_chunks(nb, s_ys, s_off, np, &s_next, fh, tl);
                 } else {
                     stream_chunks(nb, s_ys, s_off, np, &s_next, h, tl);
                 }
@@ -910,7 +842,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
     const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(PC) * sizeof(int64_t) +
-                       size_t(2 * PC + 1) * sizeof(int) + size_t(FILT_WORDS) * sizeof(uint32_t);
+                       size_t(2 * PC + 1) * sizeof(int);
     if (K.warp_blocks == 0) {
         TCB_CUDA(cudaFuncSetAttribute(k_isect_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(wsm)));
