@@ -186,6 +186,10 @@ constexpr int BFS_BLOCK = 512;
 constexpr int64_t BFS_ALPHA = 14;  // top-down -> bottom-up when m_f > m_u / ALPHA
 constexpr int64_t BFS_BETA = 24;   // bottom-up -> top-down when n_f < n / BETA
 constexpr int BFS_HEAVY = 256;     // top-down: longer lists are split into chunks
+#ifndef TCB_BFS_LOWDEG
+#define TCB_BFS_LOWDEG 64
+#endif
+constexpr int64_t BFS_LOWDEG = TCB_BFS_LOWDEG;  // td_expand<true> when dmax <= this
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
     return *(volatile const unsigned long long*)p;
@@ -198,7 +202,12 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 }
 
 // Claim and enqueue the unvisited vertices among nb[p] for p in [b, e)
-// handled by this warp (lanes stride by 32).
+// handled by this warp (lanes stride by 32).  LOWDEG (every frontier degree
+// <= BFS_LOWDEG, uniform per level): claim with a bare CAS and load the
+// neighbour's degree alongside it, two fewer dependent round trips per level
+// on high-diameter low-degree graphs; otherwise test before the CAS, so hub
+// levels do not hammer already-visited vertices with atomics.
+template <bool LOWDEG>
 __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
                                           const int32_t* __restrict__ nb, int64_t b, int64_t e,
                                           int32_t* level, int next_level, int32_t* nxt,
@@ -209,14 +218,20 @@ __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
         const int64_t p = p0 + lane;
         bool claim = false;
         int w = 0;
+        unsigned long long d = 0;
         if (p < e) {
             w = nb[p];
-            if (level[w] == -1 && atomicCAS(&level[w], -1, next_level) == -1) claim = true;
+            if (LOWDEG) {
+                d = row[w + 1] - row[w];
+                claim = atomicCAS(&level[w], -1, next_level) == -1;
+            } else if (level[w] == -1 && atomicCAS(&level[w], -1, next_level) == -1) {
+                claim = true;
+                d = row[w + 1] - row[w];
+            }
         }
         unsigned long long slot = warp_append(claim, qlen);
         if (claim) {
             nxt[slot] = w;
-            const unsigned long long d = row[w + 1] - row[w];
             my_deg += d;
             my_dmax = max(my_dmax, d);
         }
@@ -273,7 +288,12 @@ __global__ void __launch_bounds__(BFS_BLOCK)
                         chunks[base + k] = make_int2(u, k * BFS_HEAVY);
                     continue;
                 }
-                td_expand(row, nb, b, e, level, L + 1, nxt, &C->q_len[sn], my_deg, my_dmax);
+                if (dmax <= BFS_LOWDEG)
+                    td_expand<true>(row, nb, b, e, level, L + 1, nxt, &C->q_len[sn], my_deg,
+                                    my_dmax);
+                else
+                    td_expand<false>(row, nb, b, e, level, L + 1, nxt, &C->q_len[sn], my_deg,
+                                     my_dmax);
             }
             if (heavy) {
                 grid.sync();
@@ -285,7 +305,8 @@ __global__ void __launch_bounds__(BFS_BLOCK)
                     const int2 ch = chunks[c];
                     const int64_t b = row[ch.x] + ch.y;
                     const int64_t e = min(row[ch.x + 1], b + BFS_HEAVY);
-                    td_expand(row, nb, b, e, level, L + 1, nxt, &C->q_len[sn], my_deg, my_dmax);
+                    td_expand<false>(row, nb, b, e, level, L + 1, nxt, &C->q_len[sn], my_deg,
+                                     my_dmax);
                 }
             }
         } else {
