@@ -354,9 +354,10 @@ void forward_device(Context* ctx, const int64_t* row, const int32_t* nb, const i
         cetc_intersect_owner(ctx, row, nb, src, zero, n, m, 0, 1, 1);
     }
     fetch_counters(ctx);
-    if (ctx->h_counters->c1 != 0)
-        throw Error(TCB_ERR_ASSERT, "forward count: off-level tally must be zero");
-    *triangles_out = int64_t(ctx->h_counters->c2);
+    // forward mode classes every entry OFF: each hit is a triangle, in c1
+    if (ctx->h_counters->c2 != 0)
+        throw Error(TCB_ERR_ASSERT, "forward count: same-level tally must be zero");
+    *triangles_out = int64_t(ctx->h_counters->c1);
 }
 
 TCB_API int tcb_forward_count(tcb_context* ctx, const int64_t* d_row_offsets,

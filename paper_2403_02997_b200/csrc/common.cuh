@@ -57,6 +57,9 @@ enum Slot : int {
     WS_COUNT_TMP,     // per-vertex counts / misc int64[n+1]
     WS_BINS,          // intersection work bins
     WS_MISC,
+    WS_LISTS,         // intersection: off-level / upper same-level neighbour lists int32[2m]
+    WS_CLASS,         // intersection: per-32-entry class bits + word prefixes
+    WS_VBEG,          // intersection: per-vertex list starts int64[2(n+1)]
     WS_NSLOTS
 };
 

@@ -10,30 +10,47 @@
 // element steps (2.4e12 at RMAT-24).  Here each horizontal edge is owned by
 // its higher-degree endpoint x (ties: lower id).  x's list is staged in a
 // shared-memory hash set and every partner y's list (the shorter one) is
-// streamed past it: sum_S min(d(u), d(v)) probes (10x fewer at RMAT-24).
+// streamed past it, so an edge costs at most min(d(u), d(v)) probes.
+//
+// The level rule is applied before the intersection instead of after it.
+// Both endpoints are on level L, so an apex w is on another level from both
+// (counted in c1) or on L for both; a same-level apex counts for T only when
+// w > max(u, v) (_kernels.py:687), i.e. w > x and w > y.  Every CSR row is
+// therefore split into two id-sorted lists:
+//     OFF(v) = neighbours on another level,
+//     SUP(v) = neighbours on v's level with a larger id,
+// and an edge's apexes are exactly OFF(x)∩OFF(y) (c1) plus SUP(x)∩SUP(y)
+// (the same-level apexes the reference's T keeps).  Same-level neighbours
+// below the endpoint are never read, and a hit needs no level lookup: the
+// list it was streamed from says which tally it belongs to.  Over the full
+// cover set each all-horizontal triangle is kept at exactly one of its three
+// edges, so the reference's c2 (every same-level hit, 3 per such triangle)
+// is 3 x the SUP tally — the counters hold c2 in the reference's units.
 //
 //  1. owner_select: ordered compaction over the CSR entries (x, y) keeping
 //     level[x]==level[y] && owns(x, y).  Entries are in row order, so each
-//     owner's partners come out contiguous: P[seg_beg[x], seg_end[x]).
-//  2. split points: the id space is cut into F equal ranges; split[v][r] is
-//     the position in N(v) of the first id in range r (one flat pass over
-//     the entries).  An owner whose list exceeds the table is staged one
-//     group of ranges at a time, and every partner's matching slice is read
-//     from the table — no per-partner searches.
-//  3. make_items: owners with d(x) <= TINY -> thread items; <= WT -> warp
+//     owner's partners come out contiguous: P[seg_beg[x], seg_end[x]).  The
+//     same pass writes the OFF/SUP class bits of every entry.
+//  2. lists: word prefixes of the class bits give every entry its slot in
+//     the OFF or SUP array (no second scan); one scatter writes both.
+//  3. split points: the id space is cut into F equal ranges; split[v][r] is
+//     the position in OFF(v) / SUP(v) of the first id in range r.  An owner
+//     whose staged lists exceed the table is staged one group of ranges at a
+//     time, and every partner's matching slices are read from the table.
+//  4. make_items: owners with d(x) <= TINY -> thread items; <= WT -> warp
 //     items (x, p0, p1), <= PW partners each; others -> CTA items
 //     (x, p0, p1, group), <= PC partners.  With nshards > 1 only this
 //     shard's partner blocks are listed (dist.py shard_of).
-//  4. k_isect_tiny / k_isect_warp: one thread / warp per item; the warp tier
-//     keeps a per-warp bucket hash of N(x) (4-entry buckets, LDS.128).
-//  5. k_isect_cta: one CTA per item; the group's slice of N(x) (<= HC ids)
-//     staged in a two-table cuckoo set; the partners' slices are flattened
-//     into one element stream (block scan of lengths) that warps consume in
-//     CHUNK-element grabs (CHUNK / 32 loads in flight per lane).
+//  5. k_isect_tiny / k_isect_warp: one thread / warp per item; the warp tier
+//     keeps a per-warp bucket hash of OFF(x) ∪ SUP(x) (4-entry buckets).
+//  6. k_isect_cta: one CTA per item; the group's slices of OFF(x) ∪ SUP(x)
+//     (<= HC ids) staged in a two-table cuckoo set; the partners' slices
+//     (two per partner) are flattened into one element stream (block scan of
+//     lengths) that warps consume in CHUNK-element grabs.
 //
-// Hash entries carry the apex's level relation to the owner in bit 31
-// (same level -> c2), so hits need no level gather.  Tallies reduce per warp
-// into one 64-bit atomic each.
+// Forward mode (fwd, tcb_forward_count): every entry is classed OFF, owners
+// stage only the neighbours ranked above them, and every hit is a triangle
+// (tallied in c1).
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -62,19 +79,39 @@ constexpr int PW = TCB_PW;            // partners per warp item
 constexpr int C_THREADS = 512;        // 2 CTAs per SM
 constexpr int HC = TCB_HC;            // staged ids per CTA item
 constexpr int C_SLOTS = 4 * HC;       // load <= 1/4 (64 KB)
-constexpr int PC = 2 * C_THREADS;     // partners per CTA item (2 per thread in the scan)
+constexpr int PC = 2 * C_THREADS;     // partners per CTA item
+constexpr int NSEG = 2 * PC;          // stream segments: partner t -> 2t (OFF), 2t+1 (SUP)
 constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per lane)
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int LONG_LIST = 64;         // warp tier: lists streamed by a whole warp
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
-constexpr uint32_t SAME = 0x80000000u;
 
 __device__ __forceinline__ int ceil_log2_dev(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
 // ---------------------------------------------------------------------------
-// bucketed hash set in shared memory
+// entry classes: bit i of cls[j].x / .y = CSR entry 32j+i is OFF / SUP.
+// pre[j] = exclusive prefix over words of popc(.x) | popc(.y) << 32, so an
+// entry's slot in the OFF (SUP) array is a prefix read plus one popc.
+
+__device__ __forceinline__ int64_t rank_off(const uint2* __restrict__ cls,
+                                            const unsigned long long* __restrict__ pre,
+                                            int64_t p) {
+    const int64_t j = p >> 5;
+    const uint32_t below = (1u << (p & 31)) - 1u;
+    return int64_t(pre[j] & 0xFFFFFFFFull) + __popc(cls[j].x & below);
+}
+__device__ __forceinline__ int64_t rank_sup(const uint2* __restrict__ cls,
+                                            const unsigned long long* __restrict__ pre,
+                                            int64_t p) {
+    const int64_t j = p >> 5;
+    const uint32_t below = (1u << (p & 31)) - 1u;
+    return int64_t(pre[j] >> 32) + __popc(cls[j].y & below);
+}
+
+// ---------------------------------------------------------------------------
+// bucketed hash set in shared memory (warp tier; CTA fallback)
 
 struct BucketHash {
     uint32_t* tab;
@@ -90,8 +127,8 @@ struct BucketHash {
     __device__ __forceinline__ unsigned bucket(int key) const {
         return (unsigned(key) * 0x9E3779B1u) >> shift;
     }
-    __device__ __forceinline__ void insert(int key, bool same) const {
-        const uint32_t e = uint32_t(key) | (same ? SAME : 0u);
+    __device__ __forceinline__ void insert(int key) const {
+        const uint32_t e = uint32_t(key);
         unsigned b = bucket(key);
         while (true) {
 #pragma unroll
@@ -100,52 +137,32 @@ struct BucketHash {
             b = (b + 1) & bmask;
         }
     }
-    // 0 = miss, 1 = hit other level, 2 = hit same level.  The first bucket
-    // is resolved without branches; the loop runs only when that bucket is
-    // full and does not hold the key (rare at load <= 1/4).
-    // hits: c_other += apex on another level, c_same += apex on the owner's level
-    __device__ __forceinline__ void count(int key, uint32_t& c_other, uint32_t& c_same) const {
-        const int r = find(key);
-        c_other += r == 1;
-        c_same += r >> 1;
-    }
-    __device__ __forceinline__ int find(int key) const {
+    // The first bucket is resolved without branches; the loop runs only when
+    // that bucket is full and does not hold the key (rare at load <= 1/4).
+    __device__ __forceinline__ uint32_t hit(int key) const {
         unsigned b = bucket(key);
+        const uint32_t k = uint32_t(key);
         {
             const uint4 v = reinterpret_cast<const uint4*>(tab)[b];
-            const uint32_t k = uint32_t(key);
-            const bool m0 = ((v.x ^ k) << 1) == 0u, m1 = ((v.y ^ k) << 1) == 0u;
-            const bool m2 = ((v.z ^ k) << 1) == 0u, m3 = ((v.w ^ k) << 1) == 0u;
-            const uint32_t e = m0 ? v.x : (m1 ? v.y : (m2 ? v.z : v.w));
-            const bool hit = m0 | m1 | m2 | m3;
-            if (hit || v.w == EMPTY) return hit ? 1 + int(e >> 31) : 0;
+            const bool h = (v.x == k) | (v.y == k) | (v.z == k) | (v.w == k);
+            if (h || v.w == EMPTY) return h;
             b = (b + 1) & bmask;
         }
         while (true) {
             TCB_DASSERT(b <= bmask);
             const uint4 v = reinterpret_cast<const uint4*>(tab)[b];
-            const uint32_t k = uint32_t(key);
-            if ((v.x & ~SAME) == k) return 1 + (v.x >> 31);
-            if ((v.y & ~SAME) == k) return 1 + (v.y >> 31);
-            if ((v.z & ~SAME) == k) return 1 + (v.z >> 31);
-            if ((v.w & ~SAME) == k) return 1 + (v.w >> 31);
+            if ((v.x == k) | (v.y == k) | (v.z == k) | (v.w == k)) return 1;
             if (v.w == EMPTY) return 0;  // buckets fill in slot order
             b = (b + 1) & bmask;
         }
     }
 };
 
-#ifndef TCB_CUCKOO
-#define TCB_CUCKOO 1
-#endif
-// 2-choice cuckoo set over two half tables (A/B knob TCB_CUCKOO): a probe is
-// two LDS.32 and two compares with no loop.  Parallel insertion by atomicExch kick chains; a
+// 2-choice cuckoo set over two half tables: a probe is two LDS.32 and two
+// compares with no loop.  Parallel insertion by atomicExch kick chains; a
 // chain longer than CUCKOO_KICKS reports failure and the caller falls back
 // to the bucket table (load <= 1/4 makes that vanishingly rare).
 constexpr int CUCKOO_KICKS = 64;
-#ifndef TCB_FULLTAB
-#define TCB_FULLTAB 1
-#endif
 
 struct CuckooHash {
     uint32_t* tab;   // table 1: tab[0, half); table 2: tab[half, 2 half)
@@ -159,70 +176,46 @@ struct CuckooHash {
     }
     __device__ __forceinline__ unsigned h1(uint32_t k) const { return (k * 0x9E3779B1u) >> shift; }
     __device__ __forceinline__ unsigned h2(uint32_t k) const { return (k * 0x7FEB352Du) >> shift; }
-    __device__ __forceinline__ bool insert(int key, bool same) const {
-        uint32_t e = uint32_t(key) | (same ? SAME : 0u);
-        uint32_t* slot = tab + h1(uint32_t(key));
+    __device__ __forceinline__ bool insert(int key) const {
+        uint32_t e = uint32_t(key);
+        uint32_t* slot = tab + h1(e);
         for (int it = 0; it < CUCKOO_KICKS; ++it) {
             const uint32_t old = atomicExch(slot, e);
             if (old == EMPTY) return true;
-            e = old;  // carry the evicted entry to its slot in the other table
-            const uint32_t k = old & ~SAME;
-            slot = slot < tab2 ? tab2 + h2(k) : tab + h1(k);
+            e = old;  // carry the evicted key to its slot in the other table
+            slot = slot < tab2 ? tab2 + h2(e) : tab + h1(e);
         }
         return false;
     }
-    __device__ __forceinline__ int find(int key) const {
-        const uint32_t k = uint32_t(key);
-        const uint32_t e1 = tab[h1(k)], e2 = tab2[h2(k)];
-        const bool m1 = ((e1 ^ k) << 1) == 0u, m2 = ((e2 ^ k) << 1) == 0u;
-        return (m1 | m2) ? 1 + int((m1 ? e1 : e2) >> 31) : 0;
-    }
-    // A key sits in at most one slot, stored as key (other level) or
-    // key | SAME (owner's level): two equality tests per table entry and two
-    // predicated increments.  key >= 0 (EMPTY would match free slots).
-    __device__ __forceinline__ void count(int key, uint32_t& c_other, uint32_t& c_same) const {
+    // key >= 0, so EMPTY never matches
+    __device__ __forceinline__ uint32_t hit(int key) const {
 #ifdef TCB_NOPROBE  // measurement-only variant: stream without probing
-        c_other += uint32_t(key) == 0x7FFFFFFEu;
-        return;
+        return uint32_t(key) == 0x7FFFFFFEu;
 #endif
-        const uint32_t k = uint32_t(key), ks = k | SAME;
-#ifdef TCB_NOCONFLICT  // measurement-only: same loads at bank-conflict-free addresses
-        {
-            const uint32_t f1 = tab[(h1(k) & ~31u) | (threadIdx.x & 31)];
-            const uint32_t f2 = tab2[(h2(k) & ~31u) | (threadIdx.x & 31)];
-            c_other += (f1 == k) | (f2 == k);
-            c_same += (f1 == ks) | (f2 == ks);
-            return;
-        }
-#endif
-        const uint32_t e1 = tab[h1(k)], e2 = tab2[h2(k)];
-        c_other += (e1 == k) | (e2 == k);
-        c_same += (e1 == ks) | (e2 == ks);
+        const uint32_t k = uint32_t(key);
+        return (tab[h1(k)] == k) | (tab2[h2(k)] == k);
     }
 };
 
-// c1/c2 tallies.  T is not tallied: a same-level triangle puts all three of
-// its edges in the cover set and is found once per edge, and the reference's
-// rule (w > max(u, v), _kernels.py:688-692) accepts exactly one of the three,
-// so over the full cover set T == c1 + c2/3 (formed in capi.cu fill_result).
+// c1 / same-level tallies.  `sup` counts SUP∩SUP hits, each one a same-level
+// apex the reference's T keeps (w > max(u, v)); the reference's c2 counts
+// every same-level hit, 3 per all-horizontal triangle, so c2 = 3 sup over the
+// cover set and T = c1 + c2/3 (formed in capi.cu fill_result).
 struct Tally {
-    unsigned long long c1 = 0, c2 = 0;
+    unsigned long long c1 = 0, sup = 0;
     __device__ __forceinline__ void flush(DevCounters* C) {
         c1 = warp_sum(c1);
-        c2 = warp_sum(c2);
+        sup = warp_sum(sup);
         if (lane_id() == 0) {
             if (c1) atomicAdd(&C->c1, c1);
-            if (c2) atomicAdd(&C->c2, c2);
+            if (sup) atomicAdd(&C->c2, 3ull * sup);
         }
     }
 };
 
-// Forward mode (tcb_forward_count, the forward branch of CETC-Seq-FE): every
-// edge is intersected (the caller passes an all-zero level array, so every
-// edge is selected and every hit is "same level"), and an owner stages only
-// the neighbours ranked above it in (degree desc, id asc) order, the order
-// that makes x the owner of (x, y).  A triangle a > b > c in that order is
-// then hit once: at (b, c) with apex a.  T = the same-level tally.
+// Forward mode: an owner stages only the neighbours ranked above it in
+// (degree desc, id asc) order, the order that makes x the owner of (x, y).
+// A triangle a > b > c in that order is then hit once: at (b, c) with apex a.
 __device__ __forceinline__ bool staged(const int2* __restrict__ vinfo, int w, int x, int dx,
                                        int fwd) {
     if (!fwd) return true;
@@ -230,38 +223,43 @@ __device__ __forceinline__ bool staged(const int2* __restrict__ vinfo, int w, in
     return dw > dx || (dw == dx && w < x);
 }
 
+// Per-vertex list bounds: OFF(v) = L[ob[v], ob[v+1]), SUP(v) = L[sb[v], sb[v+1]).
+struct Lists {
+    const int32_t* __restrict__ L;
+    const int64_t* __restrict__ ob;
+    const int64_t* __restrict__ sb;
+    const int2* __restrict__ split;  // [v*(F+1) + r] = (OFF pos, SUP pos) of range r
+    int rshift;
+};
+
 // ---------------------------------------------------------------------------
 // warp tier helpers: one long list with the whole warp (4 loads in flight per
 // lane); a batch of <= 32 lists flattened across lanes.
 
 template <typename Probe>
-__device__ __forceinline__ void probe_long(const int32_t* __restrict__ nb, int64_t s, int d,
-                                           const Probe& h, Tally& tl) {
+__device__ __forceinline__ uint32_t probe_long(const int32_t* __restrict__ L, int64_t s, int d,
+                                               const Probe& h) {
     const int lane = int(lane_id());
-    uint32_t co = 0, cs = 0;
+    uint32_t acc = 0;
     int i = lane;
     for (; i + 96 < d; i += 128) {
-        const int w0 = nb[s + i], w1 = nb[s + i + 32], w2 = nb[s + i + 64], w3 = nb[s + i + 96];
-        h.count(w0, co, cs);
-        h.count(w1, co, cs);
-        h.count(w2, co, cs);
-        h.count(w3, co, cs);
+        const int w0 = L[s + i], w1 = L[s + i + 32], w2 = L[s + i + 64], w3 = L[s + i + 96];
+        acc += h.hit(w0) + h.hit(w1) + h.hit(w2) + h.hit(w3);
     }
-    for (; i < d; i += 32) h.count(nb[s + i], co, cs);
-    tl.c1 += co;
-    tl.c2 += cs;
+    for (; i < d; i += 32) acc += h.hit(L[s + i]);
+    return acc;
 }
 
 template <typename Probe>
-__device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int64_t ys, int yd,
-                                            const Probe& h, Tally& tl) {
+__device__ __forceinline__ uint32_t probe_batch(const int32_t* __restrict__ L, int64_t ys, int yd,
+                                                const Probe& h) {
     const unsigned lane = lane_id();
+    uint32_t acc = 0;
     unsigned longs = __ballot_sync(0xffffffffu, yd >= LONG_LIST);
     while (longs) {
         const int k = __ffs(longs) - 1;
         longs &= longs - 1;
-        probe_long(nb, __shfl_sync(0xffffffffu, ys, k), __shfl_sync(0xffffffffu, yd, k), h,
-                   tl);
+        acc += probe_long(L, __shfl_sync(0xffffffffu, ys, k), __shfl_sync(0xffffffffu, yd, k), h);
     }
     if (yd >= LONG_LIST) yd = 0;
     const int incl = warp_inclusive_scan(yd);
@@ -276,44 +274,49 @@ __device__ __forceinline__ void probe_batch(const int32_t* __restrict__ nb, int6
         }
         const int64_t ysk = __shfl_sync(0xffffffffu, ys, k);
         const int exk = __shfl_sync(0xffffffffu, incl - yd, k);
-        if (i < total) {
-            uint32_t co = 0, cs = 0;
-            h.count(nb[ysk + (i - exk)], co, cs);
-            tl.c1 += co;
-            tl.c2 += cs;
-        }
+        if (i < total) acc += h.hit(L[ysk + (i - exk)]);
     }
+    return acc;
 }
 
 // ---------------------------------------------------------------------------
-// 1. owner-grouped selection
+// 1. owner-grouped selection + entry classes
 
 // The owner predicate is evaluated once (two random vinfo gathers per
 // entry) into a bitmask, one ballot word per 32 entries; both scan passes
-// then read bits only.
+// then read bits only.  The same gathers give the OFF / SUP class bits.
 __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
-                             const int2* __restrict__ vinfo, int64_t nnz, uint32_t* __restrict__ bits) {
+                             const int2* __restrict__ vinfo, int64_t nnz, int fwd,
+                             uint32_t* __restrict__ bits, uint2* __restrict__ cls) {
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const unsigned lane = lane_id();
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < nnz;
          base += gthreads) {
         const int64_t e = base + lane;
-        bool keep = false;
+        bool keep = false, off = false, sup = false;
         if (e < nnz) {
             const int x = src[e], y = nb[e];
             const int2 a = vinfo[x], b = vinfo[y];
             keep = a.x == b.x && (a.y > b.y || (a.y == b.y && x < y));
+            off = fwd || a.x != b.x;
+            sup = !fwd && a.x == b.x && y > x;
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) bits[base >> 5] = m;
+        const unsigned mo = __ballot_sync(0xffffffffu, off);
+        const unsigned ms = __ballot_sync(0xffffffffu, sup);
+        if (lane == 0) {
+            bits[base >> 5] = m;
+            cls[base >> 5] = make_uint2(mo, ms);
+        }
     }
 }
 
 void owner_select(Context* ctx, const int64_t* row, const int32_t* src, const int32_t* nb,
-                  const int2* vinfo, int64_t nnz, int32_t* P, int64_t* seg_beg, int64_t* seg_end,
-                  int64_t* d_ncover) {
+                  const int2* vinfo, int64_t nnz, int fwd, uint2* cls, int32_t* P,
+                  int64_t* seg_beg, int64_t* seg_end, int64_t* d_ncover) {
     uint32_t* bits = ctx->wsT<uint32_t>(WS_QUEUE_A, (nnz + 31) / 32);
-    TCB_LAUNCH(ctx, k_owner_bits, grid_for(ctx, nnz, 256), 256, 0, src, nb, vinfo, nnz, bits);
+    TCB_LAUNCH(ctx, k_owner_bits, grid_for(ctx, nnz, 256), 256, 0, src, nb, vinfo, nnz, fwd, bits,
+               cls);
     const uint32_t* B = bits;
     scan_apply(
         ctx, nnz,
@@ -335,35 +338,87 @@ __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restri
 }
 
 // ---------------------------------------------------------------------------
-// 2. split points: split[v*(F+1) + r] = first position (relative to row[v])
-//    of an id >= r << rshift; split[.][0] = 0, split[.][F] = d(v).
+// 2. OFF / SUP lists.  The OFF array comes first; SUP starts at NOFF (the
+//    class total, pre[nw] low half).  ob/sb hold absolute positions in L.
 
-__global__ void k_split_points(const int64_t* __restrict__ row, const int32_t* __restrict__ src,
-                               const int32_t* __restrict__ nb, int64_t nnz, int rshift,
-                               int* __restrict__ split) {
+__global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
+                              const uint2* __restrict__ cls,
+                              const unsigned long long* __restrict__ pre, int64_t nw,
+                              int64_t* __restrict__ ob, int64_t* __restrict__ sb,
+                              int2* __restrict__ split) {
+    const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v <= n; v += stride) {
+        const int64_t p = row[v];
+        const int64_t o = rank_off(cls, pre, p), s = noff + rank_sup(cls, pre, p);
+        ob[v] = o;
+        sb[v] = s;
+        if (v == n) continue;
+        // a class-empty list has an all-zero split row (k_split_points writes
+        // only rows with entries)
+        const int64_t p1 = row[v + 1];
+        int* sp = reinterpret_cast<int*>(split + v * (F + 1));
+        if (rank_off(cls, pre, p1) == o)
+            for (int q = 0; q <= F; ++q) sp[2 * q] = 0;
+        if (noff + rank_sup(cls, pre, p1) == s)
+            for (int q = 0; q <= F; ++q) sp[2 * q + 1] = 0;
+    }
+}
+
+__global__ void k_scatter_lists(const int32_t* __restrict__ nb, int64_t nnz,
+                                const uint2* __restrict__ cls,
+                                const unsigned long long* __restrict__ pre, int64_t nw,
+                                int32_t* __restrict__ L) {
+    const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-        const int v = src[e];
-        const int64_t rb = row[v];
-        const int r = nb[e] >> rshift;
-        int* sv = split + int64_t(v) * (F + 1);
-        const int prev = e == rb ? -1 : (nb[e - 1] >> rshift);
-        for (int q = prev + 1; q <= r; ++q) sv[q] = int(e - rb);
-        if (e == row[v + 1] - 1)
-            for (int q = r + 1; q <= F; ++q) sv[q] = int(e + 1 - rb);
+        const uint2 c = cls[e >> 5];
+        const uint32_t bit = 1u << (e & 31);
+        if (c.x & bit) L[rank_off(cls, pre, e)] = nb[e];
+        else if (c.y & bit) L[noff + rank_sup(cls, pre, e)] = nb[e];
     }
 }
 
 // ---------------------------------------------------------------------------
-// 3. work items
+// 3. split points: split[v*(F+1) + r] = (first position in OFF(v), in SUP(v))
+//    of an id >= r << rshift, relative to the list start; [0] = 0, [F] = size.
+
+__global__ void k_split_points(const int32_t* __restrict__ src, int64_t nnz,
+                               const uint2* __restrict__ cls,
+                               const unsigned long long* __restrict__ pre, int64_t nw,
+                               const int32_t* __restrict__ L, const int64_t* __restrict__ ob,
+                               const int64_t* __restrict__ sb, int rshift,
+                               int2* __restrict__ split) {
+    const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
+        const uint2 c = cls[e >> 5];
+        const uint32_t bit = 1u << (e & 31);
+        const bool off = c.x & bit;
+        if (!off && !(c.y & bit)) continue;
+        const int v = src[e];
+        const int64_t g = off ? rank_off(cls, pre, e) : noff + rank_sup(cls, pre, e);
+        const int64_t b0 = off ? ob[v] : sb[v];
+        const int64_t b1 = off ? ob[v + 1] : sb[v + 1];
+        const int k = int(g - b0);
+        const int r = L[g] >> rshift;
+        const int prev = g == b0 ? -1 : (L[g - 1] >> rshift);
+        int* sp = reinterpret_cast<int*>(split + int64_t(v) * (F + 1)) + (off ? 0 : 1);
+        for (int q = prev + 1; q <= r; ++q) sp[2 * q] = k;
+        if (g == b1 - 1)
+            for (int q = r + 1; q <= F; ++q) sp[2 * q] = k + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 4. work items
 
 __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __restrict__ seg_beg,
-                             const int64_t* __restrict__ seg_end, const int* __restrict__ split,
-                             int64_t n, longlong4* __restrict__ witems,
-                             longlong4* __restrict__ citems, longlong4* __restrict__ titems,
-                             unsigned long long* nw, unsigned long long* nc,
-                             unsigned long long* nt, int shard, int nshards, int wt, int hc,
-                             int tiny) {
+                             const int64_t* __restrict__ seg_end, Lists ls, int64_t n,
+                             longlong4* __restrict__ witems, longlong4* __restrict__ citems,
+                             longlong4* __restrict__ titems, unsigned long long* nw,
+                             unsigned long long* nc, unsigned long long* nt, int shard,
+                             int nshards, int wt, int hc, int tiny) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     // Multi-GPU (tcb_cetc_shard): partner block i of owner x belongs to
     // shard (x + i) % nshards (dist.py shard_of mirrors this).  Blocks rather
@@ -376,6 +431,10 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         if (d == 0) continue;
         const int64_t s = seg_beg[x], e = seg_end[x];
         if (e <= s) continue;
+        // nothing staged (no OFF neighbours, no same-level neighbour above
+        // x): no edge of x can have an apex
+        const int64_t st = (ls.ob[x + 1] - ls.ob[x]) + (ls.sb[x + 1] - ls.sb[x]);
+        if (st == 0) continue;
         if (d <= tiny) {  // <= TINY partners, each with <= TINY ids
             if (!mine(x, 0)) continue;
             const unsigned long long slot = atomicAdd(nt, 1ull);
@@ -395,86 +454,99 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
             }
             continue;
         }
-        // fewest range groups G (power of two <= F) whose slices all fit HC
-        const int* sx = split + x * (F + 1);
+        // fewest range groups G (power of two <= F) whose staged slices all fit HC
+        const int2* sx = ls.split + x * (F + 1);
         int lg = 0;
-        if (d > hc) {
+        if (st > hc) {
             for (lg = 1; lg < LOG_F; ++lg) {
                 const int step = F >> lg;
                 int mx = 0;
-                for (int q = 0; q < F; q += step) mx = max(mx, sx[q + step] - sx[q]);
+                for (int q = 0; q < F; q += step)
+                    mx = max(mx, (sx[q + step].x - sx[q].x) + (sx[q + step].y - sx[q].y));
                 if (mx <= hc) break;
             }
         }
-        TCB_DASSERT(sx[0] == 0 && sx[F] == int(d));
         const int G = 1 << lg;
         const int64_t per = (e - s + PC - 1) / PC;
         int64_t my = 0;
         for (int64_t i = 0; i < per; ++i) my += mine(x, i);
         if (my == 0) continue;
-        unsigned long long base = atomicAdd(nc, (unsigned long long)(my * G));
-        for (int g = 0; g < G; ++g)
+        int ng = 0;  // groups with something staged
+        for (int g = 0; g < G; ++g) {
+            const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;
+            ng += (sx[q1].x - sx[q0].x) + (sx[q1].y - sx[q0].y) > 0;
+        }
+        unsigned long long base = atomicAdd(nc, (unsigned long long)(my * ng));
+        for (int g = 0; g < G; ++g) {
+            const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;
+            if ((sx[q1].x - sx[q0].x) + (sx[q1].y - sx[q0].y) == 0) continue;
             for (int64_t i = 0; i < per; ++i) {
                 if (!mine(x, i)) continue;
                 const int64_t p0 = s + i * PC;
                 citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
             }
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// 3b. thread tier: one thread per tiny owner (d(x) <= TINY, so every partner
-//     has <= TINY ids too).  N(x) sits in registers; each partner id is
-//     compared with all of it; the level is gathered only on a hit.
+// 4b. thread tier: one thread per tiny owner (d(x) <= TINY, so every partner
+//     has <= TINY ids too).  OFF(x) ∪ SUP(x) sits in registers; each streamed
+//     id is compared with all of it.
 
 __global__ void __launch_bounds__(256)
     k_isect_tiny(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
-                 const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
-                 const int32_t* __restrict__ P, const int32_t* __restrict__ level,
-                 DevCounters* C, const int2* __restrict__ vinfo, int fwd) {
+                 Lists ls, const int32_t* __restrict__ P, DevCounters* C,
+                 const int2* __restrict__ vinfo, int fwd) {
     const int64_t nitems = int64_t(*nitems_p);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    uint32_t nh = 0, ns = 0;
+    uint32_t n1 = 0, ns = 0;
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < nitems; it += stride) {
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int64_t xb = row[x];
-        const int xd = int(row[x + 1] - xb);
-        const int lx = level[x];
+        const int64_t o0 = ls.ob[x], o1 = ls.ob[x + 1], s0 = ls.sb[x];
+        const int no = int(o1 - o0), nx = no + int(ls.sb[x + 1] - s0);
+        const int dx = fwd ? vinfo[x].y : 0;
         int a[TINY];
 #pragma unroll
-        for (int i = 0; i < TINY; ++i) a[i] = i < xd ? nb[xb + i] : -1;
+        for (int i = 0; i < TINY; ++i) {
+            int w = -1;
+            if (i < nx) w = i < no ? ls.L[o0 + i] : ls.L[s0 + (i - no)];
+            if (w >= 0 && !staged(vinfo, w, x, dx, fwd)) w = -1;
+            a[i] = w;
+        }
         for (int64_t p = item.y; p < item.z; ++p) {
             const int y = P[p];
-            const int64_t yb = row[y];
-            const int yd = int(row[y + 1] - yb);
-            for (int j = 0; j < yd; ++j) {
-                const int w = nb[yb + j];
+            const int64_t y0 = ls.ob[y], y1 = ls.ob[y + 1], y2 = ls.sb[y], y3 = ls.sb[y + 1];
+            for (int64_t j = y0; j < y1; ++j) {
+                const int w = ls.L[j];
                 bool hit = false;
 #pragma unroll
                 for (int i = 0; i < TINY; ++i) hit |= a[i] == w;
-                if (hit && staged(vinfo, w, x, xd, fwd)) {
-                    nh += 1;
-                    ns += level[w] == lx;
-                }
+                n1 += hit;
+            }
+            for (int64_t j = y2; j < y3; ++j) {
+                const int w = ls.L[j];
+                bool hit = false;
+#pragma unroll
+                for (int i = 0; i < TINY; ++i) hit |= a[i] == w;
+                ns += hit;
             }
         }
     }
     Tally tl;
-    tl.c1 = nh - ns;
-    tl.c2 = ns;
+    tl.c1 = n1;
+    tl.sup = ns;
     tl.flush(C);
 }
 
 // ---------------------------------------------------------------------------
-// 4. warp tier
+// 5. warp tier
 
 __global__ void __launch_bounds__(W_WARPS * 32, 4)
     k_isect_warp(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
-                 const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
-                 const int32_t* __restrict__ P, const int32_t* __restrict__ level,
-                 unsigned long long* fetch, DevCounters* C, const int2* __restrict__ vinfo,
-                 int fwd) {
+                 Lists ls, const int32_t* __restrict__ P, unsigned long long* fetch,
+                 DevCounters* C, const int2* __restrict__ vinfo, int fwd) {
     extern __shared__ uint4 smem4[];
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
@@ -490,27 +562,34 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
         if (it >= nitems) break;
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int64_t xb = row[x];
-        const int xd = int(row[x + 1] - xb);
-        const int lx = level[x];
-        const int slots = max(16, 2 << ceil_log2_dev(xd));
+        const int64_t o0 = ls.ob[x], s0 = ls.sb[x];
+        const int no = int(ls.ob[x + 1] - o0), nx = no + int(ls.sb[x + 1] - s0);
+        const int dx = fwd ? vinfo[x].y : 0;
+        const int qx = x >> ls.rshift;
+        const int slots = max(16, 2 << ceil_log2_dev(nx));
         BucketHash h;
         h.setup(tab, slots);
-        for (int i = lane; i < xd; i += 32) {
-            const int w = nb[xb + i];
-            if (staged(vinfo, w, x, xd, fwd)) h.insert(w, level[w] == lx);
+        for (int i = lane; i < nx; i += 32) {
+            const int w = i < no ? ls.L[o0 + i] : ls.L[s0 + (i - no)];
+            if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
         }
         __syncwarp();
         for (int64_t pb = item.y; pb < item.z; pb += 32) {
             const int64_t j = pb + lane;
-            int64_t ys = 0;
-            int yd = 0;
+            int64_t yo = 0, ys = 0;
+            int ydo = 0, yds = 0;
             if (j < item.z) {
                 const int y = P[j];
-                ys = row[y];
-                yd = int(row[y + 1] - ys);
+                yo = ls.ob[y];
+                ydo = int(ls.ob[y + 1] - yo);
+                // SUP(y) ids below x's id range cannot be in SUP(x)
+                const int64_t sy = ls.sb[y];
+                const int a = ls.split[int64_t(y) * (F + 1) + qx].y;
+                ys = sy + a;
+                yds = int(ls.sb[y + 1] - sy) - a;
             }
-            probe_batch(nb, ys, yd, h, tl);
+            tl.c1 += probe_batch(ls.L, yo, ydo, h);
+            tl.sup += probe_batch(ls.L, ys, yds, h);
         }
         __syncwarp();
         for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
@@ -520,21 +599,38 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
 }
 
 // ---------------------------------------------------------------------------
-// 5. CTA tier
+// 6. CTA tier
+//
+// Stream segments: partner t contributes segment 2t (its OFF slice) and 2t+1
+// (its SUP slice); a hit counts for c1 or the SUP tally by segment parity.
 
-// A chunk that crosses slice boundaries: each lane walks forward from the
-// chunk's first partner k0; a lane crosses a boundary in few of its J
+// Largest k < nseg with s_off[k] <= c0 (s_off[0] = 0 <= c0): three steps,
+// two 32-way ballots over a 2048-entry table and one compare.
+__device__ __forceinline__ int find_segment(const int* s_off, int nseg, int c0) {
+    const int lane = int(lane_id());
+    const int j = lane * 64;
+    const unsigned b1 = __ballot_sync(0xffffffffu, j < nseg && s_off[j] <= c0);
+    const int kb = (31 - __clz(b1)) * 64;
+    const int j2 = kb + lane * 2;
+    const unsigned b2 = __ballot_sync(0xffffffffu, j2 < nseg && s_off[j2] <= c0);
+    const int k = kb + 2 * (31 - __clz(b2));
+    return k + ((k + 1 < nseg && s_off[k + 1] <= c0) ? 1 : 0);
+}
+
+// A chunk that crosses segment boundaries: each lane walks forward from the
+// chunk's first segment k0; a lane crosses a boundary in few of its J
 // elements.  FULL: the chunk holds CHUNK elements (no bounds checks).
 template <bool FULL, typename Probe>
-__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ nb, const int64_t* s_ys,
-                                            const int* s_off, int np, int k0, int c0, int c1,
+__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const int64_t* s_ys,
+                                            const int* s_off, int nseg, int k0, int c0, int c1,
                                             const Probe& h, uint32_t& co, uint32_t& cs) {
     constexpr int J = CHUNK / 32;
     int k = k0;
     int next = s_off[k + 1];
-    const int32_t* q = nb + s_ys[k];
+    const int32_t* q = L + s_ys[k];
     const int i0 = c0 + int(lane_id());
     int w[J];
+    uint32_t par = 0;  // bit j: element j came from a SUP segment
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int i = i0 + 32 * j;
@@ -542,39 +638,44 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ nb, cons
         if (FULL || i < c1) {
             if (next <= i) {
                 do {
-                    TCB_DASSERT(k + 1 < np);
+                    TCB_DASSERT(k + 1 < nseg);
                     ++k;
                     next = s_off[k + 1];
                 } while (next <= i);
-                q = nb + s_ys[k];
+                q = L + s_ys[k];
             }
 #ifdef TCB_NOLOAD  // measurement-only variant: probe without streaming
             w[j] = int((uint32_t(i) * 2654435761u) >> 8) + int(reinterpret_cast<uintptr_t>(q) & 1);
 #else
             w[j] = q[i];
 #endif
+            par |= uint32_t(k & 1) << j;
         }
     }
+    uint32_t all = 0, sup = 0;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         if (!FULL && w[j] < 0) continue;
-        h.count(w[j], co, cs);
+        const uint32_t hv = h.hit(w[j]);
+        all += hv;
+        sup += hv & (par >> j);
     }
+    co += all - sup;
+    cs += sup;
 }
 
-// Warps consume the flattened stream of partner slices in CHUNK grabs;
-// element i belongs to partner k with s_off[k] <= i < s_off[k+1].  The
-// partner of a chunk's first element is found with two 32-way ballots over
-// s_off (np <= 1024); a chunk that lies inside one slice (the common case:
-// slices average hundreds of ids) takes a warp-uniform fast path with
-// coalesced loads and no per-element partner bookkeeping.
+// Warps consume the flattened stream of segments in CHUNK grabs; element i
+// belongs to segment k with s_off[k] <= i < s_off[k+1].  A chunk that lies
+// inside one segment (the common case: slices average hundreds of ids) takes
+// a warp-uniform fast path with coalesced loads and no per-element
+// segment bookkeeping.
 template <typename Probe>
-__device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, const int64_t* s_ys,
-                                              const int* s_off, int np,
-                                              int* s_next, const Probe& h, Tally& tl) {
+__device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, const int64_t* s_ys,
+                                              const int* s_off, int nseg, int* s_next,
+                                              const Probe& h, Tally& tl) {
     constexpr int J = CHUNK / 32;
-    const int total = s_off[np];
-    TCB_DASSERT(np >= 1 && np <= PC && total >= 0);
+    const int total = s_off[nseg];
+    TCB_DASSERT(nseg >= 1 && nseg <= NSEG && total >= 0);
     const int lane = int(lane_id());
     while (true) {
         int c0 = 0;
@@ -582,23 +683,14 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (c0 >= total) break;
         const int c1 = min(total, c0 + CHUNK);
-        // k0 = largest k with s_off[k] <= c0  (s_off[0] = 0 <= c0)
-        int k0;
-        {
-            const int j = lane * 32;
-            const unsigned b1 = __ballot_sync(0xffffffffu, j < np && s_off[j] <= c0);
-            const int kb = 31 - __clz(b1);
-            const int j2 = kb * 32 + lane;
-            const unsigned b2 = __ballot_sync(0xffffffffu, j2 < np && s_off[j2] <= c0);
-            k0 = kb * 32 + 31 - __clz(b2);
-        }
-        TCB_DASSERT(k0 >= 0 && k0 < np);
-        // per-chunk tallies: apexes on another level / on the owner's level
+        const int k0 = find_segment(s_off, nseg, c0);
+        TCB_DASSERT(k0 >= 0 && k0 < nseg && s_off[k0] <= c0 && c0 < s_off[k0 + 1]);
         uint32_t co = 0, cs = 0;
         if (s_off[k0 + 1] >= c1) {
-            // fast path: one partner slice
-            const int32_t* p = nb + s_ys[k0] + c0 + lane;
+            // fast path: one segment
+            const int32_t* p = L + s_ys[k0] + c0 + lane;
             int w[J];
+            uint32_t hits = 0;
             if (c1 - c0 == CHUNK) {
 #ifdef TCB_NOLOAD
 #pragma unroll
@@ -610,45 +702,48 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ nb, co
                 for (int j = 0; j < J; ++j) w[j] = p[32 * j];
 #endif
 #pragma unroll
-                for (int j = 0; j < J; ++j) h.count(w[j], co, cs);
+                for (int j = 0; j < J; ++j) hits += h.hit(w[j]);
             } else {
 #pragma unroll
                 for (int j = 0; j < J; ++j) w[j] = c0 + lane + 32 * j < c1 ? p[32 * j] : -1;
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
                     if (w[j] < 0) continue;
-                    h.count(w[j], co, cs);
+                    hits += h.hit(w[j]);
                 }
             }
+            if (k0 & 1) cs = hits; else co = hits;
         } else if (c1 - c0 == CHUNK) {
-            cross_chunk<true>(nb, s_ys, s_off, np, k0, c0, c1, h, co, cs);
+            cross_chunk<true>(L, s_ys, s_off, nseg, k0, c0, c1, h, co, cs);
         } else {
-            cross_chunk<false>(nb, s_ys, s_off, np, k0, c0, c1, h, co, cs);
+            cross_chunk<false>(L, s_ys, s_off, nseg, k0, c0, c1, h, co, cs);
         }
         tl.c1 += co;
-        tl.c2 += cs;
+        tl.sup += cs;
     }
 }
 
-// Exclusive block scan of the per-partner lengths (thread t holds partners
-// 2t, 2t+1) into s_off[0..np]; s_off[np] = stream length.  s_ys[k] becomes
-// the stream base of partner k: stream element i of its slice is nb[s_ys[k] + i].
-__device__ __forceinline__ void scan_lengths(int* s_off, int64_t* s_ys, int np, int64_t* s_tmp) {
-    __syncthreads();  // lengths were written with a different thread->partner map
+// Exclusive block scan of the per-segment counts in s_off[0..nseg) (thread t
+// holds segments 4t..4t+3) into s_off[0..nseg]; s_ys[k] is rebased so that
+// stream element i of segment k is L[s_ys[k] + i].
+__device__ __forceinline__ void scan_counts(int* s_off, int64_t* s_ys, int nseg, int64_t* s_tmp) {
+    __syncthreads();  // counts were written with a different thread->segment map
     const int t = threadIdx.x;
-    const int a = 2 * t < np ? s_off[2 * t] : 0;
-    const int b = 2 * t + 1 < np ? s_off[2 * t + 1] : 0;
+    int c[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = 4 * t + i < nseg ? s_off[4 * t + i] : 0;
     int64_t tot;
-    const int64_t ex = block_exclusive_scan<C_THREADS>(int64_t(a + b), s_tmp, tot);
-    if (2 * t < np) {
-        s_off[2 * t] = int(ex);
-        s_ys[2 * t] -= ex;
+    int64_t ex = block_exclusive_scan<C_THREADS>(int64_t(c[0] + c[1] + c[2] + c[3]), s_tmp, tot);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = 4 * t + i;
+        if (k < nseg) {
+            s_off[k] = int(ex);
+            s_ys[k] -= ex;
+        }
+        ex += c[i];
     }
-    if (2 * t + 1 < np) {
-        s_off[2 * t + 1] = int(ex + a);
-        s_ys[2 * t + 1] -= ex + a;
-    }
-    if (t == 0) s_off[np] = int(tot);
+    if (t == 0) s_off[nseg] = int(tot);
     __syncthreads();
 }
 
@@ -657,19 +752,18 @@ __device__ __forceinline__ void scan_lengths(int* s_off, int64_t* s_ys, int np, 
 #endif
 __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     k_isect_cta(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
-                const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
-                const int32_t* __restrict__ P, const int32_t* __restrict__ level,
-                const int* __restrict__ split, unsigned long long* fetch, DevCounters* C,
-                int hc, int dbg, const int2* __restrict__ vinfo, int fwd) {
+                Lists ls, const int32_t* __restrict__ P, unsigned long long* fetch,
+                DevCounters* C, int hc, int dbg, const int2* __restrict__ vinfo, int fwd) {
     extern __shared__ uint4 smem4[];
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS
-    int64_t* s_ys = reinterpret_cast<int64_t*>(tab + C_SLOTS);    // PC
-    int* s_off = reinterpret_cast<int*>(s_ys + PC);               // PC + 1
-    int* s_end = s_off + PC + 1;                                  // PC (sub-chunk cursors)
+    int64_t* s_ys = reinterpret_cast<int64_t*>(tab + C_SLOTS);    // NSEG: next unread position
+    int* s_off = reinterpret_cast<int*>(s_ys + NSEG);             // NSEG + 1
+    int* s_len = s_off + NSEG + 1;                                // NSEG: unread length
     __shared__ int64_t s_tmp[C_THREADS / 32 + 1];
     __shared__ unsigned long long s_item;
     __shared__ int s_next;
     __shared__ int s_fail;
+    const int32_t* __restrict__ L = ls.L;
     const unsigned long long nitems = *nitems_p;
     Tally tl;
     while (true) {
@@ -681,104 +775,106 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         const int x = int(item.x);
         const int lg = int(item.w >> 8), g = int(item.w & 255);
         const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;  // ranges [q0, q1)
-        const int64_t xrow = row[x];
-        const int* sx = split + int64_t(x) * (F + 1);
-        const int64_t xs = xrow + (lg ? sx[q0] : 0);
-        const int64_t xe = lg ? xrow + sx[q1] : row[x + 1];
-        const int lx = level[x];
-        const int dx = int(row[x + 1] - xrow);
+        const int2* sx = ls.split + int64_t(x) * (F + 1);
+        const int2 ax = sx[q0], bx = sx[q1];
+        // the owner's staged slices: OFF [xo0, xo1), SUP [xs0, xs1)
+        const int64_t xo0 = ls.ob[x] + ax.x, xo1 = ls.ob[x] + bx.x;
+        const int64_t xs0 = ls.sb[x] + ax.y, xs1 = ls.sb[x] + bx.y;
+        const int no = int(xo1 - xo0), ns = int(xs1 - xs0);
+        const int dx = fwd ? vinfo[x].y : 0;
+        // SUP(y) ids below x's id range cannot be in SUP(x)
+        const int qa = max(q0, x >> ls.rshift);
         const int np = int(item.z - item.y);
-        // partner slices for ranges [q0, q1) (the whole list when lg == 0)
+        const int nseg = 2 * np;
         for (int t = threadIdx.x; t < np; t += C_THREADS) {
             const int y = P[item.y + t];
-            const int64_t yb = row[y];
-            int a = 0, b;
-            if (lg) {
-                const int* sy = split + int64_t(y) * (F + 1);
-                a = sy[q0];
-                b = sy[q1];
-            } else {
-                b = int(row[y + 1] - yb);
-            }
-            s_ys[t] = yb + a;
-            TCB_DASSERT(0 <= a && a <= b && b <= int(row[y + 1] - yb));
-            s_end[t] = b - a;  // slice length; consumed below
+            const int2* sy = ls.split + int64_t(y) * (F + 1);
+            const int2 a = sy[q0], b = sy[q1];
+            s_ys[2 * t] = ls.ob[y] + a.x;
+            s_len[2 * t] = no ? b.x - a.x : 0;
+            const int as = qa < q1 ? sy[qa].y : b.y;
+            s_ys[2 * t + 1] = ls.sb[y] + as;
+            s_len[2 * t + 1] = ns ? b.y - as : 0;
         }
-        // stage the owner slice in sub-chunks of hc ids (one pass unless the
-        // slice still exceeds hc with every range split — the largest hubs)
-        for (int64_t cb = xs; cb < xe; cb += hc) {
-            const int len = int(min(int64_t(hc), xe - cb));
-            TCB_DASSERT(len >= 1 && len <= HC && xs >= row[x] && xe <= row[x + 1]);
-            const bool single = (cb == xs) && (cb + len >= xe);
-            const int slots = TCB_FULLTAB ? C_SLOTS : 4 << ceil_log2_dev(max(len, 4));
-            BucketHash h;
-            h.setup(tab, slots);
-            TCB_DASSERT(slots <= C_SLOTS && np <= PC);
-            for (int i = threadIdx.x; i < slots; i += C_THREADS) tab[i] = EMPTY;
-            if (threadIdx.x == 0) s_next = 0;
-            __syncthreads();
-            CuckooHash ch;
-            ch.setup(tab, slots);
-            if (TCB_CUCKOO && threadIdx.x == 0) s_fail = 0;
-            if (TCB_CUCKOO) __syncthreads();
-            if (!(dbg & 2))
-                for (int i = threadIdx.x; i < len; i += C_THREADS) {
-                    const int w = nb[cb + i];
-                    if (!staged(vinfo, w, x, dx, fwd)) continue;
-                    if (TCB_CUCKOO) {
-                        if (!ch.insert(w, level[w] == lx)) s_fail = 1;
-                    } else {
-                        h.insert(w, level[w] == lx);
+        // Passes: one when both owner slices fit the table; otherwise the
+        // OFF slice then the SUP slice, each in sub-chunks of hc ids (only
+        // the largest hubs), each sub-chunk [.., vhi] matched against every
+        // partner's next unread part of the same class.
+        const bool single = no + ns <= hc;
+        for (int phase = single ? 2 : 0; phase < 3; ++phase) {
+            if (phase == 2 && !single) break;
+            const int64_t p0 = phase == 1 ? xs0 : xo0;
+            const int64_t p1 = phase == 0 ? xo1 : xs1;  // phase 2: [xo0, xo1) ∪ [xs0, xs1)
+            const int plen = phase == 2 ? no + ns : int(p1 - p0);
+            for (int cb = 0; cb < plen; cb += hc) {
+                const int len = min(hc, plen - cb);
+                TCB_DASSERT(len >= 1 && len <= HC);
+                BucketHash h;
+                h.setup(tab, C_SLOTS);
+                for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = EMPTY;
+                if (threadIdx.x == 0) {
+                    s_next = 0;
+                    s_fail = 0;
+                }
+                __syncthreads();
+                CuckooHash ch;
+                ch.setup(tab, C_SLOTS);
+                auto owner_id = [&](int i) -> int {  // i-th staged id of this sub-chunk
+                    const int k = cb + i;
+                    return phase == 2 ? (k < no ? L[xo0 + k] : L[xs0 + (k - no)]) : L[p0 + k];
+                };
+                if (!(dbg & 2))
+                    for (int i = threadIdx.x; i < len; i += C_THREADS) {
+                        const int w = owner_id(i);
+                        if (!staged(vinfo, w, x, dx, fwd)) continue;
+                        if (!ch.insert(w)) s_fail = 1;
+                    }
+                if (phase == 2) {
+                    for (int k = threadIdx.x; k < nseg; k += C_THREADS) s_off[k] = s_len[k];
+                } else {
+                    const bool last = cb + len >= plen;
+                    const int vhi = L[p0 + cb + len - 1];
+                    for (int k = threadIdx.x; k < nseg; k += C_THREADS) {
+                        int cnt = 0;
+                        if ((k & 1) == phase && s_len[k] > 0) {
+                            if (last) {
+                                cnt = s_len[k];
+                            } else {  // ids <= vhi in the partner's unread part
+                                int64_t lo = s_ys[k], hi = s_ys[k] + s_len[k];
+                                while (lo < hi) {
+                                    const int64_t mid = (lo + hi) >> 1;
+                                    if (L[mid] <= vhi) lo = mid + 1; else hi = mid;
+                                }
+                                cnt = int(lo - s_ys[k]);
+                            }
+                        }
+                        s_off[k] = cnt;
                     }
                 }
-            if (single) {
-                for (int t = threadIdx.x; t < np; t += C_THREADS) s_off[t] = s_end[t];
-            } else {
-                // sub-chunk [vlo, vhi] of the owner slice: each partner's
-                // matching part starts where its previous part ended
-                const int vhi = nb[cb + len - 1];
-                const bool last = cb + len >= xe;
-                for (int t = threadIdx.x; t < np; t += C_THREADS) {
-                    int64_t a = s_ys[t];
-                    const int64_t e = a + s_end[t];
-                    int64_t lo = a, hi = e;
-                    if (!last)
-                        while (lo < hi) {
-                            const int64_t mid = (lo + hi) >> 1;
-                            if (nb[mid] <= vhi) lo = mid + 1; else hi = mid;
-                        }
-                    else
-                        lo = e;
-                    s_off[t] = int(lo - a);
+                scan_counts(s_off, s_ys, nseg, s_tmp);  // ends with __syncthreads
+                if (s_fail) {  // rare: rebuild this sub-chunk as a bucket table
+                    for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = EMPTY;
+                    __syncthreads();
+                    for (int i = threadIdx.x; i < len; i += C_THREADS) {
+                        const int w = owner_id(i);
+                        if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
+                    }
+                    __syncthreads();
                 }
-            }
-            scan_lengths(s_off, s_ys, np, s_tmp);  // ends with __syncthreads
-            if (TCB_CUCKOO && s_fail) {  // rare: rebuild this sub-chunk as a bucket table
-                for (int i = threadIdx.x; i < slots; i += C_THREADS) tab[i] = EMPTY;
-                __syncthreads();
-                for (int i = threadIdx.x; i < len; i += C_THREADS) {
-                    const int w = nb[cb + i];
-                    if (staged(vinfo, w, x, dx, fwd)) h.insert(w, level[w] == lx);
+                if (!(dbg & 1)) {
+                    if (!s_fail) stream_chunks(L, s_ys, s_off, nseg, &s_next, ch, tl);
+                    else stream_chunks(L, s_ys, s_off, nseg, &s_next, h, tl);
                 }
                 __syncthreads();
-            }
-            if (!(dbg & 1)) {
-                if (TCB_CUCKOO && !s_fail) {
-                    stream_chunks(nb, s_ys, s_off, np, &s_next, ch, tl);
-                } else {
-                    stream_chunks(nb, s_ys, s_off, np, &s_next, h, tl);
-                }
-            }
-            __syncthreads();
-            if (!single) {  // advance partner starts past this sub-chunk
-                for (int t = threadIdx.x; t < np; t += C_THREADS) {
-                    s_ys[t] += s_off[t + 1];  // stream base -> next unread id
-                    s_end[t] -= s_off[t + 1] - s_off[t];
+                // advance every segment past what this sub-chunk consumed
+                for (int k = threadIdx.x; k < nseg; k += C_THREADS) {
+                    s_ys[k] += s_off[k + 1];  // rebased base -> next unread position
+                    s_len[k] -= s_off[k + 1] - s_off[k];
                 }
                 __syncthreads();
             }
         }
-        // an item whose owner slice is empty runs no sub-chunk: without this
+        // an item whose staged slices are empty runs no pass: without this
         // barrier thread 0 could overwrite s_item before all threads read it
         __syncthreads();
     }
@@ -808,10 +904,19 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     if (n == 0 || m == 0) return;
     DevCounters* C = ctx->d_counters;
     const int64_t nnz = 2 * m;
+    require(nnz < (int64_t(1) << 32), "intersection: 2m must be below 2^32");
+    const int64_t nwords = (nnz + 31) / 32;
     int2* vinfo = ctx->wsT<int2>(WS_MISC, n);
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
-    int* split = ctx->wsT<int>(WS_COVER_V, size_t(n) * (F + 1));
+    int2* split = ctx->wsT<int2>(WS_COVER_V, size_t(n) * (F + 1));
+    int32_t* L = ctx->wsT<int32_t>(WS_LISTS, nnz);
+    const size_t cls_bytes = (size_t(nwords + 1) * sizeof(uint2) + 15) / 16 * 16;
+    char* cbuf = static_cast<char*>(
+        ctx->ws(WS_CLASS, cls_bytes + size_t(nwords + 1) * sizeof(unsigned long long)));
+    uint2* cls = reinterpret_cast<uint2*>(cbuf);
+    unsigned long long* pre = reinterpret_cast<unsigned long long*>(cbuf + cls_bytes);
+    int64_t* vb = ctx->wsT<int64_t>(WS_VBEG, 2 * size_t(n + 1));
     // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
     const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
     const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
@@ -829,20 +934,36 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     unsigned long long* fc = &C->scratch[8];
     int64_t* d_ncover = reinterpret_cast<int64_t*>(&C->ncover);
     const int rshift = max(0, bits_for(n) - LOG_F);
+    Lists ls{L, vb, vb + (n + 1), split, rshift};
 
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo);
-    owner_select(ctx, row, src, nb, vinfo, nnz, P, seg, seg + n, d_ncover);
+    TCB_CUDA(cudaMemsetAsync(cls + nwords, 0, sizeof(uint2), ctx->stream));
+    owner_select(ctx, row, src, nb, vinfo, nnz, fwd, cls, P, seg, seg + n, d_ncover);
     ctx->record(3);
-    TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, row, src, nb, nnz, rshift,
-               split);
+    const uint2* ccls = cls;
+    scan_apply(
+        ctx, nwords,
+        [ccls] __device__(int64_t j) -> int64_t {
+            const uint2 c = ccls[j];
+            return int64_t(__popc(c.x)) | (int64_t(__popc(c.y)) << 32);
+        },
+        [pre] __device__(int64_t j, int64_t pos, int64_t) { pre[j] = (unsigned long long)pos; },
+        reinterpret_cast<int64_t*>(pre + nwords));
+    TCB_LAUNCH(ctx, k_list_bounds, grid_for(ctx, n + 1, 256), 256, 0, row, n, ccls,
+               (const unsigned long long*)pre, nwords, vb, vb + (n + 1), split);
+    TCB_LAUNCH(ctx, k_scatter_lists, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
+               (const unsigned long long*)pre, nwords, L);
+    TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
+               (const unsigned long long*)pre, nwords, (const int32_t*)L, (const int64_t*)vb,
+               (const int64_t*)(vb + (n + 1)), rshift, split);
     TCB_LAUNCH(ctx, k_make_items, grid_for(ctx, n, 256), 256, 0, row, (const int64_t*)seg,
-               (const int64_t*)(seg + n), (const int*)split, n, witems, citems, titems, nw, nc,
-               nt, shard, nshards, wt, hc, tiny);
+               (const int64_t*)(seg + n), ls, n, witems, citems, titems, nw, nc, nt, shard,
+               nshards, wt, hc, tiny);
 
     IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
-    const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(PC) * sizeof(int64_t) +
-                       size_t(2 * PC + 1) * sizeof(int);
+    const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(NSEG) * sizeof(int64_t) +
+                       size_t(2 * NSEG + 1) * sizeof(int);
     if (K.warp_blocks == 0) {
         TCB_CUDA(cudaFuncSetAttribute(k_isect_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(wsm)));
@@ -858,15 +979,14 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     ctx->record(5);
     ctx->record(7);  // no separate hub kernel in this design: hub stage = 0
     TCB_LAUNCH(ctx, k_isect_cta, K.cta_blocks, C_THREADS, csm, (const longlong4*)citems,
-               (const unsigned long long*)nc, row, nb, (const int32_t*)P, level,
-               (const int*)split, fc, C, hc, debug_flags(), (const int2*)vinfo, fwd);
+               (const unsigned long long*)nc, ls, (const int32_t*)P, fc, C, hc, debug_flags(),
+               (const int2*)vinfo, fwd);
     ctx->record(6);
     TCB_LAUNCH(ctx, k_isect_warp, K.warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
-               (const unsigned long long*)nw, row, nb, (const int32_t*)P, level, fw, C,
-               (const int2*)vinfo, fwd);
+               (const unsigned long long*)nw, ls, (const int32_t*)P, fw, C, (const int2*)vinfo,
+               fwd);
     TCB_LAUNCH(ctx, k_isect_tiny, ctx->num_sms * 8, 256, 0, (const longlong4*)titems,
-               (const unsigned long long*)nt, row, nb, (const int32_t*)P, level, C,
-               (const int2*)vinfo, fwd);
+               (const unsigned long long*)nt, ls, (const int32_t*)P, C, (const int2*)vinfo, fwd);
 }
 
 }  // namespace tcb

@@ -54,9 +54,9 @@ def _partials(case, rank, world):
                 if level[w] != level[a]:
                     c1 += 1
                     t += 1
-                else:
-                    c2 += 1
-                    t += int(w > b)
+                elif w > b:  # a < b: the one same-level apex T keeps (_kernels.py:687)
+                    c2 += 3  # the device tallies c2 in the reference's units (3 per triangle)
+                    t += 1
     return t, c1, c2
 
 
