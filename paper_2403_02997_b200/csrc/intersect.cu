@@ -344,8 +344,7 @@ __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restri
 __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
                               const uint2* __restrict__ cls,
                               const unsigned long long* __restrict__ pre, int64_t nw,
-                              int64_t* __restrict__ ob, int64_t* __restrict__ sb,
-                              int2* __restrict__ split) {
+                              int64_t* __restrict__ ob, int64_t* __restrict__ sb) {
     const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v <= n; v += stride) {
@@ -353,15 +352,6 @@ __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
         const int64_t o = rank_off(cls, pre, p), s = noff + rank_sup(cls, pre, p);
         ob[v] = o;
         sb[v] = s;
-        if (v == n) continue;
-        // a class-empty list has an all-zero split row (k_split_points writes
-        // only rows with entries)
-        const int64_t p1 = row[v + 1];
-        int* sp = reinterpret_cast<int*>(split + v * (F + 1));
-        if (rank_off(cls, pre, p1) == o)
-            for (int q = 0; q <= F; ++q) sp[2 * q] = 0;
-        if (noff + rank_sup(cls, pre, p1) == s)
-            for (int q = 0; q <= F; ++q) sp[2 * q + 1] = 0;
     }
 }
 
@@ -601,55 +591,60 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
 // ---------------------------------------------------------------------------
 // 6. CTA tier
 //
-// Stream segments: partner t contributes segment 2t (its OFF slice) and 2t+1
-// (its SUP slice); a hit counts for c1 or the SUP tally by segment parity.
+// Every partner t has two unread slices, OFF at index t and SUP at PC + t
+// (s_pos / s_len).  Each pass takes a count from every slice, and the
+// non-empty ones are compacted into the stream table s_seg: all OFF slices
+// first, then all SUP slices, so an element's class is just
+// (stream index >= tsup) and a walk never steps over an empty slice.
+// s_seg[k] = (first stream index of slice k, its base): element i of slice k
+// is L[base + i] (uint32 arithmetic; 2m < 2^32).
 
-// Largest k < nseg with s_off[k] <= c0 (s_off[0] = 0 <= c0): three steps,
-// two 32-way ballots over a 2048-entry table and one compare.
-__device__ __forceinline__ int find_segment(const int* s_off, int nseg, int c0) {
+// Largest k < nseg with s_seg[k].x <= c0 (s_seg[0].x = 0 <= c0): two 32-way
+// ballots over a 2048-entry table and one compare.
+__device__ __forceinline__ int find_segment(const int2* s_seg, int nseg, int c0) {
     const int lane = int(lane_id());
     const int j = lane * 64;
-    const unsigned b1 = __ballot_sync(0xffffffffu, j < nseg && s_off[j] <= c0);
+    const unsigned b1 = __ballot_sync(0xffffffffu, j < nseg && s_seg[j].x <= c0);
     const int kb = (31 - __clz(b1)) * 64;
     const int j2 = kb + lane * 2;
-    const unsigned b2 = __ballot_sync(0xffffffffu, j2 < nseg && s_off[j2] <= c0);
+    const unsigned b2 = __ballot_sync(0xffffffffu, j2 < nseg && s_seg[j2].x <= c0);
     const int k = kb + 2 * (31 - __clz(b2));
-    return k + ((k + 1 < nseg && s_off[k + 1] <= c0) ? 1 : 0);
+    return k + ((k + 1 < nseg && s_seg[k + 1].x <= c0) ? 1 : 0);
 }
 
-// A chunk that crosses segment boundaries: each lane walks forward from the
-// chunk's first segment k0; a lane crosses a boundary in few of its J
+// A chunk that crosses slice boundaries: each lane walks forward from the
+// chunk's first slice k0; a lane crosses a boundary in few of its J
 // elements.  FULL: the chunk holds CHUNK elements (no bounds checks).
 template <bool FULL, typename Probe>
-__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const int64_t* s_ys,
-                                            const int* s_off, int nseg, int k0, int c0, int c1,
+__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const int2* s_seg,
+                                            int nseg, int k0, int c0, int c1, int tsup,
                                             const Probe& h, uint32_t& co, uint32_t& cs) {
     constexpr int J = CHUNK / 32;
     int k = k0;
-    int next = s_off[k + 1];
-    const int32_t* q = L + s_ys[k];
+    int nx = s_seg[k + 1].x;
+    uint32_t base = uint32_t(s_seg[k].y);
     const int i0 = c0 + int(lane_id());
+    // this lane's elements j >= jt come from SUP slices (stream index >= tsup)
+    const int jt = min(J, max(0, (tsup - i0 + 31) >> 5));
     int w[J];
-    uint32_t par = 0;  // bit j: element j came from a SUP segment
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int i = i0 + 32 * j;
         w[j] = -1;
         if (FULL || i < c1) {
-            if (next <= i) {
+            if (nx <= i) {
                 do {
                     TCB_DASSERT(k + 1 < nseg);
                     ++k;
-                    next = s_off[k + 1];
-                } while (next <= i);
-                q = L + s_ys[k];
+                    nx = s_seg[k + 1].x;
+                } while (nx <= i);
+                base = uint32_t(s_seg[k].y);
             }
 #ifdef TCB_NOLOAD  // measurement-only variant: probe without streaming
-            w[j] = int((uint32_t(i) * 2654435761u) >> 8) + int(reinterpret_cast<uintptr_t>(q) & 1);
+            w[j] = int(((base + uint32_t(i)) * 2654435761u) >> 8);
 #else
-            w[j] = q[i];
+            w[j] = L[base + uint32_t(i)];
 #endif
-            par |= uint32_t(k & 1) << j;
         }
     }
     uint32_t all = 0, sup = 0;
@@ -658,24 +653,21 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
         if (!FULL && w[j] < 0) continue;
         const uint32_t hv = h.hit(w[j]);
         all += hv;
-        sup += hv & (par >> j);
+        sup += j >= jt ? hv : 0u;
     }
     co += all - sup;
     cs += sup;
 }
 
-// Warps consume the flattened stream of segments in CHUNK grabs; element i
-// belongs to segment k with s_off[k] <= i < s_off[k+1].  A chunk that lies
-// inside one segment (the common case: slices average hundreds of ids) takes
-// a warp-uniform fast path with coalesced loads and no per-element
-// segment bookkeeping.
+// Warps consume the flattened stream in CHUNK grabs.  A chunk that lies
+// inside one slice takes a warp-uniform fast path with coalesced loads and
+// no per-element bookkeeping.
 template <typename Probe>
-__device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, const int64_t* s_ys,
-                                              const int* s_off, int nseg, int* s_next,
+__device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, const int2* s_seg,
+                                              int nseg, int total, int tsup, int* s_next,
                                               const Probe& h, Tally& tl) {
     constexpr int J = CHUNK / 32;
-    const int total = s_off[nseg];
-    TCB_DASSERT(nseg >= 1 && nseg <= NSEG && total >= 0);
+    TCB_DASSERT(nseg <= NSEG && total >= 0);
     const int lane = int(lane_id());
     while (true) {
         int c0 = 0;
@@ -683,20 +675,19 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, con
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (c0 >= total) break;
         const int c1 = min(total, c0 + CHUNK);
-        const int k0 = find_segment(s_off, nseg, c0);
-        TCB_DASSERT(k0 >= 0 && k0 < nseg && s_off[k0] <= c0 && c0 < s_off[k0 + 1]);
+        const int k0 = find_segment(s_seg, nseg, c0);
+        TCB_DASSERT(k0 >= 0 && k0 < nseg && s_seg[k0].x <= c0 && c0 < s_seg[k0 + 1].x);
         uint32_t co = 0, cs = 0;
-        if (s_off[k0 + 1] >= c1) {
-            // fast path: one segment
-            const int32_t* p = L + s_ys[k0] + c0 + lane;
+        if (s_seg[k0 + 1].x >= c1) {
+            // fast path: one slice
+            const uint32_t base = uint32_t(s_seg[k0].y) + uint32_t(c0 + lane);
+            const int32_t* p = L + base;
             int w[J];
             uint32_t hits = 0;
             if (c1 - c0 == CHUNK) {
 #ifdef TCB_NOLOAD
 #pragma unroll
-                for (int j = 0; j < J; ++j)
-                    w[j] = int((uint32_t(c0 + lane + 32 * j) * 2654435761u) >> 8) +
-                           int(reinterpret_cast<uintptr_t>(p) & 1);
+                for (int j = 0; j < J; ++j) w[j] = int(((base + 32u * j) * 2654435761u) >> 8);
 #else
 #pragma unroll
                 for (int j = 0; j < J; ++j) w[j] = p[32 * j];
@@ -712,39 +703,49 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, con
                     hits += h.hit(w[j]);
                 }
             }
-            if (k0 & 1) cs = hits; else co = hits;
+            if (c0 >= tsup) cs = hits; else co = hits;
         } else if (c1 - c0 == CHUNK) {
-            cross_chunk<true>(L, s_ys, s_off, nseg, k0, c0, c1, h, co, cs);
+            cross_chunk<true>(L, s_seg, nseg, k0, c0, c1, tsup, h, co, cs);
         } else {
-            cross_chunk<false>(L, s_ys, s_off, nseg, k0, c0, c1, h, co, cs);
+            cross_chunk<false>(L, s_seg, nseg, k0, c0, c1, tsup, h, co, cs);
         }
         tl.c1 += co;
         tl.sup += cs;
     }
 }
 
-// Exclusive block scan of the per-segment counts in s_off[0..nseg) (thread t
-// holds segments 4t..4t+3) into s_off[0..nseg]; s_ys[k] is rebased so that
-// stream element i of segment k is L[s_ys[k] + i].
-__device__ __forceinline__ void scan_counts(int* s_off, int64_t* s_ys, int nseg, int64_t* s_tmp) {
-    __syncthreads();  // counts were written with a different thread->segment map
-    const int t = threadIdx.x;
-    int c[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) c[i] = 4 * t + i < nseg ? s_off[4 * t + i] : 0;
-    int64_t tot;
-    int64_t ex = block_exclusive_scan<C_THREADS>(int64_t(c[0] + c[1] + c[2] + c[3]), s_tmp, tot);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int k = 4 * t + i;
-        if (k < nseg) {
-            s_off[k] = int(ex);
-            s_ys[k] -= ex;
-        }
-        ex += c[i];
+// Block-wide exclusive scan of a (int64, int) pair (one value per thread).
+__device__ __forceinline__ void block_scan_pair(int64_t a, int b, int64_t& ea, int& eb,
+                                                int64_t& ta, int& tb, int64_t* sa, int* sb) {
+    constexpr int NW = C_THREADS / 32;
+    const int w = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const int64_t ia = warp_inclusive_scan(a);
+    const int ib = warp_inclusive_scan(b);
+    if (lane == 31) {
+        sa[w] = ia;
+        sb[w] = ib;
     }
-    if (t == 0) s_off[nseg] = int(tot);
     __syncthreads();
+    if (w == 0) {
+        const int64_t xa = lane < NW ? sa[lane] : 0;
+        const int xb = lane < NW ? sb[lane] : 0;
+        const int64_t ya = warp_inclusive_scan(xa);
+        const int yb = warp_inclusive_scan(xb);
+        if (lane < NW) {
+            sa[lane] = ya - xa;
+            sb[lane] = yb - xb;
+        }
+        if (lane == NW - 1) {
+            sa[NW] = ya;
+            sb[NW] = yb;
+        }
+    }
+    __syncthreads();
+    ea = sa[w] + ia - a;
+    eb = sb[w] + ib - b;
+    ta = sa[NW];
+    tb = sb[NW];
 }
 
 #ifndef TCB_CTA_PER_SM
@@ -756,10 +757,11 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 DevCounters* C, int hc, int dbg, const int2* __restrict__ vinfo, int fwd) {
     extern __shared__ uint4 smem4[];
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS
-    int64_t* s_ys = reinterpret_cast<int64_t*>(tab + C_SLOTS);    // NSEG: next unread position
-    int* s_off = reinterpret_cast<int*>(s_ys + NSEG);             // NSEG + 1
-    int* s_len = s_off + NSEG + 1;                                // NSEG: unread length
-    __shared__ int64_t s_tmp[C_THREADS / 32 + 1];
+    int2* s_seg = reinterpret_cast<int2*>(tab + C_SLOTS);         // NSEG + 1 (stream table)
+    uint32_t* s_pos = reinterpret_cast<uint32_t*>(s_seg + NSEG + 1);  // NSEG: next unread position
+    int* s_len = reinterpret_cast<int*>(s_pos + NSEG);            // NSEG: unread length
+    __shared__ int64_t s_ta[C_THREADS / 32 + 1];
+    __shared__ int s_tb[C_THREADS / 32 + 1];
     __shared__ unsigned long long s_item;
     __shared__ int s_next;
     __shared__ int s_fail;
@@ -785,16 +787,15 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         // SUP(y) ids below x's id range cannot be in SUP(x)
         const int qa = max(q0, x >> ls.rshift);
         const int np = int(item.z - item.y);
-        const int nseg = 2 * np;
         for (int t = threadIdx.x; t < np; t += C_THREADS) {
             const int y = P[item.y + t];
             const int2* sy = ls.split + int64_t(y) * (F + 1);
             const int2 a = sy[q0], b = sy[q1];
-            s_ys[2 * t] = ls.ob[y] + a.x;
-            s_len[2 * t] = no ? b.x - a.x : 0;
+            s_pos[t] = uint32_t(ls.ob[y] + a.x);
+            s_len[t] = no ? b.x - a.x : 0;
             const int as = qa < q1 ? sy[qa].y : b.y;
-            s_ys[2 * t + 1] = ls.sb[y] + as;
-            s_len[2 * t + 1] = ns ? b.y - as : 0;
+            s_pos[PC + t] = uint32_t(ls.sb[y] + as);
+            s_len[PC + t] = ns ? b.y - as : 0;
         }
         // Passes: one when both owner slices fit the table; otherwise the
         // OFF slice then the SUP slice, each in sub-chunks of hc ids (only
@@ -829,29 +830,75 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         if (!staged(vinfo, w, x, dx, fwd)) continue;
                         if (!ch.insert(w)) s_fail = 1;
                     }
-                if (phase == 2) {
-                    for (int k = threadIdx.x; k < nseg; k += C_THREADS) s_off[k] = s_len[k];
-                } else {
-                    const bool last = cb + len >= plen;
-                    const int vhi = L[p0 + cb + len - 1];
-                    for (int k = threadIdx.x; k < nseg; k += C_THREADS) {
-                        int cnt = 0;
-                        if ((k & 1) == phase && s_len[k] > 0) {
-                            if (last) {
-                                cnt = s_len[k];
-                            } else {  // ids <= vhi in the partner's unread part
-                                int64_t lo = s_ys[k], hi = s_ys[k] + s_len[k];
+                // this pass's count from each slice of partners 2t, 2t+1
+                // (slots 0, 1: OFF; 2, 3: SUP), then the stream table
+                const bool last = cb + len >= plen;
+                const int vhi = phase == 2 ? 0 : L[p0 + cb + len - 1];
+                int cnt[4];
+                int slot[4];
+                {
+                    const int t2 = 2 * threadIdx.x;
+                    slot[0] = t2;
+                    slot[1] = t2 + 1;
+                    slot[2] = PC + t2;
+                    slot[3] = PC + t2 + 1;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int k = slot[r];
+                        int c = 0;
+                        if ((k & (PC - 1)) < np) {
+                            const int ln = s_len[k];
+                            if (phase == 2 || (ln > 0 && (r >> 1) == phase && last)) {
+                                c = ln;
+                            } else if (ln > 0 && (r >> 1) == phase) {
+                                // ids <= vhi in the unread part
+                                uint32_t lo = s_pos[k], hi = s_pos[k] + uint32_t(ln);
                                 while (lo < hi) {
-                                    const int64_t mid = (lo + hi) >> 1;
+                                    const uint32_t mid = lo + ((hi - lo) >> 1);
                                     if (L[mid] <= vhi) lo = mid + 1; else hi = mid;
                                 }
-                                cnt = int(lo - s_ys[k]);
+                                c = int(lo - s_pos[k]);
                             }
                         }
-                        s_off[k] = cnt;
+                        cnt[r] = c;
                     }
                 }
-                scan_counts(s_off, s_ys, nseg, s_tmp);  // ends with __syncthreads
+                int64_t eo;  // exclusive element prefix: OFF low 32 bits, SUP high
+                int en;      // exclusive non-empty prefix: OFF low 16 bits, SUP high
+                int64_t to;
+                int tn;
+                block_scan_pair(int64_t(cnt[0] + cnt[1]) | (int64_t(cnt[2] + cnt[3]) << 32),
+                                int(cnt[0] > 0) + int(cnt[1] > 0) +
+                                    ((int(cnt[2] > 0) + int(cnt[3] > 0)) << 16),
+                                eo, en, to, tn, s_ta, s_tb);
+                const int tsup = int(to & 0xFFFFFFFF);        // OFF elements come first
+                const int total = tsup + int(to >> 32);
+                const int noff = tn & 0xFFFF;
+                const int nseg = noff + (tn >> 16);
+                {
+                    int e_o = int(eo & 0xFFFFFFFF), e_s = tsup + int(eo >> 32);
+                    int n_o = en & 0xFFFF, n_s = noff + (en >> 16);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int c = cnt[r];
+                        if (c == 0) continue;
+                        const int k = slot[r];
+                        const bool isup = r >= 2;
+                        const int e = isup ? e_s : e_o;
+                        s_seg[isup ? n_s : n_o] = make_int2(e, int(s_pos[k] - uint32_t(e)));
+                        s_pos[k] += uint32_t(c);
+                        s_len[k] -= c;
+                        if (isup) {
+                            e_s += c;
+                            ++n_s;
+                        } else {
+                            e_o += c;
+                            ++n_o;
+                        }
+                    }
+                    if (threadIdx.x == 0) s_seg[nseg] = make_int2(total, 0);
+                }
+                __syncthreads();
                 if (s_fail) {  // rare: rebuild this sub-chunk as a bucket table
                     for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = EMPTY;
                     __syncthreads();
@@ -862,14 +909,8 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                     __syncthreads();
                 }
                 if (!(dbg & 1)) {
-                    if (!s_fail) stream_chunks(L, s_ys, s_off, nseg, &s_next, ch, tl);
-                    else stream_chunks(L, s_ys, s_off, nseg, &s_next, h, tl);
-                }
-                __syncthreads();
-                // advance every segment past what this sub-chunk consumed
-                for (int k = threadIdx.x; k < nseg; k += C_THREADS) {
-                    s_ys[k] += s_off[k + 1];  // rebased base -> next unread position
-                    s_len[k] -= s_off[k + 1] - s_off[k];
+                    if (!s_fail) stream_chunks(L, s_seg, nseg, total, tsup, &s_next, ch, tl);
+                    else stream_chunks(L, s_seg, nseg, total, tsup, &s_next, h, tl);
                 }
                 __syncthreads();
             }
@@ -950,7 +991,10 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         [pre] __device__(int64_t j, int64_t pos, int64_t) { pre[j] = (unsigned long long)pos; },
         reinterpret_cast<int64_t*>(pre + nwords));
     TCB_LAUNCH(ctx, k_list_bounds, grid_for(ctx, n + 1, 256), 256, 0, row, n, ccls,
-               (const unsigned long long*)pre, nwords, vb, vb + (n + 1), split);
+               (const unsigned long long*)pre, nwords, vb, vb + (n + 1));
+    // rows of class-empty lists stay zero (k_split_points writes only rows
+    // with entries)
+    TCB_CUDA(cudaMemsetAsync(split, 0, size_t(n) * (F + 1) * sizeof(int2), ctx->stream));
     TCB_LAUNCH(ctx, k_scatter_lists, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
                (const unsigned long long*)pre, nwords, L);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
@@ -962,8 +1006,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
 
     IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
-    const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(NSEG) * sizeof(int64_t) +
-                       size_t(2 * NSEG + 1) * sizeof(int);
+    const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(NSEG + 1) * sizeof(int2) +
+                       size_t(2 * NSEG) * sizeof(int);
     if (K.warp_blocks == 0) {
         TCB_CUDA(cudaFuncSetAttribute(k_isect_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(wsm)));
