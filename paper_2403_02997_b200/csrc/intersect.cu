@@ -223,11 +223,14 @@ __device__ __forceinline__ bool staged(const int2* __restrict__ vinfo, int w, in
     return dw > dx || (dw == dx && w < x);
 }
 
-// Per-vertex list bounds: OFF(v) = L[ob[v], ob[v+1]), SUP(v) = L[sb[v], sb[v+1]).
+// Per-vertex list bounds: OFF(v) = L[ob(v), ob(v+1)), SUP(v) = L[sb(v), sb(v+1)),
+// kept as one uint2 (ob, sb) per vertex so a vertex's bounds share a sector
+// (positions < 2m < 2^32).
 struct Lists {
     const int32_t* __restrict__ L;
-    const int64_t* __restrict__ ob;
-    const int64_t* __restrict__ sb;
+    const uint2* __restrict__ vb;
+    __device__ __forceinline__ int64_t ob(int64_t v) const { return int64_t(vb[v].x); }
+    __device__ __forceinline__ int64_t sb(int64_t v) const { return int64_t(vb[v].y); }
     const int2* __restrict__ split;  // [v*(F+1) + r] = (OFF pos, SUP pos) of range r
     int rshift;
 };
@@ -344,14 +347,13 @@ __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restri
 __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
                               const uint2* __restrict__ cls,
                               const unsigned long long* __restrict__ pre, int64_t nw,
-                              int64_t* __restrict__ ob, int64_t* __restrict__ sb) {
+                              uint2* __restrict__ vb) {
     const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v <= n; v += stride) {
         const int64_t p = row[v];
-        const int64_t o = rank_off(cls, pre, p), s = noff + rank_sup(cls, pre, p);
-        ob[v] = o;
-        sb[v] = s;
+        vb[v] = make_uint2(uint32_t(rank_off(cls, pre, p)),
+                           uint32_t(noff + rank_sup(cls, pre, p)));
     }
 }
 
@@ -376,8 +378,8 @@ __global__ void k_scatter_lists(const int32_t* __restrict__ nb, int64_t nnz,
 __global__ void k_split_points(const int32_t* __restrict__ src, int64_t nnz,
                                const uint2* __restrict__ cls,
                                const unsigned long long* __restrict__ pre, int64_t nw,
-                               const int32_t* __restrict__ L, const int64_t* __restrict__ ob,
-                               const int64_t* __restrict__ sb, int rshift,
+                               const int32_t* __restrict__ L, const uint2* __restrict__ vb,
+                               int rshift,
                                int2* __restrict__ split) {
     const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -388,8 +390,9 @@ __global__ void k_split_points(const int32_t* __restrict__ src, int64_t nnz,
         if (!off && !(c.y & bit)) continue;
         const int v = src[e];
         const int64_t g = off ? rank_off(cls, pre, e) : noff + rank_sup(cls, pre, e);
-        const int64_t b0 = off ? ob[v] : sb[v];
-        const int64_t b1 = off ? ob[v + 1] : sb[v + 1];
+        const uint2 v0 = vb[v], v1 = vb[v + 1];
+        const int64_t b0 = off ? v0.x : v0.y;
+        const int64_t b1 = off ? v1.x : v1.y;
         const int k = int(g - b0);
         const int r = L[g] >> rshift;
         const int prev = g == b0 ? -1 : (L[g - 1] >> rshift);
@@ -423,7 +426,7 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         if (e <= s) continue;
         // nothing staged (no OFF neighbours, no same-level neighbour above
         // x): no edge of x can have an apex
-        const int64_t st = (ls.ob[x + 1] - ls.ob[x]) + (ls.sb[x + 1] - ls.sb[x]);
+        const int64_t st = (ls.ob(x + 1) - ls.ob(x)) + (ls.sb(x + 1) - ls.sb(x));
         if (st == 0) continue;
         if (d <= tiny) {  // <= TINY partners, each with <= TINY ids
             if (!mine(x, 0)) continue;
@@ -494,8 +497,8 @@ __global__ void __launch_bounds__(256)
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < nitems; it += stride) {
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int64_t o0 = ls.ob[x], o1 = ls.ob[x + 1], s0 = ls.sb[x];
-        const int no = int(o1 - o0), nx = no + int(ls.sb[x + 1] - s0);
+        const int64_t o0 = ls.ob(x), o1 = ls.ob(x + 1), s0 = ls.sb(x);
+        const int no = int(o1 - o0), nx = no + int(ls.sb(x + 1) - s0);
         const int dx = fwd ? vinfo[x].y : 0;
         int a[TINY];
 #pragma unroll
@@ -507,7 +510,7 @@ __global__ void __launch_bounds__(256)
         }
         for (int64_t p = item.y; p < item.z; ++p) {
             const int y = P[p];
-            const int64_t y0 = ls.ob[y], y1 = ls.ob[y + 1], y2 = ls.sb[y], y3 = ls.sb[y + 1];
+            const int64_t y0 = ls.ob(y), y1 = ls.ob(y + 1), y2 = ls.sb(y), y3 = ls.sb(y + 1);
             for (int64_t j = y0; j < y1; ++j) {
                 const int w = ls.L[j];
                 bool hit = false;
@@ -552,8 +555,8 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
         if (it >= nitems) break;
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int64_t o0 = ls.ob[x], s0 = ls.sb[x];
-        const int no = int(ls.ob[x + 1] - o0), nx = no + int(ls.sb[x + 1] - s0);
+        const int64_t o0 = ls.ob(x), s0 = ls.sb(x);
+        const int no = int(ls.ob(x + 1) - o0), nx = no + int(ls.sb(x + 1) - s0);
         const int dx = fwd ? vinfo[x].y : 0;
         const int qx = x >> ls.rshift;
         const int slots = max(16, 2 << ceil_log2_dev(nx));
@@ -570,13 +573,13 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
             int ydo = 0, yds = 0;
             if (j < item.z) {
                 const int y = P[j];
-                yo = ls.ob[y];
-                ydo = int(ls.ob[y + 1] - yo);
+                yo = ls.ob(y);
+                ydo = int(ls.ob(y + 1) - yo);
                 // SUP(y) ids below x's id range cannot be in SUP(x)
-                const int64_t sy = ls.sb[y];
+                const int64_t sy = ls.sb(y);
                 const int a = ls.split[int64_t(y) * (F + 1) + qx].y;
                 ys = sy + a;
-                yds = int(ls.sb[y + 1] - sy) - a;
+                yds = int(ls.sb(y + 1) - sy) - a;
             }
             tl.c1 += probe_batch(ls.L, yo, ydo, h);
             tl.sup += probe_batch(ls.L, ys, yds, h);
@@ -767,6 +770,12 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     __shared__ int s_fail;
     const int32_t* __restrict__ L = ls.L;
     const unsigned long long nitems = *nitems_p;
+#ifdef TCB_NOSTREAM  // measurement-only variant: item setup and staging without streaming
+    dbg |= 1;
+#endif
+#ifdef TCB_NOINSERT  // measurement-only variant: no staging
+    dbg |= 2;
+#endif
     Tally tl;
     while (true) {
         if (threadIdx.x == 0) s_item = atomicAdd(fetch, 1ull);
@@ -780,22 +789,45 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         const int2* sx = ls.split + int64_t(x) * (F + 1);
         const int2 ax = sx[q0], bx = sx[q1];
         // the owner's staged slices: OFF [xo0, xo1), SUP [xs0, xs1)
-        const int64_t xo0 = ls.ob[x] + ax.x, xo1 = ls.ob[x] + bx.x;
-        const int64_t xs0 = ls.sb[x] + ax.y, xs1 = ls.sb[x] + bx.y;
+        const int64_t xo0 = ls.ob(x) + ax.x, xo1 = ls.ob(x) + bx.x;
+        const int64_t xs0 = ls.sb(x) + ax.y, xs1 = ls.sb(x) + bx.y;
         const int no = int(xo1 - xo0), ns = int(xs1 - xs0);
         const int dx = fwd ? vinfo[x].y : 0;
         // SUP(y) ids below x's id range cannot be in SUP(x)
         const int qa = max(q0, x >> ls.rshift);
         const int np = int(item.z - item.y);
-        for (int t = threadIdx.x; t < np; t += C_THREADS) {
-            const int y = P[item.y + t];
-            const int2* sy = ls.split + int64_t(y) * (F + 1);
-            const int2 a = sy[q0], b = sy[q1];
-            s_pos[t] = uint32_t(ls.ob[y] + a.x);
-            s_len[t] = no ? b.x - a.x : 0;
-            const int as = qa < q1 ? sy[qa].y : b.y;
-            s_pos[PC + t] = uint32_t(ls.sb[y] + as);
-            s_len[PC + t] = ns ? b.y - as : 0;
+        // partners t and t + C_THREADS of this thread: both ids are loaded
+        // before either partner's rows, so the two dependent chains overlap
+        static_assert(PC == 2 * C_THREADS, "two partners per thread");
+        {
+            int yy[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int t = threadIdx.x + r * C_THREADS;
+                yy[r] = t < np ? P[item.y + t] : -1;
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int t = threadIdx.x + r * C_THREADS;
+                if (yy[r] < 0) continue;
+                const int y = yy[r];
+                const int2* sy = ls.split + int64_t(y) * (F + 1);
+                const uint2 v0 = ls.vb[y];
+                // range ends at 0 / F come from the bounds, not the split row
+                int2 a = make_int2(0, 0), b;
+                if (q0 > 0) a = sy[q0];
+                if (q1 == F) {
+                    const uint2 v1 = ls.vb[y + 1];
+                    b = make_int2(int(v1.x - v0.x), int(v1.y - v0.y));
+                } else {
+                    b = sy[q1];
+                }
+                const int as = qa < q1 ? sy[qa].y : b.y;
+                s_pos[t] = v0.x + uint32_t(a.x);
+                s_len[t] = no ? b.x - a.x : 0;
+                s_pos[PC + t] = v0.y + uint32_t(as);
+                s_len[PC + t] = ns ? b.y - as : 0;
+            }
         }
         // Passes: one when both owner slices fit the table; otherwise the
         // OFF slice then the SUP slice, each in sub-chunks of hc ids (only
@@ -957,7 +989,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         ctx->ws(WS_CLASS, cls_bytes + size_t(nwords + 1) * sizeof(unsigned long long)));
     uint2* cls = reinterpret_cast<uint2*>(cbuf);
     unsigned long long* pre = reinterpret_cast<unsigned long long*>(cbuf + cls_bytes);
-    int64_t* vb = ctx->wsT<int64_t>(WS_VBEG, 2 * size_t(n + 1));
+    uint2* vb = ctx->wsT<uint2>(WS_VBEG, size_t(n + 1));
     // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
     const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
     const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
@@ -975,7 +1007,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     unsigned long long* fc = &C->scratch[8];
     int64_t* d_ncover = reinterpret_cast<int64_t*>(&C->ncover);
     const int rshift = max(0, bits_for(n) - LOG_F);
-    Lists ls{L, vb, vb + (n + 1), split, rshift};
+    Lists ls{L, vb, split, rshift};
 
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo);
     TCB_CUDA(cudaMemsetAsync(cls + nwords, 0, sizeof(uint2), ctx->stream));
@@ -991,15 +1023,15 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         [pre] __device__(int64_t j, int64_t pos, int64_t) { pre[j] = (unsigned long long)pos; },
         reinterpret_cast<int64_t*>(pre + nwords));
     TCB_LAUNCH(ctx, k_list_bounds, grid_for(ctx, n + 1, 256), 256, 0, row, n, ccls,
-               (const unsigned long long*)pre, nwords, vb, vb + (n + 1));
+               (const unsigned long long*)pre, nwords, vb);
     // rows of class-empty lists stay zero (k_split_points writes only rows
     // with entries)
     TCB_CUDA(cudaMemsetAsync(split, 0, size_t(n) * (F + 1) * sizeof(int2), ctx->stream));
     TCB_LAUNCH(ctx, k_scatter_lists, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
                (const unsigned long long*)pre, nwords, L);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
-               (const unsigned long long*)pre, nwords, (const int32_t*)L, (const int64_t*)vb,
-               (const int64_t*)(vb + (n + 1)), rshift, split);
+               (const unsigned long long*)pre, nwords, (const int32_t*)L, (const uint2*)vb,
+               rshift, split);
     TCB_LAUNCH(ctx, k_make_items, grid_for(ctx, n, 256), 256, 0, row, (const int64_t*)seg,
                (const int64_t*)(seg + n), ls, n, witems, citems, titems, nw, nc, nt, shard,
                nshards, wt, hc, tiny);

@@ -55,3 +55,17 @@ for name_, L, cnt in (("OFF", so, n_off[p] * 1.0), ("SUP", ss, above * 1.0)):
 for g in (1, 2, 4, 8, 16, 32):
     m = G == g
     print(f"  G={g:2d}: edges {int(m.sum()):>10}  ids {float((n_off[p] + above)[m].sum()) / tot * 100:6.2f}%")
+# CTA items: ceil(partners / 1024) per owner and group, and stream ids per item
+own_ids, per_owner = torch.unique(x, return_counts=True)
+first = torch.searchsorted(x.sort().values, own_ids)
+Gx = G[x.argsort()][first]
+items = ((per_owner + 1023) // 1024) * Gx
+tot_items = int(items.sum())
+print(f"  CTA items {tot_items}, owners {len(own_ids)}, stream ids/item {tot / max(tot_items, 1):.0f}")
+ids_per_owner = torch.zeros(n, dtype=torch.float64, device=x.device)
+ids_per_owner.index_add_(0, x, (n_off[p] + above).double())
+ipi = ids_per_owner[own_ids] / items.double()
+for lo, hi in [(0, 1024), (1024, 4096), (4096, 16384), (16384, 65536), (65536, 1e12)]:
+    m = (ipi >= lo) & (ipi < hi)
+    print(f"   items with [{lo},{hi}) ids: {int(items[m].sum()):>9} items, "
+          f"{float(ids_per_owner[own_ids][m].sum()) / tot * 100:6.2f}% of ids")
