@@ -14,37 +14,42 @@
 //
 // The level rule is applied before the intersection instead of after it.
 // Both endpoints are on level L, so an apex w is on another level from both
-// (counted in c1) or on L for both; a same-level apex counts for T only when
-// w > max(u, v) (_kernels.py:687), i.e. w > x and w > y.  Every CSR row is
-// therefore split into two id-sorted lists:
-//     OFF(v) = neighbours on another level,
-//     SUP(v) = neighbours on v's level with a larger id,
-// and an edge's apexes are exactly OFF(x)∩OFF(y) (c1) plus SUP(x)∩SUP(y)
-// (the same-level apexes the reference's T keeps).  Same-level neighbours
+// (counted in c1) or on L for both.  Every CSR row is split into two lists:
+//     OFF(v) = neighbours on another level (id-sorted),
+//     UP(v)  = neighbours on v's level that rank above v in the owner order
+//              (degree desc, id asc), sorted by degree bucket, largest first,
+// and an edge (owner x, partner p) has apexes OFF(x)∩OFF(p) (c1) and
+// UP(x)∩UP(p) (same level, ranked above both endpoints).  Every same-level
+// triangle a > b > c (owner order) is therefore found exactly once, at its
+// edge (b, c) with apex a — the reference keeps exactly one apex per such
+// triangle too (w > max(u, v), _kernels.py:687) — so the SUP tally equals
+// the reference's T - c1 and its c2 (every same-level hit, 3 per triangle,
+// _kernels.py:745-748) is 3 x this tally; the counters hold c2 in those
+// units.  Ranking by degree keeps the same-level stream short: p streams
+// only the part of UP(p) in degree buckets >= x's (a prefix, ucnt table),
+// and hubs have few neighbours above them.  Same-level neighbours ranked
 // below the endpoint are never read, and a hit needs no level lookup: the
-// list it was streamed from says which tally it belongs to.  Over the full
-// cover set each all-horizontal triangle is kept at exactly one of its three
-// edges, so the reference's c2 (every same-level hit, 3 per such triangle)
-// is 3 x the SUP tally — the counters hold c2 in the reference's units.
+// list it was streamed from says which tally it belongs to.
 //
 //  1. owner_select: ordered compaction over the CSR entries (x, y) keeping
 //     level[x]==level[y] && owns(x, y).  Entries are in row order, so each
 //     owner's partners come out contiguous: P[seg_beg[x], seg_end[x]).  The
-//     same pass writes the OFF/SUP class bits of every entry.
+//     same pass writes the OFF/UP class bits of every entry.
 //  2. lists: word prefixes of the class bits give every entry its slot in
-//     the OFF or SUP array (no second scan); one scatter writes both.
+//     the OFF array and every row its UP range (no second scan); UP rows are
+//     counting-sorted by degree bucket (per-row histogram, prefix, scatter).
 //  3. split points: the id space is cut into F equal ranges; split[v][r] is
-//     the position in OFF(v) / SUP(v) of the first id in range r.  An owner
-//     whose staged lists exceed the table is staged one group of ranges at a
-//     time, and every partner's matching slices are read from the table.
+//     the position in OFF(v) of the first id in range r.  An owner whose OFF
+//     list exceeds the table is staged one group of ranges at a time, and
+//     every partner's matching slices are read from the table.
 //  4. make_items: owners with d(x) <= TINY -> thread items; <= WT -> warp
 //     items (x, p0, p1), <= PW partners each; others -> CTA items
 //     (x, p0, p1, group), <= PC partners.  With nshards > 1 only this
 //     shard's partner blocks are listed (dist.py shard_of).
 //  5. k_isect_tiny / k_isect_warp: one thread / warp per item; the warp tier
-//     keeps a per-warp bucket hash of OFF(x) ∪ SUP(x) (4-entry buckets).
-//  6. k_isect_cta: one CTA per item; the group's slices of OFF(x) ∪ SUP(x)
-//     (<= HC ids) staged in a two-table cuckoo set; the partners' slices
+//     keeps a per-warp bucket hash of OFF(x) ∪ UP(x) (4-entry buckets).
+//  6. k_isect_cta: one CTA per item; the group's slice of OFF(x) (and, in
+//     group 0, UP(x)) staged in a two-table cuckoo set; the partners' slices
 //     (two per partner) are flattened into one element stream (block scan of
 //     lengths) that warps consume in CHUNK-element grabs.
 //
@@ -87,11 +92,13 @@ constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int LONG_LIST = 64;         // warp tier: lists streamed by a whole warp
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+constexpr int NBKT = 32;              // degree buckets: floor(log2 d)
+__device__ __forceinline__ int dbucket(int d) { return 31 - __clz(max(d, 1)); }
 
 __device__ __forceinline__ int ceil_log2_dev(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
 // ---------------------------------------------------------------------------
-// entry classes: bit i of cls[j].x / .y = CSR entry 32j+i is OFF / SUP.
+// entry classes: bit i of cls[j].x / .y = CSR entry 32j+i is OFF / UP.
 // pre[j] = exclusive prefix over words of popc(.x) | popc(.y) << 32, so an
 // entry's slot in the OFF (SUP) array is a prefix read plus one popc.
 
@@ -102,7 +109,7 @@ __device__ __forceinline__ int64_t rank_off(const uint2* __restrict__ cls,
     const uint32_t below = (1u << (p & 31)) - 1u;
     return int64_t(pre[j] & 0xFFFFFFFFull) + __popc(cls[j].x & below);
 }
-__device__ __forceinline__ int64_t rank_sup(const uint2* __restrict__ cls,
+__device__ __forceinline__ int64_t rank_up(const uint2* __restrict__ cls,
                                             const unsigned long long* __restrict__ pre,
                                             int64_t p) {
     const int64_t j = p >> 5;
@@ -223,16 +230,22 @@ __device__ __forceinline__ bool staged(const int2* __restrict__ vinfo, int w, in
     return dw > dx || (dw == dx && w < x);
 }
 
-// Per-vertex list bounds: OFF(v) = L[ob(v), ob(v+1)), SUP(v) = L[sb(v), sb(v+1)),
-// kept as one uint2 (ob, sb) per vertex so a vertex's bounds share a sector
+// Per-vertex list bounds: OFF(v) = L[ob(v), ob(v+1)), UP(v) = L[ub(v), ub(v+1)),
+// kept as one uint2 (ob, ub) per vertex so a vertex's bounds share a sector
 // (positions < 2m < 2^32).
 struct Lists {
     const int32_t* __restrict__ L;
     const uint2* __restrict__ vb;
     __device__ __forceinline__ int64_t ob(int64_t v) const { return int64_t(vb[v].x); }
-    __device__ __forceinline__ int64_t sb(int64_t v) const { return int64_t(vb[v].y); }
-    const int2* __restrict__ split;  // [v*(F+1) + r] = (OFF pos, SUP pos) of range r
+    __device__ __forceinline__ int64_t ub(int64_t v) const { return int64_t(vb[v].y); }
+    const int* __restrict__ split;  // [v*(F+1) + r] = OFF position of id range r
+    const int* __restrict__ ucnt;   // [v*NBKT + k] = UP(v) entries with degree bucket >= k
     int rshift;
+    // the part of UP(p) that can hold an apex of owner x (degree bucket kx):
+    // neighbours of p with degree >= 2^kx, a prefix of UP(p)
+    __device__ __forceinline__ int up_prefix(int64_t p, int kx) const {
+        return ucnt[p * NBKT + kx];
+    }
 };
 
 // ---------------------------------------------------------------------------
@@ -302,7 +315,7 @@ __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __r
             const int2 a = vinfo[x], b = vinfo[y];
             keep = a.x == b.x && (a.y > b.y || (a.y == b.y && x < y));
             off = fwd || a.x != b.x;
-            sup = !fwd && a.x == b.x && y > x;
+            sup = !fwd && a.x == b.x && !keep;  // UP: same level, y owns the edge
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         const unsigned mo = __ballot_sync(0xffffffffu, off);
@@ -353,53 +366,110 @@ __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
     for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v <= n; v += stride) {
         const int64_t p = row[v];
         vb[v] = make_uint2(uint32_t(rank_off(cls, pre, p)),
-                           uint32_t(noff + rank_sup(cls, pre, p)));
+                           uint32_t(noff + rank_up(cls, pre, p)));
     }
 }
 
-__global__ void k_scatter_lists(const int32_t* __restrict__ nb, int64_t nnz,
-                                const uint2* __restrict__ cls,
-                                const unsigned long long* __restrict__ pre, int64_t nw,
-                                int32_t* __restrict__ L) {
-    const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
+// OFF entries go to their slot; UP entries count into their row's degree
+// bucket (ucur = per-row histogram, zeroed by the caller).
+__global__ void k_scatter_lists(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
+                                int64_t nnz, const uint2* __restrict__ cls,
+                                const unsigned long long* __restrict__ pre,
+                                const int2* __restrict__ vinfo, int32_t* __restrict__ L,
+                                int* __restrict__ ucur) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
         const uint2 c = cls[e >> 5];
         const uint32_t bit = 1u << (e & 31);
-        if (c.x & bit) L[rank_off(cls, pre, e)] = nb[e];
-        else if (c.y & bit) L[noff + rank_sup(cls, pre, e)] = nb[e];
+        if (c.x & bit) {
+            L[rank_off(cls, pre, e)] = nb[e];
+        } else if (c.y & bit) {
+            const int w = nb[e];
+            atomicAdd(&ucur[int64_t(src[e]) * NBKT + dbucket(vinfo[w].y)], 1);
+        }
+    }
+}
+
+// Per row: ucnt[k] = entries in buckets >= k (the stream prefix for an owner
+// of bucket k); ucur[k] becomes the start of bucket k (buckets descending).
+__global__ void k_up_offsets(int64_t n, const uint2* __restrict__ vb, int* __restrict__ ucnt,
+                             int* __restrict__ ucur) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        int4* cnt = reinterpret_cast<int4*>(ucnt + v * NBKT);
+        int4* cur = reinterpret_cast<int4*>(ucur + v * NBKT);
+        if (vb[v + 1].y == vb[v].y) {  // empty UP row: zero prefix counts
+#pragma unroll
+            for (int i = 0; i < NBKT / 4; ++i) cnt[i] = make_int4(0, 0, 0, 0);
+            continue;
+        }
+        int h[NBKT];
+#pragma unroll
+        for (int i = 0; i < NBKT / 4; ++i) {
+            const int4 q = cur[i];
+            h[4 * i] = q.x;
+            h[4 * i + 1] = q.y;
+            h[4 * i + 2] = q.z;
+            h[4 * i + 3] = q.w;
+        }
+        int acc = 0;
+#pragma unroll
+        for (int k = NBKT - 1; k >= 0; --k) {
+            const int c = h[k];
+            h[k] = acc;  // start of bucket k
+            acc += c;
+        }
+        // h[k] = start of bucket k = entries in buckets > k; cnt[k] = entries
+        // in buckets >= k = start of bucket k-1 (the row size for k = 0)
+#pragma unroll
+        for (int i = 0; i < NBKT / 4; ++i) {
+            cur[i] = make_int4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            int t[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = 4 * i + j;
+                t[j] = k == 0 ? acc : h[k - 1];
+            }
+            cnt[i] = make_int4(t[0], t[1], t[2], t[3]);
+        }
+    }
+}
+
+__global__ void k_scatter_up(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
+                             int64_t nnz, const uint2* __restrict__ cls,
+                             const int2* __restrict__ vinfo, const uint2* __restrict__ vb,
+                             int32_t* __restrict__ L, int* __restrict__ ucur) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
+        if (!(cls[e >> 5].y & (1u << (e & 31)))) continue;
+        const int v = src[e], w = nb[e];
+        const int pos = atomicAdd(&ucur[int64_t(v) * NBKT + dbucket(vinfo[w].y)], 1);
+        L[int64_t(vb[v].y) + pos] = w;
     }
 }
 
 // ---------------------------------------------------------------------------
-// 3. split points: split[v*(F+1) + r] = (first position in OFF(v), in SUP(v))
-//    of an id >= r << rshift, relative to the list start; [0] = 0, [F] = size.
+// 3. split points: split[v*(F+1) + r] = first position in OFF(v) of an id
+//    >= r << rshift, relative to the list start; [0] = 0, [F] = size.
 
 __global__ void k_split_points(const int32_t* __restrict__ src, int64_t nnz,
                                const uint2* __restrict__ cls,
-                               const unsigned long long* __restrict__ pre, int64_t nw,
+                               const unsigned long long* __restrict__ pre,
                                const int32_t* __restrict__ L, const uint2* __restrict__ vb,
-                               int rshift,
-                               int2* __restrict__ split) {
-    const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
+                               int rshift, int* __restrict__ split) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-        const uint2 c = cls[e >> 5];
-        const uint32_t bit = 1u << (e & 31);
-        const bool off = c.x & bit;
-        if (!off && !(c.y & bit)) continue;
+        if (!(cls[e >> 5].x & (1u << (e & 31)))) continue;
         const int v = src[e];
-        const int64_t g = off ? rank_off(cls, pre, e) : noff + rank_sup(cls, pre, e);
-        const uint2 v0 = vb[v], v1 = vb[v + 1];
-        const int64_t b0 = off ? v0.x : v0.y;
-        const int64_t b1 = off ? v1.x : v1.y;
+        const int64_t g = rank_off(cls, pre, e);
+        const int64_t b0 = vb[v].x, b1 = vb[v + 1].x;
         const int k = int(g - b0);
         const int r = L[g] >> rshift;
         const int prev = g == b0 ? -1 : (L[g - 1] >> rshift);
-        int* sp = reinterpret_cast<int*>(split + int64_t(v) * (F + 1)) + (off ? 0 : 1);
-        for (int q = prev + 1; q <= r; ++q) sp[2 * q] = k;
+        int* sp = split + int64_t(v) * (F + 1);
+        for (int q = prev + 1; q <= r; ++q) sp[q] = k;
         if (g == b1 - 1)
-            for (int q = r + 1; q <= F; ++q) sp[2 * q] = k + 1;
+            for (int q = r + 1; q <= F; ++q) sp[q] = k + 1;
     }
 }
 
@@ -424,9 +494,10 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         if (d == 0) continue;
         const int64_t s = seg_beg[x], e = seg_end[x];
         if (e <= s) continue;
-        // nothing staged (no OFF neighbours, no same-level neighbour above
-        // x): no edge of x can have an apex
-        const int64_t st = (ls.ob(x + 1) - ls.ob(x)) + (ls.sb(x + 1) - ls.sb(x));
+        // nothing staged (no OFF neighbours, no same-level neighbour ranked
+        // above x): no edge of x can have an apex
+        const int64_t nup = ls.ub(x + 1) - ls.ub(x);
+        const int64_t st = (ls.ob(x + 1) - ls.ob(x)) + nup;
         if (st == 0) continue;
         if (d <= tiny) {  // <= TINY partners, each with <= TINY ids
             if (!mine(x, 0)) continue;
@@ -447,15 +518,15 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
             }
             continue;
         }
-        // fewest range groups G (power of two <= F) whose staged slices all fit HC
-        const int2* sx = ls.split + x * (F + 1);
+        // fewest range groups G (power of two <= F) whose OFF slices all fit
+        // HC; group 0 also stages UP(x) (not range-split: it is degree-sorted)
+        const int* sx = ls.split + x * (F + 1);
         int lg = 0;
         if (st > hc) {
             for (lg = 1; lg < LOG_F; ++lg) {
                 const int step = F >> lg;
                 int mx = 0;
-                for (int q = 0; q < F; q += step)
-                    mx = max(mx, (sx[q + step].x - sx[q].x) + (sx[q + step].y - sx[q].y));
+                for (int q = 0; q < F; q += step) mx = max(mx, sx[q + step] - sx[q]);
                 if (mx <= hc) break;
             }
         }
@@ -464,15 +535,15 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         int64_t my = 0;
         for (int64_t i = 0; i < per; ++i) my += mine(x, i);
         if (my == 0) continue;
-        int ng = 0;  // groups with something staged
-        for (int g = 0; g < G; ++g) {
+        auto staged_any = [&](int g) {
             const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;
-            ng += (sx[q1].x - sx[q0].x) + (sx[q1].y - sx[q0].y) > 0;
-        }
+            return sx[q1] - sx[q0] > 0 || (g == 0 && nup > 0);
+        };
+        int ng = 0;  // groups with something staged
+        for (int g = 0; g < G; ++g) ng += staged_any(g);
         unsigned long long base = atomicAdd(nc, (unsigned long long)(my * ng));
         for (int g = 0; g < G; ++g) {
-            const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;
-            if ((sx[q1].x - sx[q0].x) + (sx[q1].y - sx[q0].y) == 0) continue;
+            if (!staged_any(g)) continue;
             for (int64_t i = 0; i < per; ++i) {
                 if (!mine(x, i)) continue;
                 const int64_t p0 = s + i * PC;
@@ -484,7 +555,7 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
 
 // ---------------------------------------------------------------------------
 // 4b. thread tier: one thread per tiny owner (d(x) <= TINY, so every partner
-//     has <= TINY ids too).  OFF(x) ∪ SUP(x) sits in registers; each streamed
+//     has <= TINY ids too).  OFF(x) ∪ UP(x) sits in registers; each streamed
 //     id is compared with all of it.
 
 __global__ void __launch_bounds__(256)
@@ -497,9 +568,10 @@ __global__ void __launch_bounds__(256)
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < nitems; it += stride) {
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int64_t o0 = ls.ob(x), o1 = ls.ob(x + 1), s0 = ls.sb(x);
-        const int no = int(o1 - o0), nx = no + int(ls.sb(x + 1) - s0);
-        const int dx = fwd ? vinfo[x].y : 0;
+        const int64_t o0 = ls.ob(x), o1 = ls.ob(x + 1), s0 = ls.ub(x);
+        const int no = int(o1 - o0), nx = no + int(ls.ub(x + 1) - s0);
+        const int dx = vinfo[x].y;
+        const int kx = dbucket(dx);
         int a[TINY];
 #pragma unroll
         for (int i = 0; i < TINY; ++i) {
@@ -510,7 +582,8 @@ __global__ void __launch_bounds__(256)
         }
         for (int64_t p = item.y; p < item.z; ++p) {
             const int y = P[p];
-            const int64_t y0 = ls.ob(y), y1 = ls.ob(y + 1), y2 = ls.sb(y), y3 = ls.sb(y + 1);
+            const int64_t y0 = ls.ob(y), y1 = ls.ob(y + 1), y2 = ls.ub(y);
+            const int64_t y3 = y2 + ls.up_prefix(y, kx);
             for (int64_t j = y0; j < y1; ++j) {
                 const int w = ls.L[j];
                 bool hit = false;
@@ -555,10 +628,10 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
         if (it >= nitems) break;
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int64_t o0 = ls.ob(x), s0 = ls.sb(x);
-        const int no = int(ls.ob(x + 1) - o0), nx = no + int(ls.sb(x + 1) - s0);
-        const int dx = fwd ? vinfo[x].y : 0;
-        const int qx = x >> ls.rshift;
+        const int64_t o0 = ls.ob(x), s0 = ls.ub(x);
+        const int no = int(ls.ob(x + 1) - o0), nx = no + int(ls.ub(x + 1) - s0);
+        const int dx = vinfo[x].y;
+        const int kx = dbucket(dx);
         const int slots = max(16, 2 << ceil_log2_dev(nx));
         BucketHash h;
         h.setup(tab, slots);
@@ -575,11 +648,8 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
                 const int y = P[j];
                 yo = ls.ob(y);
                 ydo = int(ls.ob(y + 1) - yo);
-                // SUP(y) ids below x's id range cannot be in SUP(x)
-                const int64_t sy = ls.sb(y);
-                const int a = ls.split[int64_t(y) * (F + 1) + qx].y;
-                ys = sy + a;
-                yds = int(ls.sb(y + 1) - sy) - a;
+                ys = ls.ub(y);  // the prefix of UP(y) that can be in UP(x)
+                yds = ls.up_prefix(y, kx);
             }
             tl.c1 += probe_batch(ls.L, yo, ydo, h);
             tl.sup += probe_batch(ls.L, ys, yds, h);
@@ -786,15 +856,14 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         const int x = int(item.x);
         const int lg = int(item.w >> 8), g = int(item.w & 255);
         const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;  // ranges [q0, q1)
-        const int2* sx = ls.split + int64_t(x) * (F + 1);
-        const int2 ax = sx[q0], bx = sx[q1];
-        // the owner's staged slices: OFF [xo0, xo1), SUP [xs0, xs1)
-        const int64_t xo0 = ls.ob(x) + ax.x, xo1 = ls.ob(x) + bx.x;
-        const int64_t xs0 = ls.sb(x) + ax.y, xs1 = ls.sb(x) + bx.y;
+        const int* sx = ls.split + int64_t(x) * (F + 1);
+        // the owner's staged slices: OFF [xo0, xo1) of its id ranges, and
+        // in group 0 all of UP(x): [xs0, xs1)
+        const int64_t xo0 = ls.ob(x) + sx[q0], xo1 = ls.ob(x) + sx[q1];
+        const int64_t xs0 = ls.ub(x), xs1 = g == 0 ? ls.ub(x + 1) : xs0;
         const int no = int(xo1 - xo0), ns = int(xs1 - xs0);
-        const int dx = fwd ? vinfo[x].y : 0;
-        // SUP(y) ids below x's id range cannot be in SUP(x)
-        const int qa = max(q0, x >> ls.rshift);
+        const int dx = vinfo[x].y;
+        const int kx = dbucket(dx);
         const int np = int(item.z - item.y);
         // partners t and t + C_THREADS of this thread: both ids are loaded
         // before either partner's rows, so the two dependent chains overlap
@@ -811,28 +880,24 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 const int t = threadIdx.x + r * C_THREADS;
                 if (yy[r] < 0) continue;
                 const int y = yy[r];
-                const int2* sy = ls.split + int64_t(y) * (F + 1);
+                const int* sy = ls.split + int64_t(y) * (F + 1);
                 const uint2 v0 = ls.vb[y];
                 // range ends at 0 / F come from the bounds, not the split row
-                int2 a = make_int2(0, 0), b;
-                if (q0 > 0) a = sy[q0];
-                if (q1 == F) {
-                    const uint2 v1 = ls.vb[y + 1];
-                    b = make_int2(int(v1.x - v0.x), int(v1.y - v0.y));
-                } else {
-                    b = sy[q1];
-                }
-                const int as = qa < q1 ? sy[qa].y : b.y;
-                s_pos[t] = v0.x + uint32_t(a.x);
-                s_len[t] = no ? b.x - a.x : 0;
-                s_pos[PC + t] = v0.y + uint32_t(as);
-                s_len[PC + t] = ns ? b.y - as : 0;
+                const int a = q0 > 0 ? sy[q0] : 0;
+                const int b = q1 == F ? int(ls.vb[y + 1].x - v0.x) : sy[q1];
+                s_pos[t] = v0.x + uint32_t(a);
+                s_len[t] = no ? b - a : 0;
+                // the prefix of UP(y) that can be in UP(x) (degree >= 2^kx)
+                s_pos[PC + t] = v0.y;
+                s_len[PC + t] = ns ? ls.up_prefix(y, kx) : 0;
             }
         }
         // Passes: one when both owner slices fit the table; otherwise the
-        // OFF slice then the SUP slice, each in sub-chunks of hc ids (only
-        // the largest hubs), each sub-chunk [.., vhi] matched against every
-        // partner's next unread part of the same class.
+        // OFF slice then UP(x), each in sub-chunks of hc ids.  An OFF
+        // sub-chunk [.., vhi] is matched against every partner's next unread
+        // OFF part (id-sorted); every UP sub-chunk sees the partners' whole UP
+        // prefixes (degree-sorted, so not split by id; each apex still sits in
+        // exactly one sub-chunk).
         const bool single = no + ns <= hc;
         for (int phase = single ? 2 : 0; phase < 3; ++phase) {
             if (phase == 2 && !single) break;
@@ -863,8 +928,9 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         if (!ch.insert(w)) s_fail = 1;
                     }
                 // this pass's count from each slice of partners 2t, 2t+1
-                // (slots 0, 1: OFF; 2, 3: SUP), then the stream table
+                // (slots 0, 1: OFF; 2, 3: UP), then the stream table
                 const bool last = cb + len >= plen;
+                const bool consume = phase != 1 || last;  // UP prefixes are re-streamed
                 const int vhi = phase == 2 ? 0 : L[p0 + cb + len - 1];
                 int cnt[4];
                 int slot[4];
@@ -880,10 +946,10 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         int c = 0;
                         if ((k & (PC - 1)) < np) {
                             const int ln = s_len[k];
-                            if (phase == 2 || (ln > 0 && (r >> 1) == phase && last)) {
+                            if (phase == 2 || (ln > 0 && (r >> 1) == phase && (last || phase == 1))) {
                                 c = ln;
                             } else if (ln > 0 && (r >> 1) == phase) {
-                                // ids <= vhi in the unread part
+                                // OFF ids <= vhi in the unread part
                                 uint32_t lo = s_pos[k], hi = s_pos[k] + uint32_t(ln);
                                 while (lo < hi) {
                                     const uint32_t mid = lo + ((hi - lo) >> 1);
@@ -918,8 +984,10 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         const bool isup = r >= 2;
                         const int e = isup ? e_s : e_o;
                         s_seg[isup ? n_s : n_o] = make_int2(e, int(s_pos[k] - uint32_t(e)));
-                        s_pos[k] += uint32_t(c);
-                        s_len[k] -= c;
+                        if (consume) {
+                            s_pos[k] += uint32_t(c);
+                            s_len[k] -= c;
+                        }
                         if (isup) {
                             e_s += c;
                             ++n_s;
@@ -982,14 +1050,19 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     int2* vinfo = ctx->wsT<int2>(WS_MISC, n);
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
-    int2* split = ctx->wsT<int2>(WS_COVER_V, size_t(n) * (F + 1));
+    int* split = ctx->wsT<int>(WS_COVER_V, size_t(n) * (F + 1));
     int32_t* L = ctx->wsT<int32_t>(WS_LISTS, nnz);
     const size_t cls_bytes = (size_t(nwords + 1) * sizeof(uint2) + 15) / 16 * 16;
     char* cbuf = static_cast<char*>(
         ctx->ws(WS_CLASS, cls_bytes + size_t(nwords + 1) * sizeof(unsigned long long)));
     uint2* cls = reinterpret_cast<uint2*>(cbuf);
     unsigned long long* pre = reinterpret_cast<unsigned long long*>(cbuf + cls_bytes);
-    uint2* vb = ctx->wsT<uint2>(WS_VBEG, size_t(n + 1));
+    // per-vertex (OFF start, UP start), then the UP bucket tables ucnt, ucur
+    char* vbuf = static_cast<char*>(ctx->ws(
+        WS_VBEG, (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16 + 2 * size_t(n) * NBKT * sizeof(int)));
+    uint2* vb = reinterpret_cast<uint2*>(vbuf);
+    int* ucnt = reinterpret_cast<int*>(vbuf + (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16);
+    int* ucur = ucnt + size_t(n) * NBKT;
     // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
     const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
     const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
@@ -1007,7 +1080,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     unsigned long long* fc = &C->scratch[8];
     int64_t* d_ncover = reinterpret_cast<int64_t*>(&C->ncover);
     const int rshift = max(0, bits_for(n) - LOG_F);
-    Lists ls{L, vb, split, rshift};
+    Lists ls{L, vb, split, ucnt, rshift};
 
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo);
     TCB_CUDA(cudaMemsetAsync(cls + nwords, 0, sizeof(uint2), ctx->stream));
@@ -1024,14 +1097,18 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         reinterpret_cast<int64_t*>(pre + nwords));
     TCB_LAUNCH(ctx, k_list_bounds, grid_for(ctx, n + 1, 256), 256, 0, row, n, ccls,
                (const unsigned long long*)pre, nwords, vb);
-    // rows of class-empty lists stay zero (k_split_points writes only rows
+    // rows of empty OFF lists stay zero (k_split_points writes only rows
     // with entries)
-    TCB_CUDA(cudaMemsetAsync(split, 0, size_t(n) * (F + 1) * sizeof(int2), ctx->stream));
-    TCB_LAUNCH(ctx, k_scatter_lists, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
-               (const unsigned long long*)pre, nwords, L);
+    TCB_CUDA(cudaMemsetAsync(split, 0, size_t(n) * (F + 1) * sizeof(int), ctx->stream));
+    TCB_CUDA(cudaMemsetAsync(ucur, 0, size_t(n) * NBKT * sizeof(int), ctx->stream));
+    TCB_LAUNCH(ctx, k_scatter_lists, grid_for(ctx, nnz, 256), 256, 0, src, nb, nnz, ccls,
+               (const unsigned long long*)pre, (const int2*)vinfo, L, ucur);
+    TCB_LAUNCH(ctx, k_up_offsets, grid_for(ctx, n, 256), 256, 0, n, (const uint2*)vb, ucnt, ucur);
+    TCB_LAUNCH(ctx, k_scatter_up, grid_for(ctx, nnz, 256), 256, 0, src, nb, nnz, ccls,
+               (const int2*)vinfo, (const uint2*)vb, L, ucur);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
-               (const unsigned long long*)pre, nwords, (const int32_t*)L, (const uint2*)vb,
-               rshift, split);
+               (const unsigned long long*)pre, (const int32_t*)L, (const uint2*)vb, rshift,
+               split);
     TCB_LAUNCH(ctx, k_make_items, grid_for(ctx, n, 256), 256, 0, row, (const int64_t*)seg,
                (const int64_t*)(seg + n), ls, n, witems, citems, titems, nw, nc, nt, shard,
                nshards, wt, hc, tiny);

@@ -45,9 +45,10 @@ def shard_of(owner, partner_rank, owner_degree, world: int):
 
 def reduce_counts(c1: int, c2: int, group=None, device=None):
     """Sum per-rank (c1, c2) partials with one all-reduce and form
-    T = c1 + c2/3.  Each rank's c2 is 3 x its edges' same-level apexes with
-    w > max(u, v) (the one of three the reference's rule keeps, intersect.cu),
-    so the sum is the reference's c2 (every same-level hit, 3 per triangle).
+    T = c1 + c2/3.  Each rank's c2 is 3 x its edges' same-level apexes that
+    rank above both endpoints (each same-level triangle is kept at exactly one
+    of its three edges, intersect.cu), so the sum is the reference's c2 (every
+    same-level hit, 3 per triangle, parallel.py:127-129).
     NCCL needs the tensor on the rank's GPU; gloo takes it on the CPU.
     Returns (T, c1, c2)."""
     import torch

@@ -47,15 +47,18 @@ def _partials(case, rank, world):
         starts = np.searchsorted(so, so, side="left")
         prank[order] = np.arange(len(so)) - starts
         mine = tdist.shard_of(own, prank, deg[own], world) == rank
-        for a, b in cov[mine]:
+        for a, b, x in zip(cov[mine][:, 0], cov[mine][:, 1], own[mine]):
             common = np.intersect1d(case.nb[case.row[a]:case.row[a + 1]],
                                     case.nb[case.row[b]:case.row[b + 1]])
             for w in common:
                 if level[w] != level[a]:
                     c1 += 1
                     t += 1
-                elif w > b:  # a < b: the one same-level apex T keeps (_kernels.py:687)
-                    c2 += 3  # the device tallies c2 in the reference's units (3 per triangle)
+                elif deg[w] > deg[x] or (deg[w] == deg[x] and w < x):
+                    # a same-level triangle is kept at the edge whose apex
+                    # ranks above both endpoints (intersect.cu); the device
+                    # tallies c2 in the reference's units (3 per triangle)
+                    c2 += 3
                     t += 1
     return t, c1, c2
 

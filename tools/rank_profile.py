@@ -1,0 +1,46 @@
+"""Same-level stream volume under two dedup orientations (measurement only):
+id rule (stream SUP(p) above x: same-level w > max(x, p)) vs degree-rank rule
+(stream same-level w of p ranked above the owner x).  Run on the GPU box:
+    python tools/rank_profile.py rmat24
+"""
+import sys
+
+import torch
+
+sys.path.insert(0, __import__("os").path.dirname(__file__) + "/..")
+import paper_2403_02997_b200 as tb  # noqa: E402
+from paper_2403_02997_b200 import configs as C  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "rmat22"
+dg = C.build_device_graph(name)
+r = tb.cetc(dg, keep_level=True, keep_cover=True)
+n = dg.n
+deg = dg.row_offsets[1:] - dg.row_offsets[:-1]
+u, v = r.cover_u.long(), r.cover_v.long()
+du, dv = deg[u], deg[v]
+own_u = (du > dv) | ((du == dv) & (u < v))
+x = torch.where(own_u, u, v)
+p = torch.where(own_u, v, u)
+del du, dv, own_u, u, v
+lev = r.level
+srcl, nbl = dg.src.long(), dg.neighbors.long()
+same = lev[srcl] == lev[nbl]
+n_off = torch.bincount(srcl[~same], minlength=n)
+# rank: degree desc, id asc -> rank value (higher = higher rank)
+order = torch.argsort(deg * (n + 1) + (n - torch.arange(n, device=deg.device)), descending=False)
+rank = torch.empty(n, dtype=torch.long, device=deg.device)
+rank[order] = torch.arange(n, device=deg.device)
+s_src, s_nb = srcl[same], nbl[same]
+del srcl, nbl, same
+n_same = torch.bincount(s_src, minlength=n)
+end = torch.cumsum(n_same, 0)
+keys = s_src * n + rank[s_nb]
+keys, _ = torch.sort(keys)
+above_rank = end[p] - torch.searchsorted(keys, p * n + rank[x], right=True)
+keys = s_src * (n + 1) + s_nb  # CSR order is already sorted
+above_id = end[p] - torch.searchsorted(keys, p * (n + 1) + x, right=True)
+off = int(n_off[p].sum())
+a, b = int(above_id.sum()), int(above_rank.sum())
+print(f"{name}: OFF stream {off:.4e}  same-level: id rule {a:.4e}  rank rule {b:.4e}  "
+      f"total id {off + a:.4e}  total rank {off + b:.4e} ({(off + b) / (off + a):.3f})")
+# owner tables: id rule SUP(x) (same-level > x) vs rank rule (same-level ranked above x)
