@@ -262,41 +262,49 @@ def main():
     H = full.c1 + full.c2
     ncover = full.ncover
     expect = [full.triangles, full.c1, full.c2]
-    # bytes the CTA-tier kernel must move (owners with d > WT = 512).  With
+    # bytes the CTA-tier kernel must move (owners with d > WT = 256).  With
     # the level rule applied before the intersection (intersect.cu) an edge
     # (owner x, partner p) streams OFF(p) (p's neighbours on another level)
-    # and the part of SUP(p) (same level, id > p) above x: 4 B/id.  Plus the
-    # partner id and its 4 list bounds per cover edge (36 B), and the owner's
-    # OFF(x) ∪ SUP(x) staged once per item (<= 1024 partners).
+    # and p's same-level neighbours ranked above x (degree desc, id asc): 4
+    # B/id.  Plus the partner id and its list bounds per cover edge (36 B),
+    # and the owner's OFF(x) ∪ UP(x) staged once per item (<= 1024 partners).
     cu, cv = full.cover_u.long(), full.cover_v.long()
     own_u = (du > dv) | ((du == dv) & (cu < cv))
     d_own = torch.where(own_u, du, dv)
     owner = torch.where(own_u, cu, cv)
     partner = torch.where(own_u, cv, cu)
-    cta = d_own > 512
+    cta = d_own > 256  # intersect.cu TCB_WT
+    del cu, cv, own_u, d_own
     lev = full.level.to(dev)
+    n = dg.n
     srcl = dg.src.long()
     nbl = dg.neighbors.long()
     same = lev[srcl] == lev[nbl]
-    n_off = torch.bincount(srcl[~same], minlength=dg.n)
-    sup = same & (nbl > srcl)
-    n_sup = torch.bincount(srcl[sup], minlength=dg.n)
-    # |SUP(p) ∩ (x, inf)| by one sorted search over (row, id) keys
-    keys = srcl[sup] * (dg.n + 1) + nbl[sup]
-    del same, sup, nbl
+    n_off = torch.bincount(srcl[~same], minlength=n)
+    s_src, s_nb = srcl[same], nbl[same]
+    del srcl, nbl, same, lev
+    # rank: degree desc, id asc (higher value = ranked higher)
+    order = torch.argsort(deg * (n + 1) + (n - torch.arange(n, device=dev)))
+    rk = torch.empty(n, dtype=torch.long, device=dev)
+    rk[order] = torch.arange(n, device=dev)
+    del order
+    up = rk[s_nb] > rk[s_src]
+    n_up = torch.bincount(s_src[up], minlength=n)
+    keys, _ = torch.sort(s_src * n + rk[s_nb])
+    row_end = torch.cumsum(torch.bincount(s_src, minlength=n), 0)
+    del s_src, s_nb, up
     pc, oc = partner[cta], owner[cta]
-    sup_row_end = torch.cumsum(n_sup, 0)
-    above = sup_row_end[pc] - torch.searchsorted(keys, pc * (dg.n + 1) + oc, right=True)
+    above = row_end[pc] - torch.searchsorted(keys, pc * n + rk[oc], right=True)
     stream_cta = int((n_off[pc].sum() + above.sum()).item())
     S_cta = int(cta.sum().item())
     staged = 0
     if S_cta:
         own_ids, per_owner = torch.unique(oc, return_counts=True)
-        staged = int(((n_off + n_sup)[own_ids] * ((per_owner + 1023) // 1024)).sum().item())
+        staged = int(((n_off + n_up)[own_ids] * ((per_owner + 1023) // 1024)).sum().item())
     W_min_cta = int(torch.minimum(du, dv)[cta].sum().item())
     b_cta = 4 * stream_cta + 36 * S_cta + 4 * staged
-    del keys, pc, oc, above, sup_row_end, n_off, n_sup, srcl, lev, partner
-    del du, dv, deg, full, cu, cv, own_u, d_own, owner, cta
+    del keys, pc, oc, above, row_end, n_off, n_up, rk, partner, owner, cta
+    del du, dv, deg, full
 
     for _ in range(args.warmup):
         if flush is not None:
@@ -405,8 +413,8 @@ def main():
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_kind": peak_kind, "algorithmic_bytes": b_cta,
-                "formula": ("4*sum_{S_cta} (|OFF(p)| + |SUP(p) above x|) + 36*|S_cta| "
-                            "+ 4*staged |OFF(x)|+|SUP(x)| per item"),
+                "formula": ("4*sum_{S_cta} (|OFF(p)| + |same-level N(p) ranked above x|) "
+                            "+ 36*|S_cta| + 4*staged |OFF(x)|+|UP(x)| per item"),
                 "stream_ids": stream_cta, "W_min_cta": W_min_cta,
                 "t_ms": stages["isect_cta"],
                 "survey_8d_intersect_stage": {

@@ -66,7 +66,7 @@ namespace tcb {
 // Tier thresholds and tile sizes.  The TCB_* macros exist so tools/variants.py
 // can A/B alternatives in one GPU session; the defaults are the measured best.
 #ifndef TCB_WT
-#define TCB_WT 512
+#define TCB_WT 256
 #endif
 #ifndef TCB_HC
 #define TCB_HC 4096
@@ -89,7 +89,6 @@ constexpr int NSEG = 2 * PC;          // stream segments: partner t -> 2t (OFF),
 constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per lane)
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
-constexpr int LONG_LIST = 64;         // warp tier: lists streamed by a whole warp
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr int NBKT = 32;              // degree buckets: floor(log2 d)
@@ -247,53 +246,6 @@ struct Lists {
         return ucnt[p * NBKT + kx];
     }
 };
-
-// ---------------------------------------------------------------------------
-// warp tier helpers: one long list with the whole warp (4 loads in flight per
-// lane); a batch of <= 32 lists flattened across lanes.
-
-template <typename Probe>
-__device__ __forceinline__ uint32_t probe_long(const int32_t* __restrict__ L, int64_t s, int d,
-                                               const Probe& h) {
-    const int lane = int(lane_id());
-    uint32_t acc = 0;
-    int i = lane;
-    for (; i + 96 < d; i += 128) {
-        const int w0 = L[s + i], w1 = L[s + i + 32], w2 = L[s + i + 64], w3 = L[s + i + 96];
-        acc += h.hit(w0) + h.hit(w1) + h.hit(w2) + h.hit(w3);
-    }
-    for (; i < d; i += 32) acc += h.hit(L[s + i]);
-    return acc;
-}
-
-template <typename Probe>
-__device__ __forceinline__ uint32_t probe_batch(const int32_t* __restrict__ L, int64_t ys, int yd,
-                                                const Probe& h) {
-    const unsigned lane = lane_id();
-    uint32_t acc = 0;
-    unsigned longs = __ballot_sync(0xffffffffu, yd >= LONG_LIST);
-    while (longs) {
-        const int k = __ffs(longs) - 1;
-        longs &= longs - 1;
-        acc += probe_long(L, __shfl_sync(0xffffffffu, ys, k), __shfl_sync(0xffffffffu, yd, k), h);
-    }
-    if (yd >= LONG_LIST) yd = 0;
-    const int incl = warp_inclusive_scan(yd);
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int base = 0; base < total; base += 32) {
-        const int i = base + int(lane);
-        int k = 0;  // owning lane: smallest k with incl_k > i
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const int v = __shfl_sync(0xffffffffu, incl, k + step - 1);
-            if (v <= i) k += step;
-        }
-        const int64_t ysk = __shfl_sync(0xffffffffu, ys, k);
-        const int exk = __shfl_sync(0xffffffffu, incl - yd, k);
-        if (i < total) acc += h.hit(L[ysk + (i - exk)]);
-    }
-    return acc;
-}
 
 // ---------------------------------------------------------------------------
 // 1. owner-grouped selection + entry classes
@@ -607,7 +559,53 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// 5. warp tier
+// 5. warp tier: one warp per item (owner x with d(x) <= WT, <= PW partners).
+//    The owner's OFF(x) ∪ UP(x) sits in a per-warp bucket hash; the partners'
+//    OFF slices and UP prefixes are compacted into a per-warp slice table
+//    (OFF slices first) and streamed in rounds of 32 x JW elements, each lane
+//    walking the slice boundaries like the CTA tier's cross_chunk.
+
+constexpr int JW = 8;           // elements per lane per warp-tier round
+constexpr int W_SEG = 2 * PW;   // slices per warp item
+
+__device__ __forceinline__ void warp_stream(const int32_t* __restrict__ L, const int2* seg,
+                                            int total, int tsup, const BucketHash& h, Tally& tl) {
+    const int lane = int(lane_id());
+    int kc = 0;  // warp-uniform: the slice holding c0
+    for (int c0 = 0; c0 < total; c0 += 32 * JW) {
+        while (seg[kc + 1].x <= c0) ++kc;
+        const int c1 = min(total, c0 + 32 * JW);
+        const int i0 = c0 + lane;
+        int k = kc;
+        int nx = seg[k + 1].x;
+        uint32_t base = uint32_t(seg[k].y);
+        int w[JW];
+#pragma unroll
+        for (int j = 0; j < JW; ++j) {
+            const int i = i0 + 32 * j;
+            w[j] = -1;
+            if (i < c1) {
+                if (nx <= i) {
+                    do {
+                        ++k;
+                        nx = seg[k + 1].x;
+                    } while (nx <= i);
+                    base = uint32_t(seg[k].y);
+                }
+                w[j] = L[base + uint32_t(i)];
+            }
+        }
+        uint32_t hm = 0;
+#pragma unroll
+        for (int j = 0; j < JW; ++j)
+            if (w[j] >= 0 && h.hit(w[j])) hm |= 1u << j;
+        const int jt = (tsup - i0 + 31) >> 5;  // elements j >= jt are UP
+        const uint32_t sm = jt <= 0 ? ~0u : (jt >= JW ? 0u : ~0u << jt);
+        const uint32_t sup = __popc(hm & sm);
+        tl.c1 += __popc(hm) - sup;
+        tl.sup += sup;
+    }
+}
 
 __global__ void __launch_bounds__(W_WARPS * 32, 4)
     k_isect_warp(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
@@ -617,6 +615,8 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem4) + warp * W_SLOTS;
+    int2* seg = reinterpret_cast<int2*>(reinterpret_cast<uint32_t*>(smem4) + W_WARPS * W_SLOTS) +
+                warp * (W_SEG + 1);
     for (int i = lane; i < W_SLOTS; i += 32) tab[i] = EMPTY;
     __syncwarp();
     const unsigned long long nitems = *nitems_p;
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
         const longlong4 item = items[it];
         const int x = int(item.x);
         const int64_t o0 = ls.ob(x), s0 = ls.ub(x);
-        const int no = int(ls.ob(x + 1) - o0), nx = no + int(ls.ub(x + 1) - s0);
+        const int no = int(ls.ob(x + 1) - o0), nu = int(ls.ub(x + 1) - s0), nx = no + nu;
         const int dx = vinfo[x].y;
         const int kx = dbucket(dx);
         const int slots = max(16, 2 << ceil_log2_dev(nx));
@@ -639,21 +639,49 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
             const int w = i < no ? ls.L[o0 + i] : ls.L[s0 + (i - no)];
             if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
         }
-        __syncwarp();
-        for (int64_t pb = item.y; pb < item.z; pb += 32) {
-            const int64_t j = pb + lane;
-            int64_t yo = 0, ys = 0;
-            int ydo = 0, yds = 0;
+        // slices of partners lane and lane + 32: OFF (c0, c1), UP (c2, c3)
+        static_assert(PW <= 64, "two partners per lane");
+        int cnt[4] = {0, 0, 0, 0};
+        uint32_t pos[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int64_t j = item.y + lane + 32 * r;
             if (j < item.z) {
                 const int y = P[j];
-                yo = ls.ob(y);
-                ydo = int(ls.ob(y + 1) - yo);
-                ys = ls.ub(y);  // the prefix of UP(y) that can be in UP(x)
-                yds = ls.up_prefix(y, kx);
+                const uint2 v0 = ls.vb[y];
+                pos[r] = v0.x;
+                cnt[r] = no ? int(ls.vb[y + 1].x - v0.x) : 0;
+                pos[2 + r] = v0.y;  // the prefix of UP(y) that can be in UP(x)
+                cnt[2 + r] = nu ? ls.up_prefix(y, kx) : 0;
             }
-            tl.c1 += probe_batch(ls.L, yo, ydo, h);
-            tl.sup += probe_batch(ls.L, ys, yds, h);
         }
+        const int64_t ve = int64_t(cnt[0] + cnt[1]) | (int64_t(cnt[2] + cnt[3]) << 32);
+        const int vn = int(cnt[0] > 0) + int(cnt[1] > 0) + ((int(cnt[2] > 0) + int(cnt[3] > 0)) << 16);
+        const int64_t ie = warp_inclusive_scan(ve);
+        const int in = warp_inclusive_scan(vn);
+        const int64_t te = __shfl_sync(0xffffffffu, ie, 31);
+        const int tn = __shfl_sync(0xffffffffu, in, 31);
+        const int tsup = int(te & 0xFFFFFFFF);
+        const int total = tsup + int(te >> 32);
+        const int noff = tn & 0xFFFF;
+        {
+            const int64_t ee = ie - ve;
+            const int en = in - vn;
+            int e_o = int(ee & 0xFFFFFFFF), e_s = tsup + int(ee >> 32);
+            int n_o = en & 0xFFFF, n_s = noff + (en >> 16);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int c = cnt[r];
+                if (c == 0) continue;
+                const bool isup = r >= 2;
+                const int e = isup ? e_s : e_o;
+                seg[isup ? n_s++ : n_o++] = make_int2(e, int(pos[r] - uint32_t(e)));
+                if (isup) e_s += c; else e_o += c;
+            }
+            if (lane == 0) seg[noff + (tn >> 16)] = make_int2(total, 0);
+        }
+        __syncwarp();
+        warp_stream(ls.L, seg, total, tsup, h, tl);
         __syncwarp();
         for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
         __syncwarp();
@@ -1114,7 +1142,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
                nshards, wt, hc, tiny);
 
     IsectKernels& K = g_k[ctx->device & 15];
-    const size_t wsm = size_t(W_WARPS) * W_SLOTS * sizeof(uint32_t);
+    const size_t wsm = size_t(W_WARPS) * (W_SLOTS * sizeof(uint32_t) + (W_SEG + 1) * sizeof(int2));
     const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(NSEG + 1) * sizeof(int2) +
                        size_t(2 * NSEG) * sizeof(int);
     if (K.warp_blocks == 0) {

@@ -20,7 +20,7 @@ __all__ = ["owner_of", "shard_of", "reduce_counts", "tc_cetc_distributed"]
 # intersect.cu tier thresholds and block sizes (defaults): owners of degree
 # <= TINY are one item; <= WT are cut into blocks of PW partners, larger ones
 # into blocks of PC partners.
-TINY, WT, PW, PC = 16, 512, 64, 1024
+TINY, WT, PW, PC = 16, 256, 64, 1024  # intersect.cu TINY, TCB_WT, TCB_PW, PC
 
 
 def owner_of(u, v, du, dv):

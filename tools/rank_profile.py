@@ -44,3 +44,21 @@ a, b = int(above_id.sum()), int(above_rank.sum())
 print(f"{name}: OFF stream {off:.4e}  same-level: id rule {a:.4e}  rank rule {b:.4e}  "
       f"total id {off + a:.4e}  total rank {off + b:.4e} ({(off + b) / (off + a):.3f})")
 # owner tables: id rule SUP(x) (same-level > x) vs rank rule (same-level ranked above x)
+# degree-bucket prefixes (what the kernels stream): w in UP(p) with
+# bucket(d(w)) >= bucket(d(x)), at 1 and 2 buckets per octave, per tier
+dx = deg[x]
+for per_oct in (1, 2, 4):
+    def bk(d):
+        lg = torch.floor(torch.log2(d.clamp(min=1).double())).long()
+        frac = d.double() / torch.pow(2.0, lg.double())
+        return lg * per_oct + torch.floor((frac - 1.0) * per_oct).long()
+    rk_src = rank[s_src] if False else None
+    up = rank[s_nb] > rank[s_src]
+    b_nb = bk(deg[s_nb])
+    keys2, _ = torch.sort(s_src[up] * 256 + (255 - b_nb[up]))
+    kx = bk(dx)
+    pref = torch.searchsorted(keys2, p * 256 + (255 - kx), right=True) - \
+        torch.searchsorted(keys2, p * 256, right=False)
+    for tier, m in (("warp", (dx > 16) & (dx <= 512)), ("cta", dx > 512), ("all", dx > 0)):
+        print(f"  {per_oct}/octave {tier}: bucket prefix {int(pref[m].sum()):.4e}  exact {int(above_rank[m].sum()):.4e}  "
+              f"OFF {int(n_off[p][m].sum()):.4e}")
