@@ -250,21 +250,34 @@ struct Lists {
 // ---------------------------------------------------------------------------
 // 1. owner-grouped selection + entry classes
 
-// The owner predicate is evaluated once (two random vinfo gathers per
-// entry) into a bitmask, one ballot word per 32 entries; both scan passes
-// then read bits only.  The same gathers give the OFF / SUP class bits.
+// The owner predicate is evaluated once (two random gathers per entry) into
+// a bitmask, one ballot word per 32 entries; both scan passes then read bits
+// only.  The same gathers give the OFF / UP class bits.  The gathers read the
+// packed 32-bit (level, degree) key when every vertex fits it (4n bytes: the
+// RMAT-24 table stays in L2), else the int2 vinfo.
+constexpr int KEY_DB = 22;  // degree bits of the packed key; level gets the top 10
 __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
-                             const int2* __restrict__ vinfo, int64_t nnz, int fwd,
+                             const int2* __restrict__ vinfo, const uint32_t* __restrict__ key32,
+                             const unsigned long long* __restrict__ nopack, int64_t nnz, int fwd,
                              uint32_t* __restrict__ bits, uint2* __restrict__ cls) {
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const unsigned lane = lane_id();
+    const bool packed = *nopack == 0;
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < nnz;
          base += gthreads) {
         const int64_t e = base + lane;
         bool keep = false, off = false, sup = false;
         if (e < nnz) {
             const int x = src[e], y = nb[e];
-            const int2 a = vinfo[x], b = vinfo[y];
+            int2 a, b;
+            if (packed) {
+                const uint32_t ka = key32[x], kb = key32[y];
+                a = make_int2(int(ka >> KEY_DB), int(ka & ((1u << KEY_DB) - 1)));
+                b = make_int2(int(kb >> KEY_DB), int(kb & ((1u << KEY_DB) - 1)));
+            } else {
+                a = vinfo[x];
+                b = vinfo[y];
+            }
             keep = a.x == b.x && (a.y > b.y || (a.y == b.y && x < y));
             off = fwd || a.x != b.x;
             sup = !fwd && a.x == b.x && !keep;  // UP: same level, y owns the edge
@@ -280,11 +293,12 @@ __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __r
 }
 
 void owner_select(Context* ctx, const int64_t* row, const int32_t* src, const int32_t* nb,
-                  const int2* vinfo, int64_t nnz, int fwd, uint2* cls, int32_t* P,
-                  int64_t* seg_beg, int64_t* seg_end, int64_t* d_ncover) {
+                  const int2* vinfo, const uint32_t* key32, const unsigned long long* nopack,
+                  int64_t nnz, int fwd, uint2* cls, int32_t* P, int64_t* seg_beg,
+                  int64_t* seg_end, int64_t* d_ncover) {
     uint32_t* bits = ctx->wsT<uint32_t>(WS_QUEUE_A, (nnz + 31) / 32);
-    TCB_LAUNCH(ctx, k_owner_bits, grid_for(ctx, nnz, 256), 256, 0, src, nb, vinfo, nnz, fwd, bits,
-               cls);
+    TCB_LAUNCH(ctx, k_owner_bits, grid_for(ctx, nnz, 256), 256, 0, src, nb, vinfo, key32, nopack,
+               nnz, fwd, bits, cls);
     const uint32_t* B = bits;
     scan_apply(
         ctx, nnz,
@@ -298,11 +312,21 @@ void owner_select(Context* ctx, const int64_t* row, const int32_t* src, const in
         d_ncover);
 }
 
+// Per vertex: (level, degree), the packed key and the degree bucket.
 __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restrict__ level,
-                        int64_t n, int2* __restrict__ vinfo) {
+                        int64_t n, int2* __restrict__ vinfo, uint32_t* __restrict__ key32,
+                        uint8_t* __restrict__ dbk, unsigned long long* nopack) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
-        vinfo[v] = make_int2(level[v], int(row[v + 1] - row[v]));
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        const int l = level[v], d = int(row[v + 1] - row[v]);
+        vinfo[v] = make_int2(l, d);
+        dbk[v] = uint8_t(dbucket(d));
+        const bool fits = l >= 0 && l < (1 << (32 - KEY_DB)) && d < (1 << KEY_DB);
+        key32[v] = fits ? (uint32_t(l) << KEY_DB) | uint32_t(d) : 0u;
+        const unsigned act = __activemask();
+        const unsigned bad = __ballot_sync(act, !fits);
+        if (bad && int(lane_id()) == __ffs(act) - 1) atomicExch(nopack, 1ull);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -322,81 +346,90 @@ __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
     }
 }
 
-// OFF entries go to their slot; UP entries count into their row's degree
-// bucket (ucur = per-row histogram, zeroed by the caller).
-__global__ void k_scatter_lists(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
-                                int64_t nnz, const uint2* __restrict__ cls,
-                                const unsigned long long* __restrict__ pre,
-                                const int2* __restrict__ vinfo, int32_t* __restrict__ L,
-                                int* __restrict__ ucur) {
+// OFF entries go to their slot (word prefix + popc).
+__global__ void k_scatter_off(const int32_t* __restrict__ nb, int64_t nnz,
+                              const uint2* __restrict__ cls,
+                              const unsigned long long* __restrict__ pre,
+                              int32_t* __restrict__ L) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-        const uint2 c = cls[e >> 5];
-        const uint32_t bit = 1u << (e & 31);
-        if (c.x & bit) {
-            L[rank_off(cls, pre, e)] = nb[e];
-        } else if (c.y & bit) {
-            const int w = nb[e];
-            atomicAdd(&ucur[int64_t(src[e]) * NBKT + dbucket(vinfo[w].y)], 1);
-        }
-    }
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride)
+        if (cls[e >> 5].x & (1u << (e & 31))) L[rank_off(cls, pre, e)] = nb[e];
 }
 
-// Per row: ucnt[k] = entries in buckets >= k (the stream prefix for an owner
-// of bucket k); ucur[k] becomes the start of bucket k (buckets descending).
-__global__ void k_up_offsets(int64_t n, const uint2* __restrict__ vb, int* __restrict__ ucnt,
-                             int* __restrict__ ucur) {
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-        int4* cnt = reinterpret_cast<int4*>(ucnt + v * NBKT);
-        int4* cur = reinterpret_cast<int4*>(ucur + v * NBKT);
-        if (vb[v + 1].y == vb[v].y) {  // empty UP row: zero prefix counts
-#pragma unroll
-            for (int i = 0; i < NBKT / 4; ++i) cnt[i] = make_int4(0, 0, 0, 0);
+// UP rows, one warp per row: a counting sort by degree bucket (largest
+// first) with the histogram and cursors in shared memory, and the row's
+// prefix counts ucnt[v][k] = entries in buckets >= k.  Lanes scan the row's
+// class words 32 at a time, so a hub row with few UP entries costs d/1024
+// iterations.  Rows of isolated vertices are never read and are skipped.
+constexpr int UP_WARPS = 8;
+static_assert(NBKT == 32, "one degree bucket per lane");
+__global__ void __launch_bounds__(UP_WARPS * 32)
+    k_build_up(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
+               const uint2* __restrict__ cls, const uint8_t* __restrict__ dbk,
+               const uint2* __restrict__ vb, int32_t* __restrict__ L, int* __restrict__ ucnt) {
+    __shared__ int s_h[UP_WARPS][NBKT];
+    const int warp = threadIdx.x >> 5;
+    const int lane = int(lane_id());
+    int* h = s_h[warp];
+    const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t v = gw; v < n; v += nwarps) {
+        const int64_t r0 = row[v], r1 = row[v + 1];
+        if (r1 == r0) continue;
+        const uint32_t u0 = vb[v].y, nup = vb[v + 1].y - u0;
+        if (nup == 0) {
+            ucnt[v * NBKT + lane] = 0;
             continue;
         }
-        int h[NBKT];
-#pragma unroll
-        for (int i = 0; i < NBKT / 4; ++i) {
-            const int4 q = cur[i];
-            h[4 * i] = q.x;
-            h[4 * i + 1] = q.y;
-            h[4 * i + 2] = q.z;
-            h[4 * i + 3] = q.w;
-        }
-        int acc = 0;
-#pragma unroll
-        for (int k = NBKT - 1; k >= 0; --k) {
-            const int c = h[k];
-            h[k] = acc;  // start of bucket k
-            acc += c;
-        }
-        // h[k] = start of bucket k = entries in buckets > k; cnt[k] = entries
-        // in buckets >= k = start of bucket k-1 (the row size for k = 0)
-#pragma unroll
-        for (int i = 0; i < NBKT / 4; ++i) {
-            cur[i] = make_int4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
-            int t[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int k = 4 * i + j;
-                t[j] = k == 0 ? acc : h[k - 1];
+        h[lane] = 0;
+        __syncwarp();
+        const int64_t j0 = r0 >> 5, j1 = (r1 - 1) >> 5;
+        // pass 1: bucket histogram
+        for (int64_t jb = j0; jb <= j1; jb += 32) {
+            const int64_t j = jb + lane;
+            uint32_t m = 0;
+            if (j <= j1) {
+                m = cls[j].y;
+                if (j == j0) m &= ~0u << (r0 & 31);
+                if (j == j1 && ((r1 & 31) != 0)) m &= (1u << (r1 & 31)) - 1u;
             }
-            cnt[i] = make_int4(t[0], t[1], t[2], t[3]);
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                atomicAdd(&h[dbk[nb[j * 32 + b]]], 1);
+            }
         }
-    }
-}
-
-__global__ void k_scatter_up(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
-                             int64_t nnz, const uint2* __restrict__ cls,
-                             const int2* __restrict__ vinfo, const uint2* __restrict__ vb,
-                             int32_t* __restrict__ L, int* __restrict__ ucur) {
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-        if (!(cls[e >> 5].y & (1u << (e & 31)))) continue;
-        const int v = src[e], w = nb[e];
-        const int pos = atomicAdd(&ucur[int64_t(v) * NBKT + dbucket(vinfo[w].y)], 1);
-        L[int64_t(vb[v].y) + pos] = w;
+        __syncwarp();
+        // buckets descending: start[k] = entries in buckets > k
+        const int c = h[lane];
+        int incl = c;  // suffix sum over lanes >= lane
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_down_sync(0xffffffffu, incl, o);
+            if (lane + o < 32) incl += t;
+        }
+        ucnt[v * NBKT + lane] = incl;
+        __syncwarp();
+        h[lane] = incl - c;
+        __syncwarp();
+        // pass 2: scatter
+        for (int64_t jb = j0; jb <= j1; jb += 32) {
+            const int64_t j = jb + lane;
+            uint32_t m = 0;
+            if (j <= j1) {
+                m = cls[j].y;
+                if (j == j0) m &= ~0u << (r0 & 31);
+                if (j == j1 && ((r1 & 31) != 0)) m &= (1u << (r1 & 31)) - 1u;
+            }
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int w = nb[j * 32 + b];
+                const int pos = atomicAdd(&h[dbk[w]], 1);
+                L[int64_t(u0) + pos] = w;
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -1075,7 +1108,11 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     const int64_t nnz = 2 * m;
     require(nnz < (int64_t(1) << 32), "intersection: 2m must be below 2^32");
     const int64_t nwords = (nnz + 31) / 32;
-    int2* vinfo = ctx->wsT<int2>(WS_MISC, n);
+    // per vertex: int2 vinfo, packed key, degree bucket
+    char* mbuf = static_cast<char*>(ctx->ws(WS_MISC, size_t(n) * (8 + 4 + 1) + 64));
+    int2* vinfo = reinterpret_cast<int2*>(mbuf);
+    uint32_t* key32 = reinterpret_cast<uint32_t*>(mbuf + size_t(n) * 8);
+    uint8_t* dbk = reinterpret_cast<uint8_t*>(mbuf + size_t(n) * 12);
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
     int* split = ctx->wsT<int>(WS_COVER_V, size_t(n) * (F + 1));
@@ -1085,12 +1122,11 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         ctx->ws(WS_CLASS, cls_bytes + size_t(nwords + 1) * sizeof(unsigned long long)));
     uint2* cls = reinterpret_cast<uint2*>(cbuf);
     unsigned long long* pre = reinterpret_cast<unsigned long long*>(cbuf + cls_bytes);
-    // per-vertex (OFF start, UP start), then the UP bucket tables ucnt, ucur
+    // per-vertex (OFF start, UP start), then the UP prefix table ucnt
     char* vbuf = static_cast<char*>(ctx->ws(
-        WS_VBEG, (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16 + 2 * size_t(n) * NBKT * sizeof(int)));
+        WS_VBEG, (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16 + size_t(n) * NBKT * sizeof(int)));
     uint2* vb = reinterpret_cast<uint2*>(vbuf);
     int* ucnt = reinterpret_cast<int*>(vbuf + (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16);
-    int* ucur = ucnt + size_t(n) * NBKT;
     // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
     const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
     const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
@@ -1110,9 +1146,13 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     const int rshift = max(0, bits_for(n) - LOG_F);
     Lists ls{L, vb, split, ucnt, rshift};
 
-    TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo);
+    unsigned long long* nopack = &C->scratch[13];
+    TCB_CUDA(cudaMemsetAsync(nopack, 0, sizeof(unsigned long long), ctx->stream));
+    TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo, key32, dbk,
+               nopack);
     TCB_CUDA(cudaMemsetAsync(cls + nwords, 0, sizeof(uint2), ctx->stream));
-    owner_select(ctx, row, src, nb, vinfo, nnz, fwd, cls, P, seg, seg + n, d_ncover);
+    owner_select(ctx, row, src, nb, vinfo, key32, nopack, nnz, fwd, cls, P, seg, seg + n,
+                 d_ncover);
     ctx->record(3);
     const uint2* ccls = cls;
     scan_apply(
@@ -1128,12 +1168,10 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     // rows of empty OFF lists stay zero (k_split_points writes only rows
     // with entries)
     TCB_CUDA(cudaMemsetAsync(split, 0, size_t(n) * (F + 1) * sizeof(int), ctx->stream));
-    TCB_CUDA(cudaMemsetAsync(ucur, 0, size_t(n) * NBKT * sizeof(int), ctx->stream));
-    TCB_LAUNCH(ctx, k_scatter_lists, grid_for(ctx, nnz, 256), 256, 0, src, nb, nnz, ccls,
-               (const unsigned long long*)pre, (const int2*)vinfo, L, ucur);
-    TCB_LAUNCH(ctx, k_up_offsets, grid_for(ctx, n, 256), 256, 0, n, (const uint2*)vb, ucnt, ucur);
-    TCB_LAUNCH(ctx, k_scatter_up, grid_for(ctx, nnz, 256), 256, 0, src, nb, nnz, ccls,
-               (const int2*)vinfo, (const uint2*)vb, L, ucur);
+    TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
+               (const unsigned long long*)pre, L);
+    TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
+               (const uint8_t*)dbk, (const uint2*)vb, L, ucnt);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
                (const unsigned long long*)pre, (const int32_t*)L, (const uint2*)vb, rshift,
                split);
