@@ -78,7 +78,7 @@ namespace tcb {
 #define TCB_PW 64
 #endif
 constexpr int WT = TCB_WT;            // warp tier: owner degree <= WT
-constexpr int W_SLOTS = 2 * WT;       // per-warp bucket table: load <= 1/2
+constexpr int W_SLOTS = 4 * WT;       // per-warp bucket table: load <= 1/4
 constexpr int W_WARPS = 8;
 constexpr int PW = TCB_PW;            // partners per warp item
 constexpr int C_THREADS = 512;        // 2 CTAs per SM
@@ -628,6 +628,8 @@ __device__ __forceinline__ void warp_stream(const int32_t* __restrict__ L, const
                 w[j] = L[base + uint32_t(i)];
             }
         }
+        // the next round starts in (or just before) the last lane's slice
+        kc = __shfl_sync(0xffffffffu, k, 31);
         uint32_t hm = 0;
 #pragma unroll
         for (int j = 0; j < JW; ++j)
@@ -665,7 +667,7 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
         const int no = int(ls.ob(x + 1) - o0), nu = int(ls.ub(x + 1) - s0), nx = no + nu;
         const int dx = vinfo[x].y;
         const int kx = dbucket(dx);
-        const int slots = max(16, 2 << ceil_log2_dev(nx));
+        const int slots = max(16, 4 << ceil_log2_dev(nx));
         BucketHash h;
         h.setup(tab, slots);
         for (int i = lane; i < nx; i += 32) {
