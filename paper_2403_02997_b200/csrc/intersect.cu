@@ -358,16 +358,22 @@ __global__ void k_scatter_off(const int32_t* __restrict__ nb, int64_t nnz,
 
 // UP rows, one warp per row: a counting sort by degree bucket (largest
 // first) with the histogram and cursors in shared memory, and the row's
-// prefix counts ucnt[v][k] = entries in buckets >= k.  Lanes scan the row's
-// class words 32 at a time, so a hub row with few UP entries costs d/1024
-// iterations.  Rows of isolated vertices are never read and are skipped.
+// prefix counts ucnt[v][k] = entries in buckets >= k.  Short rows (d <=
+// UP_SHORT): a lane per entry, the UP entries and their buckets kept in
+// shared memory between the histogram and the scatter.  Long rows: lanes
+// scan the row's class words 32 at a time (a hub row with few UP entries
+// costs d/1024 iterations) and gather twice.  Rows of isolated vertices are
+// never read and are skipped.
 constexpr int UP_WARPS = 8;
+constexpr int UP_SHORT = 256;
 static_assert(NBKT == 32, "one degree bucket per lane");
 __global__ void __launch_bounds__(UP_WARPS * 32)
     k_build_up(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                const uint2* __restrict__ cls, const uint8_t* __restrict__ dbk,
                const uint2* __restrict__ vb, int32_t* __restrict__ L, int* __restrict__ ucnt) {
     __shared__ int s_h[UP_WARPS][NBKT];
+    __shared__ int s_w[UP_WARPS][UP_SHORT];
+    __shared__ uint8_t s_b[UP_WARPS][UP_SHORT];
     const int warp = threadIdx.x >> 5;
     const int lane = int(lane_id());
     int* h = s_h[warp];
@@ -383,6 +389,41 @@ __global__ void __launch_bounds__(UP_WARPS * 32)
         }
         h[lane] = 0;
         __syncwarp();
+        if (r1 - r0 <= UP_SHORT) {
+            int nbuf = 0;
+            for (int64_t e0 = r0; e0 < r1; e0 += 32) {
+                const int64_t e = e0 + lane;
+                const bool up = e < r1 && ((cls[e >> 5].y >> (e & 31)) & 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, up);
+                if (up) {
+                    const int w = nb[e];
+                    const int b = dbk[w];
+                    const int q = nbuf + __popc(bal & lanemask_lt());
+                    s_w[warp][q] = w;
+                    s_b[warp][q] = uint8_t(b);
+                    atomicAdd(&h[b], 1);
+                }
+                nbuf += __popc(bal);
+            }
+            __syncwarp();
+            const int c = h[lane];
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_down_sync(0xffffffffu, incl, o);
+                if (lane + o < 32) incl += t;
+            }
+            ucnt[v * NBKT + lane] = incl;
+            __syncwarp();
+            h[lane] = incl - c;
+            __syncwarp();
+            for (int i = lane; i < nbuf; i += 32) {
+                const int pos = atomicAdd(&h[s_b[warp][i]], 1);
+                L[int64_t(u0) + pos] = s_w[warp][i];
+            }
+            __syncwarp();
+            continue;
+        }
         const int64_t j0 = r0 >> 5, j1 = (r1 - 1) >> 5;
         // pass 1: bucket histogram
         for (int64_t jb = j0; jb <= j1; jb += 32) {
