@@ -31,10 +31,10 @@
 // below the endpoint are never read, and a hit needs no level lookup: the
 // list it was streamed from says which tally it belongs to.
 //
-//  1. owner_select: ordered compaction over the CSR entries (x, y) keeping
-//     level[x]==level[y] && owns(x, y).  Entries are in row order, so each
-//     owner's partners come out contiguous: P[seg_beg[x], seg_end[x]).  The
-//     same pass writes the OFF/UP class bits of every entry.
+//  1. owner bits: a keep bit per CSR entry (x, y) with level[x]==level[y] &&
+//     owns(x, y), and the OFF/UP class bits.  A word-level prefix of the keep
+//     bits compacts the kept entries in row order, so each owner's partners
+//     come out contiguous: P[seg_beg[x], seg_end[x]).
 //  2. lists: word prefixes of the class bits give every entry its slot in
 //     the OFF array and every row its UP range (no second scan); UP rows are
 //     counting-sorted by degree bucket (per-row histogram, prefix, scatter).
@@ -292,24 +292,26 @@ __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __r
     }
 }
 
-void owner_select(Context* ctx, const int64_t* row, const int32_t* src, const int32_t* nb,
-                  const int2* vinfo, const uint32_t* key32, const unsigned long long* nopack,
-                  int64_t nnz, int fwd, uint2* cls, int32_t* P, int64_t* seg_beg,
-                  int64_t* seg_end, int64_t* d_ncover) {
-    uint32_t* bits = ctx->wsT<uint32_t>(WS_QUEUE_A, (nnz + 31) / 32);
+// Keep bits (x owns a horizontal edge) and class bits of every CSR entry.
+// The cover edges are then compacted without an ordered scan: a word-level
+// prefix of the keep bits gives each kept entry its slot in P (k_scatter_off)
+// and each owner its segment [seg_beg, seg_end) (k_list_bounds).
+uint32_t* owner_bits(Context* ctx, const int32_t* src, const int32_t* nb, const int2* vinfo,
+                     const uint32_t* key32, const unsigned long long* nopack, int64_t nnz,
+                     int fwd, uint2* cls) {
+    const int64_t nwords = (nnz + 31) / 32;
+    uint32_t* bits = ctx->wsT<uint32_t>(WS_QUEUE_A, nwords + 1);
+    TCB_CUDA(cudaMemsetAsync(bits + nwords, 0, sizeof(uint32_t), ctx->stream));
     TCB_LAUNCH(ctx, k_owner_bits, grid_for(ctx, nnz, 256), 256, 0, src, nb, vinfo, key32, nopack,
                nnz, fwd, bits, cls);
-    const uint32_t* B = bits;
-    scan_apply(
-        ctx, nnz,
-        [B] __device__(int64_t e) -> int64_t { return (B[e >> 5] >> (e & 31)) & 1u; },
-        [src, nb, row, P, seg_beg, seg_end] __device__(int64_t e, int64_t pos, int64_t keep) {
-            const int x = src[e];
-            if (keep) P[pos] = nb[e];
-            if (e == row[x]) seg_beg[x] = pos;
-            if (e == row[x + 1] - 1) seg_end[x] = pos + keep;
-        },
-        d_ncover);
+    return bits;
+}
+
+__device__ __forceinline__ int64_t rank_keep(const uint32_t* __restrict__ bits,
+                                             const unsigned long long* __restrict__ prek,
+                                             int64_t p) {
+    const int64_t j = p >> 5;
+    return int64_t(prek[j]) + __popc(bits[j] & ((1u << (p & 31)) - 1u));
 }
 
 // Per vertex: (level, degree), the packed key and the degree bucket.
@@ -336,24 +338,36 @@ __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restri
 __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
                               const uint2* __restrict__ cls,
                               const unsigned long long* __restrict__ pre, int64_t nw,
-                              uint2* __restrict__ vb) {
+                              uint2* __restrict__ vb, const uint32_t* __restrict__ bits,
+                              const unsigned long long* __restrict__ prek,
+                              int64_t* __restrict__ seg_beg, int64_t* __restrict__ seg_end) {
     const int64_t noff = int64_t(pre[nw] & 0xFFFFFFFFull);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v <= n; v += stride) {
         const int64_t p = row[v];
+        if (v < n) {  // the owner's cover edges: P[seg_beg, seg_end)
+            seg_beg[v] = rank_keep(bits, prek, p);
+            seg_end[v] = rank_keep(bits, prek, row[v + 1]);
+        }
         vb[v] = make_uint2(uint32_t(rank_off(cls, pre, p)),
                            uint32_t(noff + rank_up(cls, pre, p)));
     }
 }
 
-// OFF entries go to their slot (word prefix + popc).
+// OFF entries go to their slot in L, kept entries (cover edges, owner
+// side) to theirs in P (word prefix + popc).
 __global__ void k_scatter_off(const int32_t* __restrict__ nb, int64_t nnz,
                               const uint2* __restrict__ cls,
                               const unsigned long long* __restrict__ pre,
-                              int32_t* __restrict__ L) {
+                              int32_t* __restrict__ L, const uint32_t* __restrict__ bits,
+                              const unsigned long long* __restrict__ prek,
+                              int32_t* __restrict__ P) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride)
-        if (cls[e >> 5].x & (1u << (e & 31))) L[rank_off(cls, pre, e)] = nb[e];
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
+        const uint32_t bit = 1u << (e & 31);
+        if (cls[e >> 5].x & bit) L[rank_off(cls, pre, e)] = nb[e];
+        if (bits[e >> 5] & bit) P[rank_keep(bits, prek, e)] = nb[e];
+    }
 }
 
 // UP rows, one warp per row: a counting sort by degree bucket (largest
@@ -1162,9 +1176,10 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     int32_t* L = ctx->wsT<int32_t>(WS_LISTS, nnz);
     const size_t cls_bytes = (size_t(nwords + 1) * sizeof(uint2) + 15) / 16 * 16;
     char* cbuf = static_cast<char*>(
-        ctx->ws(WS_CLASS, cls_bytes + size_t(nwords + 1) * sizeof(unsigned long long)));
+        ctx->ws(WS_CLASS, cls_bytes + 2 * size_t(nwords + 1) * sizeof(unsigned long long)));
     uint2* cls = reinterpret_cast<uint2*>(cbuf);
     unsigned long long* pre = reinterpret_cast<unsigned long long*>(cbuf + cls_bytes);
+    unsigned long long* prek = pre + (nwords + 1);
     // per-vertex (OFF start, UP start), then the UP prefix table ucnt
     char* vbuf = static_cast<char*>(ctx->ws(
         WS_VBEG, (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16 + size_t(n) * NBKT * sizeof(int)));
@@ -1194,8 +1209,13 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo, key32, dbk,
                nopack);
     TCB_CUDA(cudaMemsetAsync(cls + nwords, 0, sizeof(uint2), ctx->stream));
-    owner_select(ctx, row, src, nb, vinfo, key32, nopack, nnz, fwd, cls, P, seg, seg + n,
-                 d_ncover);
+    const uint32_t* bits = owner_bits(ctx, src, nb, vinfo, key32, nopack, nnz, fwd, cls);
+    scan_apply(
+        ctx, nwords, [bits] __device__(int64_t j) -> int64_t { return __popc(bits[j]); },
+        [prek] __device__(int64_t j, int64_t pos, int64_t) { prek[j] = (unsigned long long)pos; },
+        reinterpret_cast<int64_t*>(prek + nwords));
+    TCB_CUDA(cudaMemcpyAsync(d_ncover, prek + nwords, sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
     ctx->record(3);
     const uint2* ccls = cls;
     scan_apply(
@@ -1207,12 +1227,13 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         [pre] __device__(int64_t j, int64_t pos, int64_t) { pre[j] = (unsigned long long)pos; },
         reinterpret_cast<int64_t*>(pre + nwords));
     TCB_LAUNCH(ctx, k_list_bounds, grid_for(ctx, n + 1, 256), 256, 0, row, n, ccls,
-               (const unsigned long long*)pre, nwords, vb);
+               (const unsigned long long*)pre, nwords, vb, bits, (const unsigned long long*)prek,
+               seg, seg + n);
     // rows of empty OFF lists stay zero (k_split_points writes only rows
     // with entries)
     TCB_CUDA(cudaMemsetAsync(split, 0, size_t(n) * (F + 1) * sizeof(int), ctx->stream));
     TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
-               (const unsigned long long*)pre, L);
+               (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P);
     TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
                (const uint8_t*)dbk, (const uint2*)vb, L, ucnt);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
