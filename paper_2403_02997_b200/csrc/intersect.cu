@@ -91,7 +91,16 @@ constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
-constexpr int NBKT = 32;              // degree buckets: floor(log2 d)
+constexpr int NBKT = 32;
+// Per-vertex partner record for the CTA tier: one 32-byte sector with the
+// list starts, the OFF size and the UP prefix counts of the degree buckets
+// CTA-tier owners have (|UP(v)| <= sqrt(2m) < 2^16 since 2m < 2^32).
+constexpr int PR_K0 = 8, PR_NK = 10;  // buckets [8, 18): owner degrees 256 .. 2^18-1
+struct __align__(32) PRec {
+    uint32_t ob, ub, noff;
+    uint16_t uc[PR_NK];
+};
+static_assert(sizeof(PRec) == 32, "one sector per partner");              // degree buckets: floor(log2 d)
 __device__ __forceinline__ int dbucket(int d) { return 31 - __clz(max(d, 1)); }
 
 __device__ __forceinline__ int ceil_log2_dev(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
@@ -239,6 +248,7 @@ struct Lists {
     __device__ __forceinline__ int64_t ub(int64_t v) const { return int64_t(vb[v].y); }
     const int* __restrict__ split;  // [v*(F+1) + r] = OFF position of id range r
     const int* __restrict__ ucnt;   // [v*NBKT + k] = UP(v) entries with degree bucket >= k
+    const PRec* __restrict__ prec;  // per-vertex partner record (CTA tier)
     int rshift;
     // the part of UP(p) that can hold an apex of owner x (degree bucket kx):
     // neighbours of p with degree >= 2^kx, a prefix of UP(p)
@@ -384,7 +394,8 @@ static_assert(NBKT == 32, "one degree bucket per lane");
 __global__ void __launch_bounds__(UP_WARPS * 32)
     k_build_up(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                const uint2* __restrict__ cls, const uint8_t* __restrict__ dbk,
-               const uint2* __restrict__ vb, int32_t* __restrict__ L, int* __restrict__ ucnt) {
+               const uint2* __restrict__ vb, int32_t* __restrict__ L, int* __restrict__ ucnt,
+               PRec* __restrict__ prec) {
     __shared__ int s_h[UP_WARPS][NBKT];
     __shared__ int s_w[UP_WARPS][UP_SHORT];
     __shared__ uint8_t s_b[UP_WARPS][UP_SHORT];
@@ -396,9 +407,17 @@ __global__ void __launch_bounds__(UP_WARPS * 32)
     for (int64_t v = gw; v < n; v += nwarps) {
         const int64_t r0 = row[v], r1 = row[v + 1];
         if (r1 == r0) continue;
-        const uint32_t u0 = vb[v].y, nup = vb[v + 1].y - u0;
+        const uint2 b0 = vb[v], b1 = vb[v + 1];
+        const uint32_t u0 = b0.y, nup = b1.y - u0;
+        PRec* pr = prec + v;
+        if (lane == 0) {
+            pr->ob = b0.x;
+            pr->ub = b0.y;
+            pr->noff = b1.x - b0.x;
+        }
         if (nup == 0) {
             ucnt[v * NBKT + lane] = 0;
+            if (lane >= PR_K0 && lane < PR_K0 + PR_NK) pr->uc[lane - PR_K0] = 0;
             continue;
         }
         h[lane] = 0;
@@ -428,6 +447,7 @@ __global__ void __launch_bounds__(UP_WARPS * 32)
                 if (lane + o < 32) incl += t;
             }
             ucnt[v * NBKT + lane] = incl;
+            if (lane >= PR_K0 && lane < PR_K0 + PR_NK) pr->uc[lane - PR_K0] = uint16_t(incl);
             __syncwarp();
             h[lane] = incl - c;
             __syncwarp();
@@ -464,6 +484,7 @@ __global__ void __launch_bounds__(UP_WARPS * 32)
             if (lane + o < 32) incl += t;
         }
         ucnt[v * NBKT + lane] = incl;
+        if (lane >= PR_K0 && lane < PR_K0 + PR_NK) pr->uc[lane - PR_K0] = uint16_t(incl);
         __syncwarp();
         h[lane] = incl - c;
         __syncwarp();
@@ -999,15 +1020,22 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 if (yy[r] < 0) continue;
                 const int y = yy[r];
                 const int* sy = ls.split + int64_t(y) * (F + 1);
-                const uint2 v0 = ls.vb[y];
-                // range ends at 0 / F come from the bounds, not the split row
+                // the record's header and the word holding uc[kx - PR_K0]: one sector
+                const uint32_t* rw = reinterpret_cast<const uint32_t*>(ls.prec + y);
+                const uint4 hd = *reinterpret_cast<const uint4*>(rw);  // ob, ub, noff, uc[0..1]
+                const bool in_rec = kx >= PR_K0 && kx < PR_K0 + PR_NK;
+                const int ui = kx - PR_K0;
+                const uint32_t uw = in_rec ? rw[3 + (ui >> 1)] : 0u;
+                // range ends at 0 / F come from the record, not the split row
                 const int a = q0 > 0 ? sy[q0] : 0;
-                const int b = q1 == F ? int(ls.vb[y + 1].x - v0.x) : sy[q1];
-                s_pos[t] = v0.x + uint32_t(a);
+                const int b = q1 == F ? int(hd.z) : sy[q1];
+                s_pos[t] = hd.x + uint32_t(a);
                 s_len[t] = no ? b - a : 0;
                 // the prefix of UP(y) that can be in UP(x) (degree >= 2^kx)
-                s_pos[PC + t] = v0.y;
-                s_len[PC + t] = ns ? ls.up_prefix(y, kx) : 0;
+                s_pos[PC + t] = hd.y;
+                s_len[PC + t] = !ns ? 0
+                                : in_rec ? int((uw >> ((ui & 1) * 16)) & 0xFFFFu)
+                                         : ls.up_prefix(y, kx);
             }
         }
         // Passes: one when both owner slices fit the table; otherwise the
@@ -1180,11 +1208,13 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     uint2* cls = reinterpret_cast<uint2*>(cbuf);
     unsigned long long* pre = reinterpret_cast<unsigned long long*>(cbuf + cls_bytes);
     unsigned long long* prek = pre + (nwords + 1);
-    // per-vertex (OFF start, UP start), then the UP prefix table ucnt
+    // per-vertex (OFF start, UP start), the partner records, the UP prefix table ucnt
+    const size_t vb_bytes = (size_t(n + 1) * sizeof(uint2) + 31) / 32 * 32;
     char* vbuf = static_cast<char*>(ctx->ws(
-        WS_VBEG, (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16 + size_t(n) * NBKT * sizeof(int)));
+        WS_VBEG, vb_bytes + size_t(n) * sizeof(PRec) + size_t(n) * NBKT * sizeof(int)));
     uint2* vb = reinterpret_cast<uint2*>(vbuf);
-    int* ucnt = reinterpret_cast<int*>(vbuf + (size_t(n + 1) * sizeof(uint2) + 15) / 16 * 16);
+    PRec* prec = reinterpret_cast<PRec*>(vbuf + vb_bytes);
+    int* ucnt = reinterpret_cast<int*>(vbuf + vb_bytes + size_t(n) * sizeof(PRec));
     // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
     const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
     const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
@@ -1202,7 +1232,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     unsigned long long* fc = &C->scratch[8];
     int64_t* d_ncover = reinterpret_cast<int64_t*>(&C->ncover);
     const int rshift = max(0, bits_for(n) - LOG_F);
-    Lists ls{L, vb, split, ucnt, rshift};
+    Lists ls{L, vb, split, ucnt, prec, rshift};
 
     unsigned long long* nopack = &C->scratch[13];
     TCB_CUDA(cudaMemsetAsync(nopack, 0, sizeof(unsigned long long), ctx->stream));
@@ -1235,7 +1265,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
                (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P);
     TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
-               (const uint8_t*)dbk, (const uint2*)vb, L, ucnt);
+               (const uint8_t*)dbk, (const uint2*)vb, L, ucnt, prec);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
                (const unsigned long long*)pre, (const int32_t*)L, (const uint2*)vb, rshift,
                split);
