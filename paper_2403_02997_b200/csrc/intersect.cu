@@ -22,7 +22,7 @@
 // UP(x)∩UP(p) (same level, ranked above both endpoints).  Every same-level
 // triangle a > b > c (owner order) is therefore found exactly once, at its
 // edge (b, c) with apex a — the reference keeps exactly one apex per such
-// triangle too (w > max(u, v), _kernels.py:687) — so the SUP tally equals
+// triangle too (w > max(u, v), _kernels.py:687) — so the UP tally equals
 // the reference's T - c1 and its c2 (every same-level hit, 3 per triangle,
 // _kernels.py:745-748) is 3 x this tally; the counters hold c2 in those
 // units.  Ranking by degree keeps the same-level stream short: p streams
@@ -85,7 +85,7 @@ constexpr int C_THREADS = 512;        // 2 CTAs per SM
 constexpr int HC = TCB_HC;            // staged ids per CTA item
 constexpr int C_SLOTS = 4 * HC;       // load <= 1/4 (64 KB)
 constexpr int PC = 2 * C_THREADS;     // partners per CTA item
-constexpr int NSEG = 2 * PC;          // stream segments: partner t -> 2t (OFF), 2t+1 (SUP)
+constexpr int NSEG = 2 * PC;          // stream slices: partner t -> OFF slice t, UP slice PC + t
 constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per lane)
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
@@ -108,7 +108,7 @@ __device__ __forceinline__ int ceil_log2_dev(int x) { return x <= 1 ? 0 : 32 - _
 // ---------------------------------------------------------------------------
 // entry classes: bit i of cls[j].x / .y = CSR entry 32j+i is OFF / UP.
 // pre[j] = exclusive prefix over words of popc(.x) | popc(.y) << 32, so an
-// entry's slot in the OFF (SUP) array is a prefix read plus one popc.
+// entry's slot in the OFF array (and a row's UP range) is a prefix read plus one popc.
 
 __device__ __forceinline__ int64_t rank_off(const uint2* __restrict__ cls,
                                             const unsigned long long* __restrict__ pre,
@@ -212,9 +212,10 @@ struct CuckooHash {
     }
 };
 
-// c1 / same-level tallies.  `sup` counts SUP∩SUP hits, each one a same-level
-// apex the reference's T keeps (w > max(u, v)); the reference's c2 counts
-// every same-level hit, 3 per all-horizontal triangle, so c2 = 3 sup over the
+// c1 / same-level tallies.  `sup` counts UP∩UP hits: each all-horizontal
+// triangle once, at the edge whose apex ranks above both endpoints (the
+// reference keeps one of the three too, w > max(u, v)); the reference's c2
+// counts every same-level hit, 3 per such triangle, so c2 = 3 sup over the
 // cover set and T = c1 + c2/3 (formed in capi.cu fill_result).
 struct Tally {
     unsigned long long c1 = 0, sup = 0;
@@ -342,7 +343,7 @@ __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restri
 }
 
 // ---------------------------------------------------------------------------
-// 2. OFF / SUP lists.  The OFF array comes first; SUP starts at NOFF (the
+// 2. OFF / UP lists.  The OFF array comes first; UP starts at NOFF (the
 //    class total, pre[nw] low half).  ob/sb hold absolute positions in L.
 
 __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
@@ -803,10 +804,10 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
 // ---------------------------------------------------------------------------
 // 6. CTA tier
 //
-// Every partner t has two unread slices, OFF at index t and SUP at PC + t
+// Every partner t has two unread slices, OFF at index t and UP at PC + t
 // (s_pos / s_len).  Each pass takes a count from every slice, and the
 // non-empty ones are compacted into the stream table s_seg: all OFF slices
-// first, then all SUP slices, so an element's class is just
+// first, then all UP slices, so an element's class is just
 // (stream index >= tsup) and a walk never steps over an empty slice.
 // s_seg[k] = (first stream index of slice k, its base): element i of slice k
 // is L[base + i] (uint32 arithmetic; 2m < 2^32).
@@ -836,7 +837,7 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
     int nx = s_seg[k + 1].x;
     uint32_t base = uint32_t(s_seg[k].y);
     const int i0 = c0 + int(lane_id());
-    // this lane's elements j >= jt come from SUP slices (stream index >= tsup)
+    // this lane's elements j >= jt come from UP slices (stream index >= tsup)
     const int jt = min(J, max(0, (tsup - i0 + 31) >> 5));
     int w[J];
 #pragma unroll
@@ -1107,8 +1108,8 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         cnt[r] = c;
                     }
                 }
-                int64_t eo;  // exclusive element prefix: OFF low 32 bits, SUP high
-                int en;      // exclusive non-empty prefix: OFF low 16 bits, SUP high
+                int64_t eo;  // exclusive element prefix: OFF low 32 bits, UP high
+                int en;      // exclusive non-empty prefix: OFF low 16 bits, UP high
                 int64_t to;
                 int tn;
                 block_scan_pair(int64_t(cnt[0] + cnt[1]) | (int64_t(cnt[2] + cnt[3]) << 32),

@@ -15,10 +15,11 @@ charged to the call.
   _kernels.py:787-805) plus the triangles of the horizontal subgraph G0
   (forward-hashed on G0, recursively split for -SR).  Those two terms are
   exactly the cover-edge pass's two tallies — one horizontal edge with an
-  off-level apex is c1, a G0 triangle is found once per edge (c2 = 3 T(G0)) —
-  so the GPU computes both in one fused pass and returns c1 + c2/3; the CPU
-  split into two graphs exists to cut merge work, which the owner-hash
-  intersection already avoids.
+  off-level apex is c1, and a G0 triangle is the same-level tally (counted
+  once, at the edge whose apex ranks above both endpoints: the forward count
+  on G0 in owner order; c2 = 3 T(G0)) — so the GPU computes both in one
+  fused pass and returns c1 + c2/3; the CPU split into two graphs exists to
+  cut merge work, which the OFF/UP list intersection already avoids.
 """
 from __future__ import annotations
 
