@@ -112,7 +112,7 @@ void fill_result(Context* ctx, tcb_result* out, bool partial = false) {
     r.ncover = int64_t(h.ncover);
     r.components = int64_t(h.components);
     r.max_level = h.max_level;
-#if defined(TCB_NOPROBE) || defined(TCB_NOLOAD) || defined(TCB_NOSTREAM)  // measurement-only
+#if defined(TCB_NOPROBE) || defined(TCB_NOLOAD) || defined(TCB_NOSTREAM) || defined(TCB_NOUPSTREAM) || defined(TCB_NOOFFSTREAM)  // measurement-only
     partial = true;
 #endif
     if (!partial && r.c2 % 3 != 0)  // parallel.py:127-128

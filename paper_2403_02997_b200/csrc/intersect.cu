@@ -1037,6 +1037,12 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 s_len[PC + t] = !ns ? 0
                                 : in_rec ? int((uw >> ((ui & 1) * 16)) & 0xFFFFu)
                                          : ls.up_prefix(y, kx);
+#ifdef TCB_NOUPSTREAM  // measurement-only: drop the UP slices
+                s_len[PC + t] = 0;
+#endif
+#ifdef TCB_NOOFFSTREAM  // measurement-only: drop the OFF slices
+                s_len[t] = 0;
+#endif
             }
         }
         // Passes: one when both owner slices fit the table; otherwise the
