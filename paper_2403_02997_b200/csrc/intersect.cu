@@ -514,24 +514,49 @@ __global__ void __launch_bounds__(UP_WARPS * 32)
 // 3. split points: split[v*(F+1) + r] = first position in OFF(v) of an id
 //    >= r << rshift, relative to the list start; [0] = 0, [F] = size.
 
-__global__ void k_split_points(const int32_t* __restrict__ src, int64_t nnz,
-                               const uint2* __restrict__ cls,
-                               const unsigned long long* __restrict__ pre,
-                               const int32_t* __restrict__ L, const uint2* __restrict__ vb,
-                               int rshift, int* __restrict__ split) {
+// From the id-sorted OFF lists themselves: a lane per vertex walks a short
+// list once; the warp takes a long list (> SPLIT_LONG ids) together, one
+// binary search per boundary.  Rows of empty OFF lists stay zero (memset).
+constexpr int SPLIT_LONG = 256;
+__global__ void k_split_points(int64_t n, const int32_t* __restrict__ L,
+                               const uint2* __restrict__ vb, int rshift, int* __restrict__ split) {
+    const int lane = int(lane_id());
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-        if (!(cls[e >> 5].x & (1u << (e & 31)))) continue;
-        const int v = src[e];
-        const int64_t g = rank_off(cls, pre, e);
-        const int64_t b0 = vb[v].x, b1 = vb[v + 1].x;
-        const int k = int(g - b0);
-        const int r = L[g] >> rshift;
-        const int prev = g == b0 ? -1 : (L[g - 1] >> rshift);
-        int* sp = split + int64_t(v) * (F + 1);
-        for (int q = prev + 1; q <= r; ++q) sp[q] = k;
-        if (g == b1 - 1)
-            for (int q = r + 1; q <= F; ++q) sp[q] = k + 1;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < n;
+         base += stride) {
+        const int64_t v = base + lane;
+        int64_t b0 = 0, b1 = 0;
+        if (v < n) {
+            b0 = vb[v].x;
+            b1 = vb[v + 1].x;
+        }
+        const int len = int(b1 - b0);
+        if (len > 0 && len <= SPLIT_LONG) {
+            int* sp = split + v * (F + 1);
+            int q = 0;
+            for (int64_t g = b0; g < b1; ++g) {
+                const int r = L[g] >> rshift;
+                for (; q <= r; ++q) sp[q] = int(g - b0);
+            }
+            for (; q <= F; ++q) sp[q] = len;
+        }
+        unsigned longs = __ballot_sync(0xffffffffu, len > SPLIT_LONG);
+        while (longs) {
+            const int src_lane = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const int64_t lb0 = __shfl_sync(0xffffffffu, b0, src_lane);
+            const int64_t lb1 = __shfl_sync(0xffffffffu, b1, src_lane);
+            const int64_t lv = base + src_lane;
+            for (int q = lane; q <= F; q += 32) {  // first position with id >= q << rshift
+                const int64_t key = int64_t(q) << rshift;
+                int64_t lo = lb0, hi = lb1;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (int64_t(L[mid]) < key) lo = mid + 1; else hi = mid;
+                }
+                split[lv * (F + 1) + q] = int(lo - lb0);
+            }
+        }
     }
 }
 
@@ -1273,9 +1298,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
                (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P);
     TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
                (const uint8_t*)dbk, (const uint2*)vb, L, ucnt, prec);
-    TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, nnz, 256), 256, 0, src, nnz, ccls,
-               (const unsigned long long*)pre, (const int32_t*)L, (const uint2*)vb, rshift,
-               split);
+    TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, n, 256), 256, 0, n, (const int32_t*)L,
+               (const uint2*)vb, rshift, split);
     TCB_LAUNCH(ctx, k_make_items, grid_for(ctx, n, 256), 256, 0, row, (const int64_t*)seg,
                (const int64_t*)(seg + n), ls, n, witems, citems, titems, nw, nc, nt, shard,
                nshards, wt, hc, tiny);
