@@ -37,7 +37,7 @@ extern "C" {
 
 #define TCB_API __attribute__((visibility("default")))
 
-#define TCB_VERSION 3
+#define TCB_VERSION 4
 
 enum {
     TCB_OK = 0,
@@ -191,6 +191,19 @@ TCB_API int tcb_cetc_count(tcb_context* ctx, const int64_t* d_row_offsets,
                            const int32_t* d_cover_v, int64_t k0, int64_t k1,
                            int64_t* counts_out);
 
+/* ---- CETC-DM apex-range count (_kernels.py:759-783
+ *      cetc_count_restricted_k, used by dmsim.py:144-200) ---------------- */
+/* Over cover edges [0, k) of (d_cover_u, d_cover_v), u < v, counting only
+ * apexes w with lo <= w < hi (the ids processor `i` owns in CETC-DM):
+ * counts_out[0] = T partial (apex on another level, or w > v), [1] = c1,
+ * [2] = c2 of those apexes.  Summed over a partition of [0, n) the T parts
+ * give the triangle count. */
+TCB_API int tcb_cetc_count_restricted(tcb_context* ctx, const int64_t* d_row_offsets,
+                                      const int32_t* d_neighbors, const int32_t* d_level,
+                                      int64_t n, const int32_t* d_cover_u,
+                                      const int32_t* d_cover_v, int64_t k, int64_t lo,
+                                      int64_t hi, int64_t* counts_out);
+
 /* ---- fused path (sequential.py:164-168 tc_cetc) ----------------------- */
 /* Device-resident graph in, exact count out.  d_level_out (nullable,
  * int32[n]) receives the levels; d_cover_u/v (nullable, capacity m) the
@@ -201,8 +214,9 @@ TCB_API int tcb_cetc(tcb_context* ctx, const int64_t* d_row_offsets,
                      int32_t* d_cover_u, int32_t* d_cover_v, tcb_result* out);
 
 /* Multi-GPU shard of the fused path: full labeling and
- * selection on this device's replica; intersection for the owners
- * x with x % nshards == shard.  c1/c2 are this shard's partials (sum over
+ * selection on this device's replica; intersection for the work items of
+ * this shard — partner block i of owner x belongs to shard (x + i) %
+ * nshards (dist.py shard_of).  c1/c2 are this shard's partials (sum over
  * shards, e.g. one all-reduce; then T = c1 + c2/3); triangles is -1 when
  * nshards > 1; ncover/components/max_level are global. */
 TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,

@@ -46,6 +46,8 @@ from .parallel import PARALLEL_IDS, ParallelConfig, tc_cetc_sm, tc_par
 from .ops import CetcResult, cetc, cetc_host, cetc_shard
 from . import ops
 from . import dist
+from . import dm
+from .dm import DmSimResult, Partition, Shipment, partition_graph, simulate_cetc_dm
 from . import configs
 
 __version__ = "0.1.0"

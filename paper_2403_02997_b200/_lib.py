@@ -83,6 +83,8 @@ def load_library(path: Path | None = None):
             "tcb_edge_classes": ([vp, vp, vp, vp, i64, i64, vp, vp, vp], i32),
             "tcb_cover_select": ([vp, vp, vp, vp, i64, vp, vp, pi64], i32),
             "tcb_cetc_count": ([vp, vp, vp, vp, i64, vp, vp, i64, i64, pi64], i32),
+            "tcb_cetc_count_restricted": ([vp, vp, vp, vp, i64, vp, vp, i64, i64, i64, pi64],
+                                          i32),
             "tcb_cetc": ([vp, vp, vp, vp, i64, i64, vp, vp, vp,
                           ctypes.POINTER(TcbResult)], i32),
             "tcb_cetc_shard": ([vp, vp, vp, vp, i64, i64, i32, i32,

@@ -24,7 +24,7 @@ void bfs_parent(Context*, const int64_t*, const int32_t*, int64_t, const int32_t
 void edge_classes(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
                   const int32_t*, const int32_t*, int8_t*);
 void cetc_intersect(Context*, const int64_t*, const int32_t*, const int32_t*, const int32_t*,
-                    const int32_t*, const int64_t*, int64_t, int64_t, int, int, int64_t);
+                    const int32_t*, const int64_t*, int64_t, int64_t, int, int, int64_t, int, int);
 void cetc_intersect_owner(Context*, const int64_t*, const int32_t*, const int32_t*,
                           const int32_t*, int64_t, int64_t, int, int, int);
 void degree_order(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
@@ -318,7 +318,26 @@ TCB_API int tcb_cetc_count(tcb_context* ctx, const int64_t* d_row_offsets,
         (void)n;
         TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
         cetc_intersect(ctx, d_row_offsets, d_neighbors, d_level, d_cover_u, d_cover_v, nullptr,
-                       k0, k1, 0, 1, k1);
+                       k0, k1, 0, 1, k1, 0, 0x7fffffff);
+        fetch_counters(ctx);
+        counts_out[0] = int64_t(ctx->h_counters->t);
+        counts_out[1] = int64_t(ctx->h_counters->c1);
+        counts_out[2] = int64_t(ctx->h_counters->c2);
+    });
+}
+
+TCB_API int tcb_cetc_count_restricted(tcb_context* ctx, const int64_t* d_row_offsets,
+                                      const int32_t* d_neighbors, const int32_t* d_level,
+                                      int64_t n, const int32_t* d_cover_u,
+                                      const int32_t* d_cover_v, int64_t k, int64_t lo, int64_t hi,
+                                      int64_t* counts_out) {
+    return guarded(ctx, [&] {
+        require(k >= 0 && 0 <= lo && lo <= hi && hi <= n, "bad cover count or apex range");
+        require(counts_out != nullptr, "counts_out is null");
+        TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
+        if (k > 0 && hi > lo)
+            cetc_intersect(ctx, d_row_offsets, d_neighbors, d_level, d_cover_u, d_cover_v,
+                           nullptr, 0, k, 0, 1, k, int(lo), int(hi));
         fetch_counters(ctx);
         counts_out[0] = int64_t(ctx->h_counters->t);
         counts_out[1] = int64_t(ctx->h_counters->c1);

@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(INT_BLOCK)
     k_intersect_warp(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                      const int32_t* __restrict__ level, const int32_t* __restrict__ cu,
                      const int32_t* __restrict__ cv, const int64_t* __restrict__ d_total,
-                     int64_t k0, int64_t k1, int shard, int nshards, DevCounters* C) {
+                     int64_t k0, int64_t k1, int shard, int nshards, DevCounters* C, int alo,
+                     int ahi) {
     if (d_total) {  // this shard's contiguous slice of the device-side cover count
         const int64_t total = *d_total;
         k0 = total * shard / nshards;
@@ -62,6 +63,20 @@ __global__ void __launch_bounds__(INT_BLOCK)
         const int lu = level[u];
         int64_t ab = row[u], ae = row[u + 1];
         int64_t bb = row[v], be = row[v + 1];
+        if (alo > 0 || ahi < 0x7fffffff) {
+            // apexes restricted to ids [alo, ahi) (_kernels.py:766-772
+            // cetc_count_restricted_k): both lists cut to that id range
+            auto lb = [&](int64_t b, int64_t e, int key) {
+                while (b < e) {
+                    const int64_t mid = (b + e) >> 1;
+                    if (nb[mid] < key) b = mid + 1; else e = mid;
+                }
+                return b;
+            };
+            const int64_t a0 = lb(ab, ae, alo), a1 = lb(a0, ae, ahi);
+            const int64_t b0 = lb(bb, be, alo), b1 = lb(b0, be, ahi);
+            ab = a0; ae = a1; bb = b0; be = b1;
+        }
         if (ae - ab > be - bb) {
             int64_t t0 = ab, t1 = ae;
             ab = bb; ae = be; bb = t0; be = t1;
@@ -103,12 +118,12 @@ __global__ void __launch_bounds__(INT_BLOCK)
 // equal slices of [0, *d_total).  k_upper bounds the range for grid sizing.
 void cetc_intersect(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* level,
                     const int32_t* cu, const int32_t* cv, const int64_t* d_total, int64_t k0,
-                    int64_t k1, int shard, int nshards, int64_t k_upper) {
+                    int64_t k1, int shard, int nshards, int64_t k_upper, int alo, int ahi) {
     const int64_t work = k_upper - k0;
     if (work <= 0) return;
     int grid = grid_for(ctx, work * 32, INT_BLOCK, 16);
     TCB_LAUNCH(ctx, k_intersect_warp, grid, INT_BLOCK, 0, row, nb, level, cu, cv, d_total, k0, k1,
-               shard, nshards, ctx->d_counters);
+               shard, nshards, ctx->d_counters, alo, ahi);
 }
 
 }  // namespace tcb

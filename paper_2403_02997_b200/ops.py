@@ -19,6 +19,7 @@ __all__ = [
     "bfs_levels",
     "cover_select",
     "cetc_count",
+    "cetc_count_restricted",
     "cetc",
     "cetc_shard",
     "cetc_host",
@@ -106,6 +107,24 @@ def cetc_count(dg: DeviceGraph, level, cover_u, cover_v, k0: int = 0, k1: int | 
                                      _lib.ptr(level), dg.n, _lib.ptr(cover_u),
                                      _lib.ptr(cover_v), k0, k1,
                                      ctypes.cast(out, ctypes.POINTER(ctypes.c_int64))))
+    return int(out[0]), int(out[1]), int(out[2])
+
+
+def cetc_count_restricted(dg: DeviceGraph, level, cover_u, cover_v, lo: int, hi: int):
+    """_kernels.py:759-783 cetc_count_restricted_k: the cover edges'
+    apexes with lo <= w < hi only (one CETC-DM processor's share).  Returns
+    (t, c1, c2) of those apexes; t is the reference's count."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    k = int(cover_u.numel())
+    out = (ctypes.c_int64 * 3)()
+    level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    cu = cover_u.to(device=dg.device, dtype=torch.int32).contiguous()
+    cv = cover_v.to(device=dg.device, dtype=torch.int32).contiguous()
+    ctx.check(ctx.lib.tcb_cetc_count_restricted(
+        ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors), _lib.ptr(level), dg.n,
+        _lib.ptr(cu), _lib.ptr(cv), k, int(lo), int(hi),
+        ctypes.cast(out, ctypes.POINTER(ctypes.c_int64))))
     return int(out[0]), int(out[1]), int(out[2])
 
 
