@@ -182,7 +182,10 @@ __global__ void k_bfs_seed(const int64_t* __restrict__ row, int64_t n, int* pare
 // ---------------------------------------------------------------------------
 // cooperative multi-source BFS
 
-constexpr int BFS_BLOCK = 512;
+#ifndef TCB_BFS_BLOCK
+#define TCB_BFS_BLOCK 512
+#endif
+constexpr int BFS_BLOCK = TCB_BFS_BLOCK;
 constexpr int64_t BFS_ALPHA = 14;  // top-down -> bottom-up when m_f > m_u / ALPHA
 constexpr int64_t BFS_BETA = 24;   // bottom-up -> top-down when n_f < n / BETA
 constexpr int BFS_HEAVY = 256;     // top-down: longer lists are split into chunks
