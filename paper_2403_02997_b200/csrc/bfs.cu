@@ -141,29 +141,39 @@ __global__ void k_cc_rest(const int64_t* __restrict__ row, const int32_t* __rest
     }
 }
 
+// Frontier queue entry: the vertex with its row start and degree, written by
+// whoever discovers it (it has just read them), so expanding it next level
+// starts with the neighbour loads — one dependent memory trip less per level
+// on thin-level graphs.
+struct __align__(16) QEnt {
+    int v, d;
+    long long b;
+};
+
 // Flatten and seed the BFS: level 0 at roots (comp[v]==v), -1 elsewhere;
 // roots with neighbours form the first frontier.
 __global__ void k_bfs_seed(const int64_t* __restrict__ row, int64_t n, int* parent,
-                           int32_t* __restrict__ level, int32_t* __restrict__ queue,
+                           int32_t* __restrict__ level, QEnt* __restrict__ queue,
                            DevCounters* C) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     unsigned long long roots = 0, deg0 = 0, dmax0 = 0;
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
         const int64_t v = base + threadIdx.x;
         bool is_root = false, seed = false;
-        int64_t deg = 0;
+        int64_t deg = 0, rb = 0;
         if (v < n) {
             int r = find_root(int(v), parent);
             parent[v] = r;
             is_root = (r == int(v));
-            deg = row[v + 1] - row[v];
+            rb = row[v];
+            deg = row[v + 1] - rb;
             seed = is_root && deg > 0;
             level[v] = is_root ? 0 : -1;
         }
         roots += is_root;
         unsigned long long slot = warp_append(seed, &C->q_len[0]);
         if (seed) {
-            queue[slot] = int32_t(v);
+            queue[slot] = QEnt{int(v), int(deg), (long long)rb};
             deg0 += deg;
             dmax0 = max(dmax0, (unsigned long long)deg);
         }
@@ -213,7 +223,7 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 template <bool LOWDEG>
 __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
                                           const int32_t* __restrict__ nb, int64_t b, int64_t e,
-                                          int32_t* level, int next_level, int32_t* nxt,
+                                          int32_t* level, int next_level, QEnt* nxt,
                                           unsigned long long* qlen, unsigned long long& my_deg,
                                           unsigned long long& my_dmax) {
     const unsigned lane = lane_id();
@@ -222,19 +232,22 @@ __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
         bool claim = false;
         int w = 0;
         unsigned long long d = 0;
+        int64_t rw = 0;
         if (p < e) {
             w = nb[p];
             if (LOWDEG) {
-                d = row[w + 1] - row[w];
+                rw = row[w];
+                d = row[w + 1] - rw;
                 claim = atomicCAS(&level[w], -1, next_level) == -1;
             } else if (level[w] == -1 && atomicCAS(&level[w], -1, next_level) == -1) {
                 claim = true;
-                d = row[w + 1] - row[w];
+                rw = row[w];
+                d = row[w + 1] - rw;
             }
         }
         unsigned long long slot = warp_append(claim, qlen);
         if (claim) {
-            nxt[slot] = w;
+            nxt[slot] = QEnt{w, int(d), (long long)rw};
             my_deg += d;
             my_dmax = max(my_dmax, d);
         }
@@ -243,7 +256,7 @@ __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
 
 __global__ void __launch_bounds__(BFS_BLOCK)
     k_bfs_coop(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
-               int32_t* level, int32_t* qa, int32_t* qb, int2* chunks, DevCounters* C,
+               int32_t* level, QEnt* qa, QEnt* qb, int2* chunks, DevCounters* C,
                int64_t dir_edges) {
     cg::grid_group grid = cg::this_grid();
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -259,8 +272,8 @@ __global__ void __launch_bounds__(BFS_BLOCK)
     int64_t dmax = int64_t(ld_volatile_u64(&C->deg_max[0]));
     int64_t mu = dir_edges - mf;  // directed entries of not-yet-visited vertices
     bool td = true;
-    int32_t* cur = qa;
-    int32_t* nxt = qb;
+    QEnt* cur = qa;
+    QEnt* nxt = qb;
     int max_level = 0;
 
     while (nf > 0) {
@@ -280,8 +293,9 @@ __global__ void __launch_bounds__(BFS_BLOCK)
             // are cut into chunks that all warps share after a barrier
             const bool heavy = dmax > BFS_HEAVY;
             for (int64_t i = gwarp; i < nf; i += nwarps) {
-                const int u = cur[i];
-                const int64_t b = row[u], e = row[u + 1];
+                const QEnt q = cur[i];
+                const int u = q.v;
+                const int64_t b = q.b, e = q.b + q.d;
                 if (heavy && e - b > BFS_HEAVY) {
                     const int nch = int((e - b + BFS_HEAVY - 1) / BFS_HEAVY);
                     unsigned long long base = 0;
@@ -378,13 +392,16 @@ __global__ void __launch_bounds__(BFS_BLOCK)
                 const int64_t v = base + lane;
                 bool in = v < n && level[v] == L + 1;
                 unsigned long long slot = warp_append(in, qc);
-                if (in) nxt[slot] = int32_t(v);
+                if (in) {
+                    const int64_t rb = row[v];
+                    nxt[slot] = QEnt{int(v), int(row[v + 1] - rb), (long long)rb};
+                }
             }
             grid.sync();
             if (gtid == 0) *qc = 0;  // nobody reads it; next use is >= 1 sync away
         }
         if (td || next_td) {
-            int32_t* t = cur;
+            QEnt* t = cur;
             cur = nxt;
             nxt = t;
         }
@@ -416,8 +433,8 @@ void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32
         TCB_LAUNCH(ctx, k_cc_rest, grid_for(ctx, n, 256), 256, 0, row, nb, n, (const int*)giant,
                    parent);
     }
-    int32_t* qa = ctx->wsT<int32_t>(WS_QUEUE_A, n);
-    int32_t* qb = ctx->wsT<int32_t>(WS_QUEUE_B, n);
+    QEnt* qa = ctx->wsT<QEnt>(WS_QUEUE_A, n);
+    QEnt* qb = ctx->wsT<QEnt>(WS_QUEUE_B, n);
     TCB_LAUNCH(ctx, k_bfs_seed, grid_for(ctx, n, 256), 256, 0, row, n, parent, level, qa, C);
     ctx->record(1);
     if (m > 0) {
