@@ -423,7 +423,16 @@ def main():
                     "formula": "4*W + 24*|S| + 4*(c1+c2), W = sum_S (d(u)+d(v))"},
                 "bfs": {"achieved": b_bfs / t_bfs / 1e9 if t_bfs > 0 else None,
                         "bytes": b_bfs, "t_ms": stages["components"] + stages["bfs"],
-                        "formula": "8(n+1) + 16m + 4n"}}
+                        "formula": "8(n+1) + 16m + 4n (SURVEY.md 8(d), BFS incl. components)",
+                        "frac": (b_bfs / t_bfs / 1e9 / peak) if t_bfs > 0 else None,
+                        "bfs_kernel": {
+                            "achieved": (b_bfs / (stages["bfs"] * 1e-3) / 1e9
+                                         if stages["bfs"] > 0 else None),
+                            "t_ms": stages["bfs"],
+                            "frac": (b_bfs / (stages["bfs"] * 1e-3) / 1e9 / peak
+                                     if stages["bfs"] > 0 else None),
+                            "note": "the level-synchronous BFS alone (k_bfs_seed + k_bfs_coop)"},
+                        "components_ms": stages["components"]}}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
