@@ -129,15 +129,35 @@ __global__ void __launch_bounds__(CC_VOTES) k_cc_vote(int64_t n, const int* pare
     if (t == 0) *giant = int(best & 0xffffffffu);
 }
 
-// remaining neighbours (index >= CC_SAMPLE) of vertices outside the dominant tree
+// remaining neighbours (index >= CC_SAMPLE) of vertices outside the dominant
+// tree; a lane takes a short list, the whole warp a long one (a hub outside
+// the dominant tree must not serialise on one thread)
+constexpr int CC_REST_LONG = 64;
 __global__ void k_cc_rest(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
                           int64_t n, const int* __restrict__ giant_p, int* parent) {
     const int giant = *giant_p;
+    const int lane = int(lane_id());
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-        const int64_t b = row[v] + CC_SAMPLE, e = row[v + 1];
-        if (b >= e || find_root(int(v), parent) == giant) continue;
-        for (int64_t p = b; p < e; ++p) hook(int(v), nb[p], parent);
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < n;
+         base += stride) {
+        const int64_t v = base + lane;
+        int64_t b = 0, e = 0;
+        if (v < n) {
+            b = row[v] + CC_SAMPLE;
+            e = row[v + 1];
+            if (b >= e || find_root(int(v), parent) == giant) b = e = 0;
+        }
+        if (e - b <= CC_REST_LONG)
+            for (int64_t p = b; p < e; ++p) hook(int(v), nb[p], parent);
+        unsigned longs = __ballot_sync(0xffffffffu, e - b > CC_REST_LONG);
+        while (longs) {
+            const int src = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const int64_t lb = __shfl_sync(0xffffffffu, b, src);
+            const int64_t le = __shfl_sync(0xffffffffu, e, src);
+            const int lv = int(base + src);
+            for (int64_t p = lb + lane; p < le; p += 32) hook(lv, nb[p], parent);
+        }
     }
 }
 

@@ -244,3 +244,26 @@ def test_every_intersection_path_rmat16(tuning):
     finally:
         ctx.set_tuning(0, 0)
     assert (r.triangles, r.c1, r.c2) == (gold["T"], gold["c1"], gold["c2"])
+
+
+def test_hub_outside_dominant_component():
+    """A long cycle (the dominant component, found by the sample vote) plus a
+    star whose hub is not its component's minimum: the hub's remaining
+    neighbours take the warp-cooperative hooking path (k_cc_rest), and a
+    triangle fan on the star exercises the non-dominant component's count."""
+    rng = np.random.default_rng(11)
+    n_cyc, leaves = 200_000, 5000
+    cyc = np.stack([np.arange(n_cyc), (np.arange(n_cyc) + 1) % n_cyc], axis=1)
+    hub = n_cyc + leaves  # the star's largest id; its minimum is the first leaf
+    star = np.stack([np.full(leaves, hub), n_cyc + np.arange(leaves)], axis=1)
+    fan = np.stack([n_cyc + np.arange(0, leaves - 1, 2), n_cyc + np.arange(1, leaves, 2)], axis=1)
+    pairs = np.concatenate([cyc, star, fan])
+    pairs = pairs[rng.permutation(len(pairs))]
+    n = hub + 1
+    g = tb.normalize(tb.EdgeList(n=n, edges=pairs))
+    row, nb, eu, ev = oracle.normalize(n, pairs)
+    ref = oracle.run(n, row, nb, eu, ev, threads=2)
+    lab = tb.bfs_label(g)
+    assert np.array_equal(lab.level, ref["level"])
+    assert (lab.components, lab.max_level) == (ref["components"], ref["max_level"])
+    assert tb.tc_cetc(g) == ref["T"] == leaves // 2
