@@ -69,7 +69,7 @@ namespace tcb {
 #define TCB_WT 256
 #endif
 #ifndef TCB_HC
-#define TCB_HC 4096
+#define TCB_HC 6144
 #endif
 #ifndef TCB_CHUNK
 #define TCB_CHUNK 1024
@@ -83,7 +83,10 @@ constexpr int W_WARPS = 8;
 constexpr int PW = TCB_PW;            // partners per warp item
 constexpr int C_THREADS = 512;        // 2 CTAs per SM
 constexpr int HC = TCB_HC;            // staged ids per CTA item
-constexpr int C_SLOTS = 4 * HC;       // load <= 1/4 (64 KB)
+#ifndef TCB_C_SLOTS
+#define TCB_C_SLOTS 16384
+#endif
+constexpr int C_SLOTS = TCB_C_SLOTS;  // cuckoo slots (64 KB): load <= HC / C_SLOTS = 3/8
 constexpr int PC = 2 * C_THREADS;     // partners per CTA item
 constexpr int NSEG = 2 * PC;          // stream slices: partner t -> OFF slice t, UP slice PC + t
 constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per lane)
@@ -176,7 +179,7 @@ struct BucketHash {
 // 2-choice cuckoo set over two half tables: a probe is two LDS.32 and two
 // compares with no loop.  Parallel insertion by atomicExch kick chains; a
 // chain longer than CUCKOO_KICKS reports failure and the caller falls back
-// to the bucket table (load <= 1/4 makes that vanishingly rare).
+// to the bucket table (rare at the CTA tier's load <= 3/8).
 constexpr int CUCKOO_KICKS = 64;
 
 struct CuckooHash {
