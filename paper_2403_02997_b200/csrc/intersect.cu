@@ -780,23 +780,32 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
             if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
         }
         // slices of partners lane and lane + 32: OFF (c0, c1), UP (c2, c3)
-        static_assert(PW <= 64, "two partners per lane");
-        int cnt[4] = {0, 0, 0, 0};
-        uint32_t pos[4] = {0, 0, 0, 0};
+        // slices of partners lane + 32 r: OFF (cnt[r]), UP prefix (cnt[PPL + r])
+        constexpr int PPL = (PW + 31) / 32;  // partners per lane
+        static_assert(PPL * 32 * 2 <= 2 * 2048 && PW % 32 == 0, "slice table layout");
+        int cnt[2 * PPL];
+        uint32_t pos[2 * PPL];
+        int so = 0, su = 0, no_ = 0, nu_ = 0;
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < PPL; ++r) {
+            cnt[r] = cnt[PPL + r] = 0;
+            pos[r] = pos[PPL + r] = 0;
             const int64_t j = item.y + lane + 32 * r;
             if (j < item.z) {
                 const int y = P[j];
                 const uint2 v0 = ls.vb[y];
                 pos[r] = v0.x;
                 cnt[r] = no ? int(ls.vb[y + 1].x - v0.x) : 0;
-                pos[2 + r] = v0.y;  // the prefix of UP(y) that can be in UP(x)
-                cnt[2 + r] = nu ? ls.up_prefix(y, kx) : 0;
+                pos[PPL + r] = v0.y;  // the prefix of UP(y) that can be in UP(x)
+                cnt[PPL + r] = nu ? ls.up_prefix(y, kx) : 0;
             }
+            so += cnt[r];
+            su += cnt[PPL + r];
+            no_ += cnt[r] > 0;
+            nu_ += cnt[PPL + r] > 0;
         }
-        const int64_t ve = int64_t(cnt[0] + cnt[1]) | (int64_t(cnt[2] + cnt[3]) << 32);
-        const int vn = int(cnt[0] > 0) + int(cnt[1] > 0) + ((int(cnt[2] > 0) + int(cnt[3] > 0)) << 16);
+        const int64_t ve = int64_t(so) | (int64_t(su) << 32);
+        const int vn = no_ + (nu_ << 16);
         const int64_t ie = warp_inclusive_scan(ve);
         const int in = warp_inclusive_scan(vn);
         const int64_t te = __shfl_sync(0xffffffffu, ie, 31);
@@ -810,10 +819,10 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
             int e_o = int(ee & 0xFFFFFFFF), e_s = tsup + int(ee >> 32);
             int n_o = en & 0xFFFF, n_s = noff + (en >> 16);
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < 2 * PPL; ++r) {
                 const int c = cnt[r];
                 if (c == 0) continue;
-                const bool isup = r >= 2;
+                const bool isup = r >= PPL;
                 const int e = isup ? e_s : e_o;
                 seg[isup ? n_s++ : n_o++] = make_int2(e, int(pos[r] - uint32_t(e)));
                 if (isup) e_s += c; else e_o += c;
