@@ -92,6 +92,11 @@ TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n);
  * are staged <= cta_stage_max ids (4..4096) per CTA pass.  Results do not
  * depend on them; tests shrink them to drive every code path. */
 TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_stage_max);
+/* Test hook (no reference counterpart): TCB_TEST_FORCE_FALLBACK makes every
+ * CTA-tier pass use the bucket-table fallback that otherwise runs only when
+ * a cuckoo build fails, so the tests reach that path.  0 = normal. */
+#define TCB_TEST_FORCE_FALLBACK 4
+TCB_API int tcb_set_test_flags(tcb_context* ctx, int flags);
 
 /* ---- input synthesis (rmat.py:45-72) ---------------------------------- */
 /* generate_rmat: edge_factor*2^scale pairs into d_pairs[2*total] (u,v

@@ -70,6 +70,7 @@ def load_library(path: Path | None = None):
             "tcb_launch_count": ([vp], i64),
             "tcb_set_timing": ([vp, i32], i32),
             "tcb_set_tuning": ([vp, i32, i32], i32),
+            "tcb_set_test_flags": ([vp, i32], i32),
             "tcb_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), i32], i32),
             "tcb_rmat_generate": ([vp, i32, i64, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, u64, u64, u64, u64, vp, vp], i32),
@@ -157,6 +158,10 @@ class Context:
 
     def set_timing(self, on: bool):
         self.check(self.lib.tcb_set_timing(self.h, int(bool(on))))
+
+    def set_test_flags(self, flags: int = 0):
+        """Test hook: force rarely taken device paths (tcb_set_test_flags)."""
+        self.check(self.lib.tcb_set_test_flags(self.h, int(flags)))
 
     def set_tuning(self, warp_tier_max_degree: int = 0, cta_stage_max: int = 0):
         """Intersection work-split knobs (0 = defaults); results are unchanged."""

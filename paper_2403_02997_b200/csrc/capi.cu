@@ -193,6 +193,13 @@ TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_s
     });
 }
 
+TCB_API int tcb_set_test_flags(tcb_context* ctx, int flags) {
+    return guarded(ctx, [&] {
+        require(flags >= 0, "negative flags");
+        ctx->test_flags = flags;
+    });
+}
+
 TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n) {
     return guarded(ctx, [&] {
         require(ms_out != nullptr, "ms_out is null");

@@ -94,6 +94,7 @@ struct Context {
     int bfs_coop_blocks = 0;
     int tune_wt = 0;   // intersection: warp-tier max owner degree (0 = default)
     int tune_hc = 0;   // intersection: ids staged per CTA pass (0 = default)
+    int test_flags = 0;  // tcb_set_test_flags: force rarely taken paths (tests only)
     bool isect_events = false;  // events 5/6 bracket the CTA-tier kernel
 
     void* ws(Slot s, size_t bytes) {

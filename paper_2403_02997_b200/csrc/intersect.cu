@@ -1117,6 +1117,7 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         if (!staged(vinfo, w, x, dx, fwd)) continue;
                         if (!ch.insert(w)) s_fail = 1;
                     }
+                if ((dbg & TCB_TEST_FORCE_FALLBACK) && threadIdx.x == 0) s_fail = 1;
                 // this pass's count from each slice of partners 2t, 2t+1
                 // (slots 0, 1: OFF; 2, 3: UP), then the stream table
                 const bool last = cb + len >= plen;
@@ -1335,7 +1336,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     ctx->record(5);
     ctx->record(7);  // no separate hub kernel in this design: hub stage = 0
     TCB_LAUNCH(ctx, k_isect_cta, K.cta_blocks, C_THREADS, csm, (const longlong4*)citems,
-               (const unsigned long long*)nc, ls, (const int32_t*)P, fc, C, hc, debug_flags(),
+               (const unsigned long long*)nc, ls, (const int32_t*)P, fc, C, hc,
+               debug_flags() | ctx->test_flags,
                (const int2*)vinfo, fwd);
     ctx->record(6);
     TCB_LAUNCH(ctx, k_isect_warp, K.warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,

@@ -267,3 +267,23 @@ def test_hub_outside_dominant_component():
     assert np.array_equal(lab.level, ref["level"])
     assert (lab.components, lab.max_level) == (ref["components"], ref["max_level"])
     assert tb.tc_cetc(g) == ref["T"] == leaves // 2
+
+
+@pytest.mark.parametrize("tuning", [(16, 64), (0, 0)])
+def test_cta_bucket_fallback_path(tuning):
+    """The bucket-table fallback of the CTA tier (taken when a cuckoo build
+    fails) forced on every pass: counts must not change."""
+    ctx = tb._lib.context()
+    ctx.set_tuning(*tuning)
+    ctx.set_test_flags(4)  # TCB_TEST_FORCE_FALLBACK
+    try:
+        for case in SMALL_CASES:
+            g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+            r = tb.cetc(tb.device_graph(g))
+            assert (r.triangles, r.c1, r.c2) == (case.T, case.c1, case.c2), case.name
+        gold = config_goldens()["rmat16"]
+        r = tb.cetc(C.build_device_graph("rmat16"))
+        assert (r.triangles, r.c1, r.c2) == (gold["T"], gold["c1"], gold["c2"])
+    finally:
+        ctx.set_test_flags(0)
+        ctx.set_tuning(0, 0)
