@@ -48,6 +48,9 @@ from . import ops
 from . import dist
 from . import dm
 from .dm import DmSimResult, Partition, Shipment, partition_graph, simulate_cetc_dm
+from .dm import (CommReport, ScalingFit, comm_report, comm_volume_breakdown, comm_volume_cetc_dm,
+                 comm_volume_previous, fit_scaling, format_volume, projected_comm_volume,
+                 reports_to_csv, wedge_count)
 from . import configs
 
 __version__ = "0.1.0"

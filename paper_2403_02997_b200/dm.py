@@ -22,11 +22,24 @@ to the triangle count (every apex lies in exactly one range).
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
 
 __all__ = [
+    "CommReport",
+    "ScalingFit",
+    "ceil_log2",
+    "format_volume",
+    "wedge_count",
+    "comm_volume_previous",
+    "comm_volume_cetc_dm",
+    "comm_volume_breakdown",
+    "projected_comm_volume",
+    "fit_scaling",
+    "comm_report",
+    "reports_to_csv",
     "Partition",
     "Shipment",
     "DmSimResult",
@@ -211,3 +224,148 @@ def reduce_tally(t: int, group=None, device=None) -> int:
     buf = torch.tensor([int(t)], dtype=torch.int64, device=device)
     dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return int(buf.item())
+
+
+# ---------------------------------------------------------------------------
+# The communication-volume model (dmsim.py:203-336). Pure host arithmetic over
+# graph statistics; the labeling it prices (levels, |S|, depth) and the
+# triangle count come from the GPU path.
+
+_BYTE_SCALES = tuple((u, 1 << (10 * k)) for k, u in
+                     ((6, "EB"), (5, "PB"), (4, "TB"), (3, "GB"), (2, "MB"), (1, "KB")))
+
+
+def ceil_log2(x: int) -> int:
+    """dmsim.py:61-65: the least b with 2**b >= x (x >= 1)."""
+    x = int(x)
+    if x < 1:
+        raise ValueError("ceil_log2 requires x >= 1")
+    return (x - 1).bit_length()
+
+
+def format_volume(bits: float) -> str:
+    """dmsim.py:68-73: a bit count rendered in binary byte units, 3 sig. digits."""
+    nbytes = bits / 8
+    unit, scale = next(((u, sc) for u, sc in _BYTE_SCALES if nbytes >= sc), ("B", 1))
+    return f"{nbytes / scale:.3g}{unit}"
+
+
+def wedge_count(g) -> int:
+    """graph.py:216-219: 2-paths, the sum over vertices of C(d(v), 2)."""
+    deg = np.diff(np.asarray(g.row_offsets, dtype=np.int64))
+    return int(np.sum(deg * (deg - 1)) // 2)
+
+
+def comm_volume_previous(g, p: int = 1) -> int:
+    """dmsim.py:203-212: the wedge-query baseline, 2 ids per wedge; p is
+    accepted for symmetry and does not enter."""
+    return 0 if g.n == 0 else 2 * ceil_log2(g.n) * wedge_count(g)
+
+
+def comm_volume_breakdown(g, lab, p: int) -> tuple[int, int, int]:
+    """dmsim.py:225-238: bits for (BFS construction, cover-edge exchange,
+    final reduction) in exact integers: m(log D + 3 log n), |S| p log n,
+    (p - 1) log n with log = ceil_log2 of max(., 1)."""
+    ln = ceil_log2(max(g.n, 1))
+    ld = ceil_log2(max(lab.max_level, 1))
+    return (g.m * (ld + 3 * ln), lab.horizontal_count * p * ln, (p - 1) * ln)
+
+
+def comm_volume_cetc_dm(g, lab, p: int) -> int:
+    """dmsim.py:215-222: total model bits for distributed cover-edge counting."""
+    if len(lab.level) != g.n:
+        raise ValueError("labeling does not match graph")
+    return 0 if g.n == 0 else sum(comm_volume_breakdown(g, lab, p))
+
+
+def projected_comm_volume(n: int, m: int, k: float, p: int, log_d: int) -> float:
+    """dmsim.py:241-250: the model for a graph too large to build, with a
+    covering-ratio estimate k and a fixed depth width log_d (float bits)."""
+    ln = ceil_log2(n)
+    return m * log_d + m * (k * p + 3) * ln + (p - 1) * ln
+
+
+@dataclass(frozen=True)
+class ScalingFit:
+    """dmsim.py:253-263: y = a exp(b x) ("exponential") or y = a x^b ("power")."""
+
+    kind: str
+    a: float
+    b: float
+    r_squared: float
+
+    def predict(self, x: float) -> float:
+        if self.kind == "exponential":
+            return self.a * math.exp(self.b * x)
+        return self.a * x**self.b
+
+
+_FIT_AXES = {"exponential": lambda x: x, "power": np.log}
+
+
+def fit_scaling(xs, ys, kind: str = "exponential") -> ScalingFit:
+    """dmsim.py:266-290: degree-1 least squares of ln y against x (or ln x);
+    r^2 computed in log space, 1.0 for an exact constant fit."""
+    if kind not in _FIT_AXES:
+        raise ValueError(f"unknown fit kind {kind!r}")
+    x = np.asarray(xs, dtype=np.float64)
+    y = np.asarray(ys, dtype=np.float64)
+    if len(x) != len(y) or len(x) < 3:
+        raise ValueError("need at least 3 (x, y) points")
+    if (y <= 0).any():
+        raise ValueError("y values must be positive for a log-space fit")
+    if kind == "power" and (x <= 0).any():
+        raise ValueError("x values must be positive for a power-law fit")
+    t, ly = _FIT_AXES[kind](x), np.log(y)
+    slope, icpt = np.polyfit(t, ly, 1)
+    ss_res = float(((ly - (icpt + slope * t)) ** 2).sum())
+    ss_tot = float(((ly - ly.mean()) ** 2).sum())
+    r2 = (1.0 - ss_res / ss_tot) if ss_tot != 0.0 else float(ss_res < 1e-12)
+    return ScalingFit(kind, float(np.exp(icpt)), float(slope), r2)
+
+
+@dataclass(frozen=True)
+class CommReport:
+    """dmsim.py:293-305: one baseline-vs-cover-edge comparison row."""
+
+    graph: str
+    n: int
+    m: int
+    triangles: int
+    wedges: int
+    k: float
+    p: int
+    bits_previous: int
+    bits_cetc_dm: int
+    reduction: float
+    log_n: int
+    log_d: int
+
+
+def comm_report(g, p: int, name: str = "") -> CommReport:
+    """dmsim.py:308-326; labeling and triangle count computed on the GPU
+    (one bfs_label plus the cover-edge count)."""
+    from .bfs import bfs_label
+    from .sequential import tc_cetc
+    lab = bfs_label(g)
+    tri = tc_cetc(g)
+    before = comm_volume_previous(g, p)
+    after = comm_volume_cetc_dm(g, lab, p)
+    return CommReport(
+        graph=name, n=g.n, m=g.m, triangles=tri, wedges=wedge_count(g),
+        k=(lab.horizontal_count / g.m) if g.m else 0.0, p=p,
+        bits_previous=before, bits_cetc_dm=after,
+        reduction=(before / after) if after else float("inf"),
+        log_n=ceil_log2(max(g.n, 1)), log_d=ceil_log2(max(lab.max_level, 1)))
+
+
+_CSV_HEADER = "graph,n,m,triangles,wedges,c,p,bits_previous,bits_cetc_dm,reduction"
+
+
+def reports_to_csv(reports) -> str:
+    """dmsim.py:329-336: CSV rows, covering ratio to 6 places, reduction to 4."""
+    rows = [_CSV_HEADER]
+    rows += [",".join((r.graph, str(r.n), str(r.m), str(r.triangles), str(r.wedges),
+                       f"{r.k:.6f}", str(r.p), str(r.bits_previous), str(r.bits_cetc_dm),
+                       f"{r.reduction:.4f}")) for r in reports]
+    return "\n".join(rows) + "\n"
