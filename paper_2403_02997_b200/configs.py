@@ -12,6 +12,9 @@ with the shapes BASELINE.json names:
 * ``lattice2048`` — 2048x2048 grid, 4-neighbour + down-right diagonal,
                  row-major ids; T = 2*2047^2 in closed form.
 * ``rmat22`` / ``rmat24`` — as rmat16 at scale 22 / 24.
+* ``rmat25`` / ``rmat26`` — capacity cases beyond BASELINE.json (scale 26:
+                 2m ≈ 2.1e9 adjacency entries, the int32-id / 32-bit list
+                 offset ceiling); checked against the GPU forward count.
 
 RMAT and ER pairs are produced on the device (the PCG64 stream numpy's
 default_rng uses, reproduced bit-exactly: tcb_rmat_generate,
@@ -59,6 +62,10 @@ CONFIGS = {
     "rmat22": Config("rmat22", "rmat", 1 << 22, scale=22, seed=RMAT_SEED,
                      perm_seed=PERM_SEED),
     "rmat24": Config("rmat24", "rmat", 1 << 24, scale=24, seed=RMAT_SEED,
+                     perm_seed=PERM_SEED),
+    "rmat25": Config("rmat25", "rmat", 1 << 25, scale=25, seed=RMAT_SEED,
+                     perm_seed=PERM_SEED),
+    "rmat26": Config("rmat26", "rmat", 1 << 26, scale=26, seed=RMAT_SEED,
                      perm_seed=PERM_SEED),
 }
 

@@ -287,3 +287,18 @@ def test_cta_bucket_fallback_path(tuning):
     finally:
         ctx.set_test_flags(0)
         ctx.set_tuning(0, 0)
+
+
+@pytest.mark.slow
+def test_capacity_rmat25_matches_forward():
+    """Beyond BASELINE.json's sizes (2m ≈ 1.05e9 entries): the cover-edge
+    count equals the independent GPU forward count, c2 is a multiple of 3 and
+    the level rule splits T = c1 + c2/3 (size-independent properties)."""
+    import torch
+    dg = C.build_device_graph("rmat25")
+    r = tb.cetc(dg)
+    assert dg.m == 523_604_945
+    assert r.c2 % 3 == 0 and r.triangles == r.c1 + r.c2 // 3
+    assert r.triangles == tb.ops.forward_count(dg) == 22_534_446_128
+    del dg
+    torch.cuda.empty_cache()
