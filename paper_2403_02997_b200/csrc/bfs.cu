@@ -434,6 +434,31 @@ __global__ void __launch_bounds__(BFS_BLOCK)
 
 // ---------------------------------------------------------------------------
 
+__global__ void k_cc_iota(int64_t n, int* __restrict__ parent) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+        parent[v] = int(v);
+}
+
+// Streaming components for the host-buffer entries: every vertex its own
+// tree, then each neighbour chunk, once resident, hooks its entries (u, v)
+// with u < v — one hook per undirected edge over all chunks, the full
+// union-find, hidden under the rest of the transfer.  Roots are min ids
+// whatever the hook order, so bfs_levels (which then skips its Afforest
+// phases) labels exactly as from the sampled path.
+void cc_stream_begin(Context* ctx, int64_t n) {
+    int* parent = ctx->wsT<int>(WS_COMP, n);
+    TCB_LAUNCH(ctx, k_cc_iota, grid_for(ctx, n, 256), 256, 0, n, parent);
+    ctx->cc_ready = true;
+}
+
+void cc_stream_hook(Context* ctx, const int32_t* src, const int32_t* nb, int64_t e0, int64_t e1) {
+    if (e1 <= e0) return;
+    int* parent = static_cast<int*>(ctx->slot_ptr[WS_COMP]);
+    TCB_LAUNCH(ctx, k_cc_hook, grid_for(ctx, e1 - e0, 256), 256, 0, src + e0, nb + e0, e1 - e0,
+               parent);
+}
+
 void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
                 int64_t n, int64_t m, int32_t* level, bool reset_counters) {
     require(n < (int64_t(1) << 31), "vertex ids must fit int32");
@@ -442,8 +467,10 @@ void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32
     if (n == 0) return;
     int* parent = ctx->wsT<int>(WS_COMP, n);
     ctx->record(0);
-    TCB_LAUNCH(ctx, k_cc_init, grid_for(ctx, n, 256), 256, 0, row, nb, n, parent);
-    if (m > 0) {
+    const bool hooked = ctx->cc_ready;  // cc_stream_* already built the full union-find
+    ctx->cc_ready = false;
+    if (!hooked) TCB_LAUNCH(ctx, k_cc_init, grid_for(ctx, n, 256), 256, 0, row, nb, n, parent);
+    if (m > 0 && !hooked) {
         (void)src;
         int* giant = reinterpret_cast<int*>(&C->scratch[11]);
         for (int r = 0; r < CC_SAMPLE; ++r)

@@ -17,6 +17,8 @@ void csr_rows(Context*, const int64_t*, int64_t, int32_t*);
 void csr_edges(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*, int32_t*);
 void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
                 int32_t*, bool);
+void cc_stream_begin(Context*, int64_t);
+void cc_stream_hook(Context*, const int32_t*, const int32_t*, int64_t, int64_t);
 void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
                   int32_t*, int64_t*);
 void bfs_parent(Context*, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t,
@@ -42,6 +44,7 @@ namespace {
 template <typename F>
 int guarded(tcb_context* ctx, F&& f) {
     if (!ctx) return TCB_ERR_INVALID;
+    ctx->cc_ready = false;  // a streamed union-find never outlives its call
     try {
         TCB_CUDA(cudaSetDevice(ctx->device));
         f();
@@ -167,6 +170,9 @@ TCB_API int tcb_context_destroy(tcb_context* ctx) {
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->chunk_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
     return TCB_OK;
 }
@@ -241,15 +247,18 @@ TCB_API int tcb_csr_build(tcb_context* ctx, const int64_t* d_pairs, int64_t k, i
     return guarded(ctx, [&] {
         require(d_row_offsets && m_out, "null output");
         require(k == 0 || (d_pairs && d_neighbors), "null input");
+        require(k >= 0, "negative size");
+        require_sizes(n);
         csr_build(ctx, d_pairs, k, n, d_row_offsets, d_neighbors, d_src, d_edge_u, d_edge_v,
                   m_out);
+        require_sizes(n, *m_out);  // the deduplicated graph must fit the layout
     });
 }
 
 TCB_API int tcb_csr_rows(tcb_context* ctx, const int64_t* d_row_offsets, int64_t n,
                          int32_t* d_src) {
     return guarded(ctx, [&] {
-        require(n >= 0, "negative size");
+        require_sizes(n);
         csr_rows(ctx, d_row_offsets, n, d_src);
     });
 }
@@ -258,7 +267,8 @@ TCB_API int tcb_csr_edges(tcb_context* ctx, const int64_t* d_row_offsets,
                           const int32_t* d_neighbors, int64_t n, int64_t m, int32_t* d_edge_u,
                           int32_t* d_edge_v) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         csr_edges(ctx, d_row_offsets, d_neighbors, n, m, d_edge_u, d_edge_v);
     });
 }
@@ -267,7 +277,8 @@ TCB_API int tcb_bfs_levels(tcb_context* ctx, const int64_t* d_row_offsets,
                            const int32_t* d_neighbors, const int32_t* d_src, int64_t n, int64_t m,
                            int32_t* d_level, int64_t* components_out, int64_t* max_level_out) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         require(n == 0 || (d_row_offsets && d_level), "null array");
         bfs_levels(ctx, d_row_offsets, d_neighbors, d_src, n, m, d_level, true);
         fetch_counters(ctx);
@@ -280,7 +291,7 @@ TCB_API int tcb_bfs_parent(tcb_context* ctx, const int64_t* d_row_offsets,
                            const int32_t* d_neighbors, int64_t n, const int32_t* d_level,
                            int64_t max_level, int32_t* d_parent_out) {
     return guarded(ctx, [&] {
-        require(n >= 0, "negative size");
+        require_sizes(n);
         require(n == 0 || (d_row_offsets && d_level && d_parent_out), "null array");
         bfs_parent(ctx, d_row_offsets, d_neighbors, n, d_level, max_level, d_parent_out);
         sync(ctx);
@@ -292,7 +303,8 @@ TCB_API int tcb_edge_classes(tcb_context* ctx, const int64_t* d_row_offsets,
                              int64_t m, const int32_t* d_level, const int32_t* d_parent,
                              int8_t* d_class_out) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         require(m == 0 || (d_neighbors && d_src && d_level && d_parent && d_class_out),
                 "null array");
         edge_classes(ctx, d_row_offsets, d_neighbors, d_src, n, m, d_level, d_parent,
@@ -306,6 +318,7 @@ TCB_API int tcb_cover_select(tcb_context* ctx, const int32_t* d_level, const int
                              int32_t* d_cover_v, int64_t* ncover_out) {
     return guarded(ctx, [&] {
         require(m >= 0, "negative size");
+        require_sizes(0, m);
         int64_t* d_n = reinterpret_cast<int64_t*>(&ctx->d_counters->scratch[2]);
         cover_select(ctx, d_level, d_src, d_neighbors, 2 * m, d_cover_u, d_cover_v, d_n);
         int64_t k = 0;
@@ -356,7 +369,8 @@ TCB_API int tcb_cetc(tcb_context* ctx, const int64_t* d_row_offsets, const int32
                      const int32_t* d_src, int64_t n, int64_t m, int32_t* d_level_out,
                      int32_t* d_cover_u, int32_t* d_cover_v, tcb_result* out) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         int32_t* level = d_level_out ? d_level_out : ctx->wsT<int32_t>(WS_LEVEL, n);
         cetc_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, level);
         if (n > 0) collect_stage_times(ctx);
@@ -390,7 +404,8 @@ TCB_API int tcb_forward_count(tcb_context* ctx, const int64_t* d_row_offsets,
                               const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
                               int64_t m, int64_t* triangles_out) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         require(triangles_out != nullptr, "triangles_out is null");
         forward_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, triangles_out);
     });
@@ -400,7 +415,8 @@ TCB_API int tcb_cetc_fe(tcb_context* ctx, const int64_t* d_row_offsets,
                         const int32_t* d_neighbors, const int32_t* d_src, int64_t n, int64_t m,
                         double threshold, tcb_result* out, int32_t* used_forward_out) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
         TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
         bfs_levels(ctx, d_row_offsets, d_neighbors, d_src, n, m, level, false);
@@ -439,7 +455,8 @@ TCB_API int tcb_degree_order(tcb_context* ctx, const int64_t* d_row_offsets,
                              int64_t m, int64_t* d_row_out, int32_t* d_neighbors_out,
                              int32_t* d_src_out) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         require(d_row_out && (m == 0 || (d_neighbors_out && d_src_out)), "null output");
         degree_order(ctx, d_row_offsets, d_neighbors, d_src, n, m, d_row_out, d_neighbors_out,
                      d_src_out);
@@ -451,7 +468,8 @@ TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
                            const int32_t* d_neighbors, const int32_t* d_src, int64_t n, int64_t m,
                            int shard, int nshards, tcb_result* out) {
     return guarded(ctx, [&] {
-        require(n >= 0 && m >= 0, "negative size");
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
         require(nshards >= 1 && shard >= 0 && shard < nshards, "bad shard index");
         int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
         cetc_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, level, shard, nshards);
@@ -466,7 +484,7 @@ TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
 static int host_entry(tcb_context* ctx, const int64_t* h_row_offsets, const int32_t* h_neighbors,
                       int64_t n, int64_t* h_level_out, int shard, int nshards, tcb_result* out) {
     return guarded(ctx, [&] {
-        require(n >= 0, "negative size");
+        require_sizes(n);
         require(nshards >= 1 && shard >= 0 && shard < nshards, "bad shard index");
         require(h_row_offsets != nullptr, "null row offsets");
         const int64_t nnz = h_row_offsets[n];
@@ -476,12 +494,33 @@ static int host_entry(tcb_context* ctx, const int64_t* h_row_offsets, const int3
         int64_t* row = ctx->wsT<int64_t>(WS_ROW, n + 1);
         int32_t* nb = ctx->wsT<int32_t>(WS_NB, nnz);
         int32_t* src = ctx->wsT<int32_t>(WS_EDGE_U, nnz);
+        // The row offsets first, then the neighbour array in chunks on a copy
+        // stream; the entry->row map and the component union-find run on the
+        // compute stream under the transfer, chunk by chunk (bfs.cu).
         TCB_CUDA(cudaMemcpyAsync(row, h_row_offsets, sizeof(int64_t) * (n + 1),
                                  cudaMemcpyHostToDevice, ctx->stream));
-        if (nnz)
-            TCB_CUDA(cudaMemcpyAsync(nb, h_neighbors, sizeof(int32_t) * nnz,
-                                     cudaMemcpyHostToDevice, ctx->stream));
         csr_rows(ctx, row, n, src);
+        if (nnz) {
+            if (!ctx->copy_stream) {
+                TCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+                for (auto& e : ctx->chunk_ev)
+                    TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            const int K = Context::kCopyChunks;
+            // the copy may not overtake earlier work on the compute stream
+            TCB_CUDA(cudaEventRecord(ctx->chunk_ev[K], ctx->stream));
+            TCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[K], 0));
+            cc_stream_begin(ctx, n);
+            const int nch = nnz >= (int64_t(1) << 23) ? K : 1;
+            for (int c = 0; c < nch; ++c) {
+                const int64_t e0 = nnz * c / nch, e1 = nnz * (c + 1) / nch;
+                TCB_CUDA(cudaMemcpyAsync(nb + e0, h_neighbors + e0, sizeof(int32_t) * (e1 - e0),
+                                         cudaMemcpyHostToDevice, ctx->copy_stream));
+                TCB_CUDA(cudaEventRecord(ctx->chunk_ev[c], ctx->copy_stream));
+                TCB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[c], 0));
+                cc_stream_hook(ctx, src, nb, e0, e1);
+            }
+        }
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[9], ctx->stream));
         int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
         cetc_device(ctx, row, nb, src, n, m, level, shard, nshards);

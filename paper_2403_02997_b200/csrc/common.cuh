@@ -36,6 +36,16 @@ inline void require(bool ok, const std::string& msg) {
     if (!ok) throw Error(TCB_ERR_INVALID, msg);
 }
 
+// Size ceiling of the device layout: vertex ids are int32 (the reference's
+// neighbors dtype) and per-list offsets / stream cursors are 32-bit, so n and
+// the 2m adjacency entries must stay below 2^31 (RMAT-26, 2m = 2.10e9, is the
+// largest measured case).  m < 0 skips the edge check.
+inline void require_sizes(int64_t n, int64_t m = -1) {
+    require(n >= 0, "negative size");
+    require(n < (int64_t(1) << 31), "n exceeds the int32 vertex-id range");
+    if (m >= 0) require(2 * m < (int64_t(1) << 31), "2m adjacency entries exceed 2^31 - 1");
+}
+
 // ---------------------------------------------------------------------------
 // workspace slots owned by a context (grown on demand, reused across calls)
 
@@ -96,6 +106,12 @@ struct Context {
     int tune_hc = 0;   // intersection: ids staged per CTA pass (0 = default)
     int test_flags = 0;  // tcb_set_test_flags: force rarely taken paths (tests only)
     bool isect_events = false;  // events 5/6 bracket the CTA-tier kernel
+    // host-buffer entries: neighbour chunks land on copy_stream while the
+    // union-find hooks the ones already resident (bfs.cu cc_stream_*)
+    static constexpr int kCopyChunks = 8;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t chunk_ev[kCopyChunks + 1] = {};
+    bool cc_ready = false;  // components already hooked: bfs_levels skips its CC phases
 
     void* ws(Slot s, size_t bytes) {
         if (bytes == 0) bytes = 16;

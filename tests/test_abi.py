@@ -51,3 +51,16 @@ def test_no_cpu_fallback_without_gpu():
     import paper_2403_02997_b200 as tb
     with pytest.raises(RuntimeError, match="CUDA"):
         tb.normalize(tb.EdgeList(n=3, edges=np.array([[0, 1], [1, 2], [0, 2]])))
+
+
+@pytest.mark.gpu
+def test_size_ceiling_is_rejected():
+    """n >= 2^31 or 2m >= 2^31 fails with TCB_ERR_INVALID before any launch
+    (common.cuh require_sizes), instead of overflowing the 32-bit layout."""
+    from paper_2403_02997_b200 import _lib
+    ctx = _lib.context(0)
+    lib = ctx.lib
+    assert lib.tcb_bfs_levels(ctx.h, None, None, None, 1 << 31, 0, None, None, None) == 1
+    assert lib.tcb_bfs_levels(ctx.h, None, None, None, 16, 1 << 30, None, None, None) == 1
+    assert lib.tcb_cover_select(ctx.h, None, None, None, 1 << 30, None, None, None) == 1
+    assert b"2^31" in lib.tcb_last_error(ctx.h)
