@@ -302,3 +302,45 @@ def test_capacity_rmat25_matches_forward():
     assert r.triangles == tb.ops.forward_count(dg) == 22_534_446_128
     del dg
     torch.cuda.empty_cache()
+
+
+def test_host_entry_chunked_copy_rmat22():
+    """tcb_cetc_host on a graph large enough for the chunked neighbour copy
+    with the union-find hooked under it (2m >= 2^23 entries, 8 chunks):
+    identical counts, components and levels to the device-resident path."""
+    import torch
+    dg = C.build_device_graph("rmat22")
+    dev = tb.cetc(dg, keep_level=True)
+    row = dg.row_offsets.cpu().numpy()
+    nb = dg.neighbors.cpu().numpy()
+    assert len(nb) >= 1 << 23
+    host = tb.ops.cetc_host(row, nb, dg.n, want_level=True)
+    assert (host["triangles"], host["c1"], host["c2"], host["ncover"], host["components"],
+            host["max_level"]) == (dev.triangles, dev.c1, dev.c2, dev.ncover, dev.components,
+                                   dev.max_level)
+    assert np.array_equal(host["level"], dev.level.cpu().numpy().astype(np.int64))
+    del dg, dev
+    torch.cuda.empty_cache()
+
+
+def test_concurrent_calls_from_threads():
+    """The reference kernels are nogil and safe for concurrent calls
+    (_kernels.py:1-8); here every Python thread gets its own library context
+    (workspace + copy stream), so concurrent tc_cetc / bfs_label / host-entry
+    calls on shared Graphs give the single-threaded answers."""
+    from concurrent.futures import ThreadPoolExecutor
+    cases = SMALL_CASES[:12]
+    graphs = [tb.normalize(tb.EdgeList(n=c.n, edges=c.pairs)) for c in cases]
+
+    def work(i):
+        c, g = cases[i % len(cases)], graphs[i % len(cases)]
+        lab = tb.bfs_label(g)
+        h = tb.ops.cetc_host(c.row, c.nb, c.n) if c.n else {"triangles": 0}
+        return tb.tc_cetc(g), np.asarray(lab.level).tolist(), h["triangles"]
+
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        out = list(ex.map(work, range(4 * len(cases))))
+    for i, (t, level, th) in enumerate(out):
+        c = cases[i % len(cases)]
+        assert t == th == c.T, c.name
+        assert level == c.level.tolist(), c.name
