@@ -19,6 +19,9 @@ to the triangle count (every apex lies in exactly one range).
   union), each rank counts its apex range on its GPU, one all-reduce sums
   the tallies.  With NCCL the exchange runs over NVLink; the CPU tests run
   the same host logic over gloo.
+* The communication-volume model (dmsim.py:203-336): `comm_volume_*`,
+  `projected_comm_volume`, `fit_scaling`, `comm_report`, `reports_to_csv`,
+  `format_volume` — host arithmetic over the GPU labeling and count.
 """
 from __future__ import annotations
 
