@@ -306,14 +306,14 @@ def test_capacity_rmat25_matches_forward():
 
 def test_host_entry_chunked_copy_rmat22():
     """tcb_cetc_host on a graph large enough for the chunked neighbour copy
-    with the union-find hooked under it (2m >= 2^23 entries, 8 chunks):
+    with the union-find hooked under it (2m >= 2^26 entries, 8 chunks):
     identical counts, components and levels to the device-resident path."""
     import torch
     dg = C.build_device_graph("rmat22")
     dev = tb.cetc(dg, keep_level=True)
     row = dg.row_offsets.cpu().numpy()
     nb = dg.neighbors.cpu().numpy()
-    assert len(nb) >= 1 << 23
+    assert len(nb) >= 1 << 26
     host = tb.ops.cetc_host(row, nb, dg.n, want_level=True)
     assert (host["triangles"], host["c1"], host["c2"], host["ncover"], host["components"],
             host["max_level"]) == (dev.triangles, dev.c1, dev.c2, dev.ncover, dev.components,
