@@ -9,10 +9,19 @@ per-cover-edge intersection -> exact 64-bit count (tcb_cetc).  Graph
 construction is outside the timed region, as in the reference's protocol
 (bench.py:1-9 of the reference).  metric = m / t_step (undirected edges/s).
 
-For N > 1 (torchrun, one rank per GPU, NCCL): every rank holds a replica of
-the CSR, labels it, and intersects its 1/N slice of the cover set; the three
-partial tallies are summed with one all-reduce.  Total work
-is fixed as N grows: "scaling": "strong".
+For N > 1 (one rank per GPU, NCCL): every rank holds a replica of the CSR,
+labels it, and intersects its 1/N slice of the cover set; the partial
+tallies are summed with one all-reduce.  Total work is
+fixed as N grows: "scaling": "strong".  `--gpus N` without torchrun starts the
+N ranks itself (torch.distributed.run on 127.0.0.1); under torchrun the world
+size must equal N.
+
+--impl reference: the reference's CPU path (the oracle's C port of
+bfs_levels_k + cetc_sm_range_k, all host threads) over the SAME workload.
+The timed region is one complete run, measured, not extrapolated: the
+1-core BFS, then CETC-SM over every edge, cut into K contiguous edge ranges
+(step k = range k; the K ranges cover every edge exactly once, and their
+summed tallies must reproduce T).
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 cuda.synchronize, CUDA events on the launching stream, max over ranks.  The
@@ -167,12 +176,50 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; "
+                         f"launch with --nproc-per-node {args.gpus} or drop torchrun")
     return world, rank, local
 
 
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def workload_config(name: str, n: int, m: int, ncover: int, triangles: int) -> dict:
+    """The `config` dict both arms print (identical by construction)."""
+    csr_bytes = 8 * (n + 1) + 8 * m
+    return {"workload": name, "n": int(n), "m": int(m), "ncover": int(ncover),
+            "triangles": int(triangles),
+            "l2": ("inputs larger than L2" if csr_bytes >= 4 * L2_BYTES
+                   else "L2 flushed between steps (GPU arm)")}
+
+
+def cpu_model() -> str:
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU path (the oracle port; see
-    DESIGN.md) on the host cores, same config/metric.  Rank 0 only."""
+    """--impl reference: the reference's CPU path (the oracle's C port,
+    oracle/cetc_oracle.c, of _kernels.py:129-157 and :729-755 under
+    parallel.py:117-137) on the host cores, same config/metric.  Rank 0
+    only.  Measured in full: timed region = 1-core BFS + CETC-SM over all m
+    edges, split into K contiguous edge ranges (one per step)."""
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return
@@ -191,22 +238,66 @@ def run_reference(args):
     row, nb, eu, ev = oracle.normalize(cfg.n, pairs)
     del pairs
     build_s = time.time() - t0
-    per_step = max(5.0, 60.0 / max(1, args.steps + args.warmup))
-    vals = []
-    last = None
-    for i in range(args.warmup + args.steps):
-        last = cpu_sample(cfg.n, row, nb, eu, ev, per_step, threads)
-        if i >= args.warmup:
-            vals.append(last["value"])
-    value = float(np.mean(vals))
-    ms = len(eu) / value * 1e3
+    m = len(eu)
+    K = max(1, args.steps)
+    bounds = [m * k // K for k in range(K + 1)]
+    # warm-up: W short ranges (0.1% of the edges each) — thread pool, pages
+    wlen = max(1, m // 1000)
+    for i in range(args.warmup):
+        k0 = (i * 7919 * wlen) % max(1, m - wlen)
+        oracle.cetc_sm_counts(row, nb, np.zeros(cfg.n, dtype=np.int64),
+                              np.ascontiguousarray(eu[k0:k0 + wlen]),
+                              np.ascontiguousarray(ev[k0:k0 + wlen]), threads=threads)
+    # timed: BFS (1 core, as the reference's bfs_label) + K edge ranges; a
+    # run under 1 s is repeated (up to 20 runs, ~5 s) and the runs averaged
+    eus = [np.ascontiguousarray(eu[bounds[k]:bounds[k + 1]]) for k in range(K)]
+    evs = [np.ascontiguousarray(ev[bounds[k]:bounds[k + 1]]) for k in range(K)]
+
+    def one_run():
+        t0 = time.perf_counter()
+        lev, _, comps, max_level = oracle.bfs_levels(row, nb, cfg.n)
+        tb_ = time.perf_counter() - t0
+        c1 = c2 = 0
+        ts = []
+        for k in range(K):
+            t0 = time.perf_counter()
+            a, b = oracle.cetc_sm_counts(row, nb, lev, eus[k], evs[k], threads=threads)
+            ts.append(time.perf_counter() - t0)
+            c1 += a
+            c2 += b
+        return tb_, ts, lev, comps, max_level, c1, c2
+
+    runs = [one_run()]
+    t_first = runs[0][0] + sum(runs[0][1])
+    R = 1 if t_first >= 1.0 else min(20, max(1, int(5.0 / max(t_first, 1e-6))))
+    for _ in range(R - 1):
+        runs.append(one_run())
+    _, _, level, comps, max_level, c1, c2 = runs[0]
+    assert all(r[5:] == (c1, c2) for r in runs)
+    assert c2 % 3 == 0, "c2 % 3 != 0"  # parallel.py:127-128
+    T = c1 + c2 // 3
+    t_bfs = float(np.mean([r[0] for r in runs]))
+    step_s = [float(np.mean([r[1][k] for r in runs])) for k in range(K)]
+    total = t_bfs + sum(step_s)
+    value = m / total
+    ncover = int(np.count_nonzero(level[eu] == level[ev]))
+    sample = (f"complete run, measured: oracle (C port of the reference) 1-core BFS "
+              f"{t_bfs:.2f} s + CETC-SM on {threads} threads over all {m} edges in {K} "
+              f"contiguous ranges ({sum(step_s):.2f} s); no extrapolation"
+              + (f"; mean of {R} complete runs" if R > 1 else ""))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "n_gpus": args.gpus, "steps": K, "warmup": args.warmup,
+            "ms_per_step": total / K * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": cfg.name, "n": cfg.n, "m": len(eu),
-                       "host_build_s": round(build_s, 1)},
-            "cpu_baseline": dict(last, value=value),
+            "config": workload_config(cfg.name, cfg.n, m, ncover, T),
+            "timed_runs": R, "seconds_full_run": total,
+            "step_note": ("step k = CETC-SM over edge range k of K (BFS charged to the run); "
+                          "ms_per_step = full-run time / K"),
+            "counts": {"c1": c1, "c2": c2, "components": comps, "max_level": max_level},
+            "host_build_s": round(build_s, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "cpu_model": cpu_model(), "sample": sample,
+                             "t_bfs_s": t_bfs, "t_cetc_sm_s": sum(step_s)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -214,6 +305,8 @@ def run_reference(args):
 
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        raise SystemExit(spawn_ranks(args))
     if args.impl == "reference":
         return run_reference(args)
 
@@ -391,6 +484,35 @@ def main():
                     "tcb_cetc_host_shard per rank + one all-reduce: pinned host CSR replicas")}
     del row_h, nb_h
 
+    # e2e, drop-in variant: the reference's own call, tc_cetc(Graph), on a
+    # FRESH Graph over pageable frozen numpy arrays every step (no cached
+    # device copy), so the pageable upload is inside the timed region
+    if world == 1:
+        host_g = dg.to_host()
+        for _ in range(max(1, args.warmup)):
+            assert tb.tc_cetc(tb.Graph(host_g.n, host_g.m, host_g.row_offsets,
+                                       host_g.neighbors, host_g.edge_u,
+                                       host_g.edge_v)) == expect[0]
+        t_dropin = []
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            g_fresh = tb.Graph(host_g.n, host_g.m, host_g.row_offsets, host_g.neighbors,
+                               host_g.edge_u, host_g.edge_v)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            T_fresh = tb.tc_cetc(g_fresh)
+            t_dropin.append(time.perf_counter() - t0)
+            assert T_fresh == expect[0]
+            del g_fresh
+        td = float(np.mean(t_dropin))
+        e2e["dropin"] = {"value": dg.m / td, "unit": UNIT, "ms_per_step": td * 1e3,
+                         "h2d_bytes_per_step": 8 * (dg.n + 1) + 4 * 2 * dg.m,
+                         "d2h_bytes_per_step": 48,
+                         "path": "tc_cetc(Graph) on a fresh Graph of pageable frozen numpy "
+                                 "arrays (sequential.py:164-168 call shape)"}
+        del host_g
+
     peak, peak_kind = hbm_peak()
     # roofline of the dominant kernel, k_isect_cta (the CTA tier of the
     # intersection), timed alone with CUDA events on its launch stream
@@ -438,12 +560,10 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic (seeded generator, see DESIGN.md)",
-            "config": {"workload": cfg.name, "n": dg.n, "m": dg.m, "ncover": ncover,
-                       "triangles": expect[0], "W": W, "W_min": W_min,
-                       "parallelism": f"replicated CSR, cover set sharded x{world}",
-                       "l2": ("inputs larger than L2" if flush is None
-                              else "L2 flushed between steps"),
-                       "graph_build_s": round(build_s, 3)},
+            "config": workload_config(cfg.name, dg.n, dg.m, ncover, expect[0]),
+            "parallelism": f"replicated CSR, cover set sharded x{world}",
+            "work": {"W": W, "W_min": W_min, "c1": expect[1], "c2": expect[2],
+                     "graph_build_s": round(build_s, 3)},
             "stages_ms": stages, "clocks": clocks, "gpu_launches": launches,
             "e2e": e2e, "roofline": roofline}
 

@@ -493,8 +493,11 @@ static int host_entry(tcb_context* ctx, const int64_t* h_row_offsets, const int3
         require(nshards >= 1 && shard >= 0 && shard < nshards, "bad shard index");
         require(h_row_offsets != nullptr, "null row offsets");
         const int64_t nnz = h_row_offsets[n];
+        require(h_row_offsets[0] == 0 && nnz >= 0, "row offsets must start at 0 and end >= 0");
         require(nnz % 2 == 0, "CSR is not symmetric (odd entry count)");
         const int64_t m = nnz / 2;
+        require_sizes(n, m);
+        require(nnz == 0 || h_neighbors != nullptr, "null neighbour array");
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[8], ctx->stream));
         int64_t* row = ctx->wsT<int64_t>(WS_ROW, n + 1);
         int32_t* nb = ctx->wsT<int32_t>(WS_NB, nnz);

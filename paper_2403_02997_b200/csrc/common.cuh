@@ -101,7 +101,11 @@ struct Context {
     bool timing = false;
     cudaEvent_t ev[16] = {};
     float stage_ms[TCB_NSTAGES] = {};
+    // occupancy-derived grid sizes, computed on first use (per context, so
+    // per thread and per device: no shared mutable state across contexts)
     int bfs_coop_blocks = 0;
+    int isect_warp_blocks = 0, isect_cta_blocks = 0;
+    int parent_blocks_per_sm = 0;
     int tune_wt = 0;   // intersection: warp-tier max owner degree (0 = default)
     int tune_hc = 0;   // intersection: ids staged per CTA pass (0 = default)
     int test_flags = 0;  // tcb_set_test_flags: force rarely taken paths (tests only)

@@ -1225,11 +1225,6 @@ static int debug_flags() {
 #endif
 }
 
-struct IsectKernels {
-    int warp_blocks = 0, cta_blocks = 0;
-};
-static IsectKernels g_k[16];
-
 void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
                           const int32_t* level, int64_t n, int64_t m, int shard, int nshards,
                           int fwd) {
@@ -1317,11 +1312,10 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
                (const int64_t*)(seg + n), ls, n, witems, citems, titems, nw, nc, nt, shard,
                nshards, wt, hc, tiny);
 
-    IsectKernels& K = g_k[ctx->device & 15];
     const size_t wsm = size_t(W_WARPS) * (W_SLOTS * sizeof(uint32_t) + (W_SEG + 1) * sizeof(int2));
     const size_t csm = size_t(C_SLOTS) * sizeof(uint32_t) + size_t(NSEG + 1) * sizeof(int2) +
                        size_t(2 * NSEG) * sizeof(int);
-    if (K.warp_blocks == 0) {
+    if (ctx->isect_warp_blocks == 0) {
         TCB_CUDA(cudaFuncSetAttribute(k_isect_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(wsm)));
         TCB_CUDA(cudaFuncSetAttribute(k_isect_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1330,17 +1324,17 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_isect_warp, W_WARPS * 32, wsm));
         TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_isect_cta, C_THREADS, csm));
         require(a > 0 && b > 0, "intersection kernels do not fit on an SM");
-        K.warp_blocks = a * ctx->num_sms;
-        K.cta_blocks = b * ctx->num_sms;
+        ctx->isect_cta_blocks = b * ctx->num_sms;
+        ctx->isect_warp_blocks = a * ctx->num_sms;
     }
     ctx->record(5);
     ctx->record(7);  // no separate hub kernel in this design: hub stage = 0
-    TCB_LAUNCH(ctx, k_isect_cta, K.cta_blocks, C_THREADS, csm, (const longlong4*)citems,
+    TCB_LAUNCH(ctx, k_isect_cta, ctx->isect_cta_blocks, C_THREADS, csm, (const longlong4*)citems,
                (const unsigned long long*)nc, ls, (const int32_t*)P, fc, C, hc,
                debug_flags() | ctx->test_flags,
                (const int2*)vinfo, fwd);
     ctx->record(6);
-    TCB_LAUNCH(ctx, k_isect_warp, K.warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
+    TCB_LAUNCH(ctx, k_isect_warp, ctx->isect_warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
                (const unsigned long long*)nw, ls, (const int32_t*)P, fw, C, (const int2*)vinfo,
                fwd);
     TCB_LAUNCH(ctx, k_isect_tiny, ctx->num_sms * 8, 256, 0, (const longlong4*)titems,

@@ -200,8 +200,7 @@ void bfs_parent(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n,
                              ctx->stream));
     TCB_LAUNCH(ctx, k_level_scatter, grid_for(ctx, n, 256), 256, 0, level, n, cursor, list);
 
-    static int blocks_per_sm[16] = {};
-    int& per_sm = blocks_per_sm[ctx->device & 15];
+    int& per_sm = ctx->parent_blocks_per_sm;
     if (per_sm == 0) {
         TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_parent_coop, PAR_BLOCK, 0));
         require(per_sm > 0, "parent kernel cannot be co-resident");

@@ -67,6 +67,14 @@ class Partition:
     def vertex_range(self, i: int) -> tuple[int, int]:
         return int(self.bounds[i]), int(self.bounds[i + 1])
 
+    def local_adjacency(self, g, i: int) -> tuple[np.ndarray, np.ndarray]:
+        """dmsim.py:88-93: the CSR slice of processor i's owned vertices,
+        offsets rebased to 0."""
+        lo, hi = self.vertex_range(i)
+        row = np.asarray(g.row_offsets)
+        start = row[lo]
+        return row[lo:hi + 1] - start, np.asarray(g.neighbors)[start:row[hi]]
+
 
 def partition_bounds(degrees: np.ndarray, p: int) -> np.ndarray:
     """dmsim.py:96-109: p contiguous ranges of about 2m/p endpoints each."""
@@ -138,10 +146,12 @@ def owned_cover(cover_u, bounds):
     return np.searchsorted(bounds, cover_u, side="right") - 1
 
 
-def simulate_cetc_dm(g, p: int) -> DmSimResult:
+def simulate_cetc_dm(g, p: int, workers: int = 1) -> DmSimResult:
     """dmsim.py:144-200 simulate_cetc_dm with every processor's counting on
     the GPU (tcb_cetc_count_restricted): count, per-processor local edge
-    counts and the XOR shipment log."""
+    counts and the XOR shipment log.  ``workers`` is accepted for the
+    reference's signature; as there (dmsim.py:149-151) the result and the
+    exchange log do not depend on it — the GPU is the worker pool."""
     from . import ops
     from .graph import device_graph
     schedule = xor_schedule(p)

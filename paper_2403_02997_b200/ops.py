@@ -99,13 +99,20 @@ def cetc_count(dg: DeviceGraph, level, cover_u, cover_v, k0: int = 0, k1: int | 
     Returns (t, c1, c2); over the full set t == c1 + c2 // 3."""
     import torch
     ctx = _lib.context(dg.device.index)
+    k = int(cover_u.numel())
+    if int(cover_v.numel()) != k:
+        raise ValueError("cover_u and cover_v differ in length")
     if k1 is None:
-        k1 = int(cover_u.numel())
+        k1 = k
+    if not 0 <= k0 <= k1 <= k:
+        raise ValueError(f"need 0 <= k0 <= k1 <= {k}, got k0={k0}, k1={k1}")
     out = (ctypes.c_int64 * 3)()
     level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    cu = cover_u.to(device=dg.device, dtype=torch.int32).contiguous()
+    cv = cover_v.to(device=dg.device, dtype=torch.int32).contiguous()
     ctx.check(ctx.lib.tcb_cetc_count(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
-                                     _lib.ptr(level), dg.n, _lib.ptr(cover_u),
-                                     _lib.ptr(cover_v), k0, k1,
+                                     _lib.ptr(level), dg.n, _lib.ptr(cu),
+                                     _lib.ptr(cv), k0, k1,
                                      ctypes.cast(out, ctypes.POINTER(ctypes.c_int64))))
     return int(out[0]), int(out[1]), int(out[2])
 

@@ -64,3 +64,18 @@ def test_size_ceiling_is_rejected():
     assert lib.tcb_bfs_levels(ctx.h, None, None, None, 16, 1 << 30, None, None, None) == 1
     assert lib.tcb_cover_select(ctx.h, None, None, None, 1 << 30, None, None, None) == 1
     assert b"2^31" in lib.tcb_last_error(ctx.h)
+    # the host-buffer entries check m from the row offsets too
+    import ctypes
+    import numpy as np
+    row = np.array([0, 1 << 31], dtype=np.int64)
+    r = _lib.TcbResult()
+    assert lib.tcb_cetc_host(ctx.h, row.ctypes.data_as(ctypes.c_void_p), None, 1, None,
+                             ctypes.byref(r)) == 1
+    assert lib.tcb_cetc_host_shard(ctx.h, row.ctypes.data_as(ctypes.c_void_p), None, 1, 0, 1,
+                                   ctypes.byref(r)) == 1
+    bad = np.array([0, -2], dtype=np.int64)
+    assert lib.tcb_cetc_host(ctx.h, bad.ctypes.data_as(ctypes.c_void_p), None, 1, None,
+                             ctypes.byref(r)) == 1
+    two = np.array([0, 2], dtype=np.int64)
+    assert lib.tcb_cetc_host(ctx.h, two.ctypes.data_as(ctypes.c_void_p), None, 1, None,
+                             ctypes.byref(r)) == 1  # null neighbours
