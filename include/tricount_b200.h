@@ -87,6 +87,13 @@ TCB_API int64_t tcb_launch_count(tcb_context* ctx);
  * for the last fused call (tcb_cetc / tcb_cetc_shard / tcb_cetc_host). */
 TCB_API int tcb_set_timing(tcb_context* ctx, int enabled);
 TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n);
+/* Diagnostics (no reference counterpart): per-level BFS records of the last
+ * call that ran the BFS, for profiling.  Writes up to cap records of three
+ * int64 each — (mode: 0 top-down / 1 bottom-up, level-step end time in ns
+ * from the BFS start, frontier size after the step) — and returns the
+ * number written (levels past TCB_LEVEL_RECORDS are not recorded). */
+#define TCB_LEVEL_RECORDS 48
+TCB_API int tcb_level_records(tcb_context* ctx, int64_t* out, int cap);
 /* Intersection work-split knobs (0 = built-in default): owners with degree
  * <= warp_tier_max_degree (max 1024) use the per-warp tier; larger owners
  * are staged <= cta_stage_max ids (4..4096) per CTA pass.  Results do not

@@ -72,6 +72,7 @@ def load_library(path: Path | None = None):
             "tcb_set_tuning": ([vp, i32, i32], i32),
             "tcb_set_test_flags": ([vp, i32], i32),
             "tcb_stage_times": ([vp, ctypes.POINTER(ctypes.c_float), i32], i32),
+            "tcb_level_records": ([vp, pi64, i32], i32),
             "tcb_rmat_generate": ([vp, i32, i64, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, u64, u64, u64, u64, vp, vp], i32),
             "tcb_er_generate": ([vp, i64, ctypes.c_double, u64, u64, u64, u64, vp, pi64], i32),
@@ -172,6 +173,17 @@ class Context:
         arr = (ctypes.c_float * len(STAGES))()
         self.check(self.lib.tcb_stage_times(self.h, arr, len(STAGES)))
         return {k: float(arr[i]) for i, k in enumerate(STAGES)}
+
+    def level_records(self) -> list[tuple[str, float, int]]:
+        """Per-level BFS records of the last call (diagnostics):
+        (mode "TD"/"BU", step end in us from the BFS start, next frontier)."""
+        cap = 64
+        arr = (ctypes.c_int64 * (3 * cap))()
+        k = int(self.lib.tcb_level_records(self.h, arr, cap))
+        if k < 0:
+            self.check(-k)
+        return [("BU" if arr[3 * i] else "TD", arr[3 * i + 1] / 1e3, int(arr[3 * i + 2]))
+                for i in range(k)]
 
     def __del__(self):
         try:

@@ -2,23 +2,36 @@
 //
 // The reference roots each component at its lowest unvisited id
 // (_kernels.py:137-142), i.e. at the component's minimum vertex id, and
-// levels are BFS distances from that root.  So the levels equal those of ONE
-// multi-source BFS seeded with every component's min-id vertex at level 0:
+// levels are BFS distances from that root.  So the levels equal those of a
+// multi-source BFS seeded with every component's minimum at level 0.  The
+// minima are found without a union-find over the whole graph:
 //
-//   1. components: union-find over the u<v edges where a larger root is always
-//      hooked under a smaller one (ECL-CC style, lock-free CAS), so each tree's
-//      root is its minimum id; roots give `components` (isolated vertices are
-//      their own roots and sit at level 0).
-//   2. BFS: one cooperative persistent kernel runs every level with a grid-wide
-//      barrier between levels (no host round trip per level — the 2048-level
-//      lattice would otherwise be launch/sync bound).  Direction-optimising:
-//      top-down warp-per-frontier-vertex expansion with CAS claims and
-//      warp-aggregated queue appends; bottom-up over unvisited vertices with
-//      early exit when the frontier's incident edges exceed the unexplored
-//      ones / ALPHA; back to top-down when the frontier shrinks below n / BETA.
+//   1. probe: isolated vertices (degree 0) are their own components at level
+//      0; r0 = the lowest NON-isolated id is the minimum of its component
+//      (every smaller id is isolated), so it is a root.
+//   2. BFS from r0 (one cooperative persistent kernel, every level, grid-wide
+//      barriers; direction-optimising).  On the graphs this path targets r0's
+//      component is almost the whole graph.  The kernel ends by listing the
+//      vertices it left unvisited (other components, U).
+//   3. remainder: a lock-free min-root union-find over U only (hooking the
+//      larger root under the smaller, so each tree's root is its component's
+//      minimum), roots seeded at level 0, and a second BFS over U.  Nothing
+//      runs when U is empty.
 //
-// parent/TREE-vs-STRUT classes depend on the reference's FIFO order and are
-// not produced; levels, components and max_level are exact.
+// BFS steps.  Top-down: a warp per frontier vertex (lists longer than
+// BFS_HEAVY are cut into chunks all warps share), int4 neighbour loads, CAS
+// claims, one queue append per warp pass.  Bottom-up (for the wide middle
+// levels): a warp per 32 consecutive vertices; a visited bitmap skips settled
+// words, each unvisited vertex scans its row with int4 loads against the
+// frontier BITMAP (ceil(n/32) words: 2 MB at RMAT-24, L2-resident) and stops
+// at the first hit; the next frontier bitmap word is the warp's ballot (no
+// atomics).  Switch top-down -> bottom-up when the frontier's incident edges
+// exceed the unexplored ones / ALPHA; back when the frontier drops below
+// n / BETA.  Counters are accumulated per thread and added once per warp per
+// level.
+//
+// parent/TREE-vs-STRUT classes (FIFO order) are produced by parent.cu from
+// these levels; levels, components and max_level are exact.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -46,20 +59,6 @@ __device__ __forceinline__ int find_root(int v, int* parent) {
     return curr;
 }
 
-__global__ void k_cc_init(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
-                          int64_t n, int* __restrict__ parent) {
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-        // rows are sorted: the first neighbour is the smallest one
-        int p = int(v);
-        if (row[v + 1] > row[v]) {
-            int w = nb[row[v]];
-            if (w < p) p = w;
-        }
-        parent[v] = p;
-    }
-}
-
 // Union the trees of u and v, hooking the larger root under the smaller one
 // (so every tree's root stays its minimum id).  Lock-free: a failed CAS means
 // the root moved; continue from what it points to now.
@@ -79,93 +78,6 @@ __device__ __forceinline__ void hook(int u, int v, int* parent) {
     }
 }
 
-// one hook per undirected edge: the CSR entries (u, v) with u < v
-__global__ void k_cc_hook(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
-                          int64_t nnz, int* parent) {
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-        const int u = src[e], v = nb[e];
-        if (v > u) hook(u, v, parent);
-    }
-}
-
-// ---- Afforest-style sampling: hook every vertex to its first CC_SAMPLE
-// neighbours, compress, find the dominant root from a fixed sample, and give
-// the full neighbour lists only to vertices outside that tree.  Any edge with
-// one end outside the dominant tree is still hooked from that end, so the
-// result equals the full union-find whatever tree is chosen.
-
-constexpr int CC_SAMPLE = 2;
-constexpr int CC_VOTES = 1024;
-
-// both sampling rounds in one pass (CC_SAMPLE = 2): one read of the row
-// bounds, the second hook right after the first (RMAT-22 components
-// 1.15 -> 0.82 ms against one launch per round)
-static_assert(CC_SAMPLE == 2, "k_cc_sample hooks exactly two neighbours");
-__global__ void k_cc_sample(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
-                            int64_t n, int* parent) {
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
-        const int64_t p = row[v], e = row[v + 1];
-        if (p < e) hook(int(v), nb[p], parent);
-        if (p + 1 < e) hook(int(v), nb[p + 1], parent);
-    }
-}
-
-__global__ void k_cc_compress(int64_t n, int* parent) {
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
-        parent[v] = find_root(int(v), parent);
-}
-
-// most frequent root among CC_VOTES fixed, spread-out vertices (one block)
-__global__ void __launch_bounds__(CC_VOTES) k_cc_vote(int64_t n, const int* parent, int* giant) {
-    __shared__ int roots[CC_VOTES];
-    __shared__ unsigned long long best;
-    const int t = threadIdx.x;
-    const int64_t v = (int64_t(t) * 2654435761ll + 12345) % n;
-    roots[t] = parent[v];
-    if (t == 0) best = 0;
-    __syncthreads();
-    int cnt = 0;
-    for (int j = 0; j < CC_VOTES; ++j) cnt += roots[j] == roots[t];
-    atomicMax(&best, (unsigned long long)cnt << 32 | unsigned(roots[t]));
-    __syncthreads();
-    if (t == 0) *giant = int(best & 0xffffffffu);
-}
-
-// remaining neighbours (index >= CC_SAMPLE) of vertices outside the dominant
-// tree; a lane takes a short list, the whole warp a long one (a hub outside
-// the dominant tree must not serialise on one thread)
-constexpr int CC_REST_LONG = 64;
-__global__ void k_cc_rest(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
-                          int64_t n, const int* __restrict__ giant_p, int* parent) {
-    const int giant = *giant_p;
-    const int lane = int(lane_id());
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < n;
-         base += stride) {
-        const int64_t v = base + lane;
-        int64_t b = 0, e = 0;
-        if (v < n) {
-            b = row[v] + CC_SAMPLE;
-            e = row[v + 1];
-            if (b >= e || find_root(int(v), parent) == giant) b = e = 0;
-        }
-        if (e - b <= CC_REST_LONG)
-            for (int64_t p = b; p < e; ++p) hook(int(v), nb[p], parent);
-        unsigned longs = __ballot_sync(0xffffffffu, e - b > CC_REST_LONG);
-        while (longs) {
-            const int src = __ffs(longs) - 1;
-            longs &= longs - 1;
-            const int64_t lb = __shfl_sync(0xffffffffu, b, src);
-            const int64_t le = __shfl_sync(0xffffffffu, e, src);
-            const int lv = int(base + src);
-            for (int64_t p = lb + lane; p < le; p += 32) hook(lv, nb[p], parent);
-        }
-    }
-}
-
 // Frontier queue entry: the vertex with its row start and degree, written by
 // whoever discovers it (it has just read them), so expanding it next level
 // starts with the neighbour loads — one dependent memory trip less per level
@@ -175,54 +87,68 @@ struct __align__(16) QEnt {
     long long b;
 };
 
-// Flatten and seed the BFS: level 0 at roots (comp[v]==v), -1 elsewhere;
-// roots with neighbours form the first frontier.
-__global__ void k_bfs_seed(const int64_t* __restrict__ row, int64_t n, int* parent,
-                           int32_t* __restrict__ level, QEnt* __restrict__ queue,
-                           DevCounters* C) {
+
+// ---------------------------------------------------------------------------
+// 1. probe: level 0 at isolated vertices, -1 elsewhere; isolated count; the
+//    lowest non-isolated id r0 (max-reduced as n - v).  The last block to
+//    finish seeds the BFS with r0.
+
+__global__ void k_bfs_probe(const int64_t* __restrict__ row, int64_t n,
+                            int32_t* __restrict__ level, QEnt* __restrict__ queue,
+                            DevCounters* C) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    unsigned long long roots = 0, deg0 = 0, dmax0 = 0;
-    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
-        const int64_t v = base + threadIdx.x;
-        bool is_root = false, seed = false;
-        int64_t deg = 0, rb = 0;
-        if (v < n) {
-            int r = find_root(int(v), parent);
-            parent[v] = r;
-            is_root = (r == int(v));
-            rb = row[v];
-            deg = row[v + 1] - rb;
-            seed = is_root && deg > 0;
-            level[v] = is_root ? 0 : -1;
-        }
-        roots += is_root;
-        unsigned long long slot = warp_append(seed, &C->q_len[0]);
-        if (seed) {
-            queue[slot] = QEnt{int(v), int(deg), (long long)rb};
-            deg0 += deg;
-            dmax0 = max(dmax0, (unsigned long long)deg);
-        }
+    unsigned long long iso = 0, key = 0;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+        const bool isolated = row[v + 1] == row[v];
+        level[v] = isolated ? 0 : -1;
+        iso += isolated;
+        if (!isolated) key = max(key, (unsigned long long)(n - v));
     }
-    roots = warp_sum(roots);
-    deg0 = warp_sum(deg0);
+    iso = warp_sum(iso);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dmax0 = max(dmax0, __shfl_xor_sync(0xffffffffu, dmax0, o));
+    for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
     if (lane_id() == 0) {
-        if (dmax0) atomicMax(&C->deg_max[0], dmax0);
-        if (roots) atomicAdd(&C->components, roots);
-        if (deg0) atomicAdd(&C->deg_sum[0], deg0);
+        if (iso) atomicAdd(&C->components, iso);
+        if (key) atomicMax(&C->r0key, key);
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0)
+        last = atomicAdd(&C->probe_done, 1ull) == (unsigned long long)(gridDim.x - 1);
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long k = *(volatile unsigned long long*)&C->r0key;
+        if (k) {
+            const int r0 = int(n - int64_t(k));
+            const int64_t b = row[r0];
+            const int64_t d = row[r0 + 1] - b;
+            level[r0] = 0;
+            queue[0] = QEnt{r0, int(d), (long long)b};
+            C->q_len[0] = 1;
+            C->deg_sum[0] = (unsigned long long)d;
+            C->deg_max[0] = (unsigned long long)d;
+            C->components += 1;
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// cooperative multi-source BFS
+// 2. cooperative direction-optimising BFS
 
 #ifndef TCB_BFS_BLOCK
 #define TCB_BFS_BLOCK 512
 #endif
 constexpr int BFS_BLOCK = TCB_BFS_BLOCK;
-constexpr int64_t BFS_ALPHA = 14;  // top-down -> bottom-up when m_f > m_u / ALPHA
-constexpr int64_t BFS_BETA = 24;   // bottom-up -> top-down when n_f < n / BETA
+#ifndef TCB_BFS_ALPHA
+#define TCB_BFS_ALPHA 14
+#endif
+#ifndef TCB_BFS_BETA
+#define TCB_BFS_BETA 24
+#endif
+constexpr int64_t BFS_ALPHA = TCB_BFS_ALPHA;  // top-down -> bottom-up when m_f > m_u / ALPHA
+constexpr int64_t BFS_BETA = TCB_BFS_BETA;    // bottom-up -> top-down when n_f < n / BETA
 constexpr int BFS_HEAVY = 256;     // top-down: longer lists are split into chunks
 #ifndef TCB_BFS_LOWDEG
 #define TCB_BFS_LOWDEG 64
@@ -239,12 +165,23 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
-// Claim and enqueue the unvisited vertices among nb[p] for p in [b, e)
-// handled by this warp (lanes stride by 32).  LOWDEG (every frontier degree
-// <= BFS_LOWDEG, uniform per level): claim with a bare CAS and load the
-// neighbour's degree alongside it, two fewer dependent round trips per level
-// on high-diameter low-degree graphs; otherwise test before the CAS, so hub
-// levels do not hammer already-visited vertices with atomics.
+// The int4 of neighbour entries holding position q (q % 4 == 0).  Rows are
+// not 16-byte aligned, so a lane's four entries are masked to [b, e); the
+// aligned load never leaves the allocation that holds nb[b, e).
+__device__ __forceinline__ int4 ld_nb4(const int32_t* __restrict__ nb, int64_t q) {
+    return __ldg(reinterpret_cast<const int4*>(nb + q));
+}
+
+// Claim and enqueue the unvisited vertices among nb[p], p in [b, e), that
+// this warp handles.
+//  * LOWDEG (every frontier degree <= BFS_LOWDEG, uniform per level: the
+//    high-diameter, low-degree case): lane per entry, claim with a bare CAS
+//    and load the neighbour's row bounds alongside it — two fewer dependent
+//    round trips per level.
+//  * otherwise (hub levels): lane l takes the aligned int4 at a0 + 4 l + 128 k
+//    (four entries per load, masked to [b, e)); test before the CAS so hub
+//    levels do not hammer visited vertices with atomics; one queue append
+//    per 128 entries.
 template <bool LOWDEG>
 __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
                                           const int32_t* __restrict__ nb, int64_t b, int64_t e,
@@ -252,54 +189,154 @@ __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
                                           unsigned long long* qlen, unsigned long long& my_deg,
                                           unsigned long long& my_dmax) {
     const unsigned lane = lane_id();
-    for (int64_t p0 = b; p0 < e; p0 += 32) {
-        const int64_t p = p0 + lane;
-        bool claim = false;
-        int w = 0;
-        unsigned long long d = 0;
-        int64_t rw = 0;
-        if (p < e) {
-            w = nb[p];
-            if (LOWDEG) {
+    if (LOWDEG) {
+        for (int64_t p0 = b; p0 < e; p0 += 32) {
+            const int64_t p = p0 + lane;
+            bool claim = false;
+            int w = 0;
+            unsigned long long d = 0;
+            int64_t rw = 0;
+            if (p < e) {
+                w = nb[p];
                 rw = row[w];
                 d = row[w + 1] - rw;
                 claim = atomicCAS(&level[w], -1, next_level) == -1;
-            } else if (level[w] == -1 && atomicCAS(&level[w], -1, next_level) == -1) {
-                claim = true;
-                rw = row[w];
-                d = row[w + 1] - rw;
+            }
+            unsigned long long slot = warp_append(claim, qlen);
+            if (claim) {
+                nxt[slot] = QEnt{w, int(d), (long long)rw};
+                my_deg += d;
+                my_dmax = max(my_dmax, d);
             }
         }
-        unsigned long long slot = warp_append(claim, qlen);
-        if (claim) {
-            nxt[slot] = QEnt{w, int(d), (long long)rw};
-            my_deg += d;
-            my_dmax = max(my_dmax, d);
+        return;
+    }
+    const int bi = int(b), ei = int(e);  // 2m < 2^31
+    for (int q0 = bi & ~3; q0 < ei; q0 += 128) {
+        const int q = q0 + 4 * int(lane);
+        int w[4] = {0, 0, 0, 0};
+        unsigned cm = 0;  // claimed entries of this lane
+        if (q < ei) {
+            const int4 x = ld_nb4(nb, q);
+            w[0] = x.x;
+            w[1] = x.y;
+            w[2] = x.z;
+            w[3] = x.w;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (q + i >= bi && q + i < ei && level[w[i]] == -1 &&
+                    atomicCAS(&level[w[i]], -1, next_level) == -1)
+                    cm |= 1u << i;
+        }
+        const int c = __popc(cm);
+        const int inc = warp_inclusive_scan(c);
+        const int tot = __shfl_sync(0xffffffffu, inc, 31);
+        if (tot == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(qlen, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(inc - c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (!((cm >> i) & 1u)) continue;
+            const int64_t rw = row[w[i]];
+            const int d = int(row[w[i] + 1] - rw);
+            nxt[base++] = QEnt{w[i], d, (long long)rw};
+            my_deg += (unsigned long long)d;
+            my_dmax = max(my_dmax, (unsigned long long)d);
         }
     }
 }
 
-__global__ void __launch_bounds__(BFS_BLOCK)
+// Does v (row [b, e)) have a neighbour in the frontier bitmap?  int4 loads,
+// the four bit tests of a load issued together; stops at the first hit.
+__device__ __forceinline__ bool bu_scan(const int32_t* __restrict__ nb, int64_t b, int64_t e,
+                                        const uint32_t* __restrict__ fc) {
+    for (int64_t q = b & ~int64_t(3); q < e; q += 4) {
+        const int4 x = ld_nb4(nb, q);
+        const int w[4] = {x.x, x.y, x.z, x.w};
+        bool hit = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (q + i >= b && q + i < e) hit |= (fc[w[i] >> 5] >> (w[i] & 31)) & 1u;
+        if (hit) return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct BfsBits {
+    uint32_t* vis;    // visited
+    uint32_t* fb[2];  // frontier of level L in fb[L & 1]
+    int64_t nw;       // words per bitmap
+};
+
+// bottom-up step L over bitmaps: warp per word of 32 consecutive vertices;
+// the word's ballot is the next frontier word and updates the visited word
+__device__ __forceinline__ void bu_step(const int64_t* __restrict__ row,
+                                     const int32_t* __restrict__ nb, int64_t n, int32_t* level,
+                                     const BfsBits& bits, int L, int gwarp, int nwarps,
+                                     unsigned long long& my_deg, unsigned long long& my_dmax,
+                                     unsigned long long& my_cnt) {
+    const unsigned lane = lane_id();
+    const uint32_t* __restrict__ fc = bits.fb[L & 1];
+    uint32_t* fn = bits.fb[(L + 1) & 1];
+    for (int j = gwarp; j < int(bits.nw); j += nwarps) {
+        const uint32_t vw = bits.vis[j];
+        uint32_t fm = 0;
+        if (vw != 0xFFFFFFFFu) {
+            const int v = j * 32 + int(lane);
+            bool found = false;
+            int64_t d = 0;
+            if (v < n && !((vw >> lane) & 1u)) {
+                const int64_t b = row[v], e = row[v + 1];
+                d = e - b;
+                found = bu_scan(nb, b, e, fc);
+            }
+            fm = __ballot_sync(0xffffffffu, found);
+            if (found) {
+                level[v] = L + 1;
+                my_deg += (unsigned long long)d;
+                my_dmax = max(my_dmax, (unsigned long long)d);
+            }
+            if (lane == 0 && fm) bits.vis[j] = vw | fm;
+        }
+        if (lane == 0) fn[j] = fm;
+        my_cnt += lane == 0 ? __popc(fm) : 0;
+    }
+}
+
+__global__ void __launch_bounds__(BFS_BLOCK, 2)
     k_bfs_coop(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                int32_t* level, QEnt* qa, QEnt* qb, int2* chunks, DevCounters* C,
-               int64_t dir_edges) {
+               int64_t dir_edges, const unsigned long long* dir_edges_p, BfsBits bits,
+               int* rest, int* parent, int collect) {
     cg::grid_group grid = cg::this_grid();
-    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
-    const int64_t gwarp = gtid >> 5;
-    const int64_t nwarps = gthreads >> 5;
+    // 2m < 2^31 (require_sizes): every count below fits 32 bits, which
+    // keeps the persistent kernel within 64 registers (2 CTAs per SM)
+    const int gtid = int(blockIdx.x * blockDim.x + threadIdx.x);
+    const int gthreads = int(gridDim.x * blockDim.x);
+    const int gwarp = gtid >> 5;
+    const int nwarps = gthreads >> 5;
     const unsigned lane = lane_id();
     __shared__ long long s_bc[3];  // per-block broadcast of the level counters
 
     int L = 0;
-    int64_t nf = int64_t(ld_volatile_u64(&C->q_len[0]));
-    int64_t mf = int64_t(ld_volatile_u64(&C->deg_sum[0]));
-    int64_t dmax = int64_t(ld_volatile_u64(&C->deg_max[0]));
-    int64_t mu = dir_edges - mf;  // directed entries of not-yet-visited vertices
+    int nf = int(ld_volatile_u64(&C->q_len[0]));
+    const int mf = int(ld_volatile_u64(&C->deg_sum[0]));
+    int dmax = int(ld_volatile_u64(&C->deg_max[0]));
+    // directed entries of unvisited vertices (the second BFS reads its total
+    // from the device: the remainder's degree sum)
+    int mu = int((dir_edges_p ? int64_t(*dir_edges_p) : dir_edges) - mf);
     bool td = true;
     QEnt* cur = qa;
     QEnt* nxt = qb;
     int max_level = 0;
+    if (collect && gtid == 0) C->bfs_t0 = globaltimer_ns();
 
     while (nf > 0) {
         const int sc = L % 3, sn = (L + 1) % 3;
@@ -312,12 +349,10 @@ __global__ void __launch_bounds__(BFS_BLOCK)
             C->deg_max[sr] = 0;
             C->nchunks[sr] = 0;
         }
-        unsigned long long my_deg = 0, my_dmax = 0;
+        unsigned long long my_deg = 0, my_dmax = 0, my_cnt = 0;
         if (td) {
-            // top-down: warp per frontier vertex; lists longer than BFS_HEAVY
-            // are cut into chunks that all warps share after a barrier
             const bool heavy = dmax > BFS_HEAVY;
-            for (int64_t i = gwarp; i < nf; i += nwarps) {
+            for (int i = gwarp; i < nf; i += nwarps) {
                 const QEnt q = cur[i];
                 const int u = q.v;
                 const int64_t b = q.b, e = q.b + q.d;
@@ -341,9 +376,9 @@ __global__ void __launch_bounds__(BFS_BLOCK)
                 grid.sync();
                 if (threadIdx.x == 0) s_bc[0] = (long long)ld_volatile_u64(&C->nchunks[sc]);
                 __syncthreads();
-                const int64_t nch = s_bc[0];
+                const int nch = int(s_bc[0]);
                 __syncthreads();
-                for (int64_t c = gwarp; c < nch; c += nwarps) {
+                for (int c = gwarp; c < nch; c += nwarps) {
                     const int2 ch = chunks[c];
                     const int64_t b = row[ch.x] + ch.y;
                     const int64_t e = min(row[ch.x + 1], b + BFS_HEAVY);
@@ -352,33 +387,15 @@ __global__ void __launch_bounds__(BFS_BLOCK)
                 }
             }
         } else {
-            // bottom-up: every unvisited vertex looks for a parent on level L
-            for (int64_t base = gtid - lane; base < n; base += gthreads) {
-                const int64_t v = base + lane;
-                bool found = false;
-                if (v < n && level[v] == -1) {
-                    const int64_t b = row[v], e = row[v + 1];
-                    for (int64_t p = b; p < e; ++p) {
-                        if (level[nb[p]] == L) {
-                            found = true;
-                            break;
-                        }
-                    }
-                    if (found) {
-                        level[v] = L + 1;
-                        my_deg += e - b;
-                        my_dmax = max(my_dmax, (unsigned long long)(e - b));
-                    }
-                }
-                unsigned cnt = __popc(__ballot_sync(0xffffffffu, found));
-                if (lane == 0 && cnt) atomicAdd(&C->q_len[sn], (unsigned long long)cnt);
-            }
+            bu_step(row, nb, n, level, bits, L, gwarp, nwarps, my_deg, my_dmax, my_cnt);
         }
         my_deg = warp_sum(my_deg);
         my_dmax = warp_max_u64(my_dmax);
+        my_cnt = warp_sum(my_cnt);
         if (lane == 0) {
             if (my_deg) atomicAdd(&C->deg_sum[sn], my_deg);
             if (my_dmax) atomicMax(&C->deg_max[sn], my_dmax);
+            if (my_cnt) atomicAdd(&C->q_len[sn], my_cnt);
         }
 
         grid.sync();
@@ -389,9 +406,9 @@ __global__ void __launch_bounds__(BFS_BLOCK)
             s_bc[2] = (long long)ld_volatile_u64(&C->deg_max[sn]);
         }
         __syncthreads();
-        const int64_t nf_next = s_bc[0];
-        const int64_t mf_next = s_bc[1];
-        dmax = s_bc[2];
+        const int nf_next = int(s_bc[0]);
+        const int mf_next = int(s_bc[1]);
+        dmax = int(s_bc[2]);
         __syncthreads();
 #ifdef TCB_CHECKS
         if (gtid == 0 && (L < 40 || (L & 255) == 0)) {
@@ -402,20 +419,42 @@ __global__ void __launch_bounds__(BFS_BLOCK)
                    (long long)dmax, now);
         }
 #endif
+        if (collect && gtid == 0 && L < TCB_LEVEL_RECORDS) {  // first BFS only
+            C->lev_rec[2 * L] = (td ? 0ull : 1ull << 62) | globaltimer_ns();
+            C->lev_rec[2 * L + 1] = (unsigned long long)nf_next;
+            C->nlev = L + 1;
+        }
         if (nf_next > 0) max_level = L + 1;
         mu -= mf_next;
         bool next_td;
         if (td)
             next_td = !(mf_next > mu / BFS_ALPHA);
         else
-            next_td = (nf_next < n / BFS_BETA) && (nf_next < nf);
+            next_td = (nf_next < int(n / BFS_BETA)) && (nf_next < nf);
 
-        if (nf_next > 0 && next_td && !td) {
-            // materialise the level-(L+1) frontier as a queue for top-down
+        if (nf_next > 0 && !next_td && td) {
+            // entering bottom-up: visited and level-(L+1) bitmaps from the levels
+            uint32_t* fn = bits.fb[(L + 1) & 1];
+            for (int j = gwarp; j < int(bits.nw); j += nwarps) {
+                const int v = j * 32 + int(lane);
+                const int lv = v < n ? level[v] : 0;
+                const unsigned vm = __ballot_sync(0xffffffffu, lv != -1);
+                const unsigned fm = __ballot_sync(0xffffffffu, v < n && lv == L + 1);
+                if (lane == 0) {
+                    bits.vis[j] = vm;
+                    fn[j] = fm;
+                }
+            }
+            grid.sync();
+        } else if (nf_next > 0 && next_td && !td) {
+            // leaving bottom-up: the level-(L+1) frontier bitmap as a queue
+            const uint32_t* fn = bits.fb[(L + 1) & 1];
             unsigned long long* qc = &C->scratch[4];
-            for (int64_t base = gtid - lane; base < n; base += gthreads) {
-                const int64_t v = base + lane;
-                bool in = v < n && level[v] == L + 1;
+            for (int j = gwarp; j < int(bits.nw); j += nwarps) {
+                const uint32_t fm = fn[j];
+                if (fm == 0) continue;  // warp-uniform
+                const bool in = (fm >> lane) & 1u;
+                const int v = j * 32 + int(lane);
                 unsigned long long slot = warp_append(in, qc);
                 if (in) {
                     const int64_t rb = row[v];
@@ -434,75 +473,152 @@ __global__ void __launch_bounds__(BFS_BLOCK)
         nf = nf_next;
         ++L;
     }
-    if (gtid == 0) C->max_level = max_level;
+    if (gtid == 0 && max_level) atomicMax(&C->max_level, max_level);
+    if (!collect) return;
+    // vertices left unvisited belong to other components: list them (each its
+    // own union-find tree for now) with their degree total
+    unsigned long long my_rest_deg = 0;
+    for (int base = gtid - int(lane); base < n; base += gthreads) {
+        const int v = base + int(lane);
+        const bool un = v < n && level[v] == -1;
+        const unsigned long long slot = warp_append(un, &C->rest_n);
+        if (un) {
+            rest[slot] = int(v);
+            parent[v] = int(v);
+            my_rest_deg += (unsigned long long)(row[v + 1] - row[v]);
+        }
+    }
+    my_rest_deg = warp_sum(my_rest_deg);
+    if (lane == 0 && my_rest_deg) atomicAdd(&C->rest_deg, my_rest_deg);
 }
 
 // ---------------------------------------------------------------------------
+// 3. the remainder: union-find over the unvisited vertices (every edge of an
+//    unvisited vertex stays inside U), then its roots seed the second BFS
 
-__global__ void k_cc_iota(int64_t n, int* __restrict__ parent) {
+constexpr int CC_REST_LONG = 64;
+__global__ void k_rest_hook(const int64_t* __restrict__ row, const int32_t* __restrict__ nb,
+                            const int* __restrict__ rest, const DevCounters* C, int* parent) {
+    const int64_t nr = int64_t(C->rest_n);
+    const int lane = int(lane_id());
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
-        parent[v] = int(v);
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < nr;
+         base += stride) {
+        const int64_t i = base + lane;
+        int v = 0;
+        int64_t b = 0, e = 0;
+        if (i < nr) {
+            v = rest[i];
+            b = row[v];
+            e = row[v + 1];
+        }
+        // one hook per undirected edge: from the lower endpoint
+        if (e - b <= CC_REST_LONG)
+            for (int64_t p = b; p < e; ++p) {
+                const int w = nb[p];
+                if (w > v) hook(v, w, parent);
+            }
+        unsigned longs = __ballot_sync(0xffffffffu, e - b > CC_REST_LONG);
+        while (longs) {  // a hub outside r0's component: the whole warp
+            const int src = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const int64_t lb = __shfl_sync(0xffffffffu, b, src);
+            const int64_t le = __shfl_sync(0xffffffffu, e, src);
+            const int lv = __shfl_sync(0xffffffffu, v, src);
+            for (int64_t p = lb + lane; p < le; p += 32) {
+                const int w = nb[p];
+                if (w > lv) hook(lv, w, parent);
+            }
+        }
+    }
 }
 
-// Streaming components for the host-buffer entries: every vertex its own
-// tree, then each neighbour chunk, once resident, hooks its entries (u, v)
-// with u < v — one hook per undirected edge over all chunks, the full
-// union-find, hidden under the rest of the transfer.  Roots are min ids
-// whatever the hook order, so bfs_levels (which then skips its Afforest
-// phases) labels exactly as from the sampled path.
-void cc_stream_begin(Context* ctx, int64_t n) {
-    int* parent = ctx->wsT<int>(WS_COMP, n);
-    TCB_LAUNCH(ctx, k_cc_iota, grid_for(ctx, n, 256), 256, 0, n, parent);
-    ctx->cc_ready = true;
+__global__ void k_rest_seed(const int64_t* __restrict__ row, const int* __restrict__ rest,
+                            int* parent, int32_t* __restrict__ level, QEnt* __restrict__ queue,
+                            DevCounters* C) {
+    const int64_t nr = int64_t(*(volatile unsigned long long*)&C->rest_n);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    unsigned long long deg = 0, dmax = 0, roots = 0;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < nr; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        bool root = false;
+        int v = 0;
+        int64_t b = 0, d = 0;
+        if (i < nr) {
+            v = rest[i];
+            root = find_root(v, parent) == v;
+            if (root) {
+                level[v] = 0;
+                b = row[v];
+                d = row[v + 1] - b;
+            }
+        }
+        const unsigned long long slot = warp_append(root, &C->q_len[0]);
+        if (root) {
+            queue[slot] = QEnt{v, int(d), (long long)b};
+            deg += (unsigned long long)d;
+            dmax = max(dmax, (unsigned long long)d);
+            ++roots;
+        }
+    }
+    deg = warp_sum(deg);
+    dmax = warp_max_u64(dmax);
+    roots = warp_sum(roots);
+    if (lane_id() == 0) {
+        if (deg) atomicAdd(&C->deg_sum[0], deg);
+        if (dmax) atomicMax(&C->deg_max[0], dmax);
+        if (roots) atomicAdd(&C->components, roots);
+    }
 }
 
-void cc_stream_hook(Context* ctx, const int32_t* src, const int32_t* nb, int64_t e0, int64_t e1) {
-    if (e1 <= e0) return;
-    int* parent = static_cast<int*>(ctx->slot_ptr[WS_COMP]);
-    TCB_LAUNCH(ctx, k_cc_hook, grid_for(ctx, e1 - e0, 256), 256, 0, src + e0, nb + e0, e1 - e0,
-               parent);
+static void launch_bfs(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n,
+                       int32_t* level, QEnt* qa, QEnt* qb, int2* chunks, int64_t dir_edges,
+                       const unsigned long long* dir_edges_p, BfsBits bits, int* rest,
+                       int* parent, int collect) {
+    DevCounters* C = ctx->d_counters;
+    if (ctx->bfs_coop_blocks == 0) {
+        int per_sm = 0;
+        TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_coop, BFS_BLOCK, 0));
+        require(per_sm > 0, "BFS kernel cannot be co-resident");
+        ctx->bfs_coop_blocks = per_sm * ctx->num_sms;
+    }
+    void* args[] = {(void*)&row,   (void*)&nb,          (void*)&n,    (void*)&level,
+                    (void*)&qa,    (void*)&qb,          (void*)&chunks, (void*)&C,
+                    (void*)&dir_edges, (void*)&dir_edges_p, (void*)&bits,  (void*)&rest,
+                    (void*)&parent, (void*)&collect};
+    TCB_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_coop, dim3(ctx->bfs_coop_blocks),
+                                         dim3(BFS_BLOCK), args, 0, ctx->stream));
+    ctx->launches++;
 }
 
 void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
                 int64_t n, int64_t m, int32_t* level, bool reset_counters) {
+    (void)src;
     require(n < (int64_t(1) << 31), "vertex ids must fit int32");
     DevCounters* C = ctx->d_counters;
     if (reset_counters) TCB_CUDA(cudaMemsetAsync(C, 0, sizeof(DevCounters), ctx->stream));
     if (n == 0) return;
-    int* parent = ctx->wsT<int>(WS_COMP, n);
-    ctx->record(0);
-    const bool hooked = ctx->cc_ready;  // cc_stream_* already built the full union-find
-    ctx->cc_ready = false;
-    if (!hooked) TCB_LAUNCH(ctx, k_cc_init, grid_for(ctx, n, 256), 256, 0, row, nb, n, parent);
-    if (m > 0 && !hooked) {
-        (void)src;
-        int* giant = reinterpret_cast<int*>(&C->scratch[11]);
-        TCB_LAUNCH(ctx, k_cc_sample, grid_for(ctx, n, 256), 256, 0, row, nb, n, parent);
-        TCB_LAUNCH(ctx, k_cc_compress, grid_for(ctx, n, 256), 256, 0, n, parent);
-        TCB_LAUNCH(ctx, k_cc_vote, 1, CC_VOTES, 0, n, (const int*)parent, giant);
-        TCB_LAUNCH(ctx, k_cc_rest, grid_for(ctx, n, 256), 256, 0, row, nb, n, (const int*)giant,
-                   parent);
-    }
     QEnt* qa = ctx->wsT<QEnt>(WS_QUEUE_A, n);
     QEnt* qb = ctx->wsT<QEnt>(WS_QUEUE_B, n);
-    TCB_LAUNCH(ctx, k_bfs_seed, grid_for(ctx, n, 256), 256, 0, row, n, parent, level, qa, C);
+    ctx->record(0);
+    TCB_LAUNCH(ctx, k_bfs_probe, grid_for(ctx, n, 256), 256, 0, row, n, level, qa, C);
     ctx->record(1);
     if (m > 0) {
-        if (ctx->bfs_coop_blocks == 0) {
-            int per_sm = 0;
-            TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_coop,
-                                                                   BFS_BLOCK, 0));
-            require(per_sm > 0, "BFS kernel cannot be co-resident");
-            ctx->bfs_coop_blocks = per_sm * ctx->num_sms;
-        }
-        int64_t dir_edges = 2 * m;
+        int* parent = ctx->wsT<int>(WS_COMP, n);
+        const int64_t nw = (n + 31) / 32;
+        uint32_t* bw = ctx->wsT<uint32_t>(WS_BFS_BITS, 3 * nw);
+        BfsBits bits{bw, {bw + nw, bw + 2 * nw}, nw};
         int2* chunks = ctx->wsT<int2>(WS_MISC, 2 * m / BFS_HEAVY + n + 1);
-        void* args[] = {(void*)&row, (void*)&nb,     (void*)&n, (void*)&level,    (void*)&qa,
-                        (void*)&qb,  (void*)&chunks, (void*)&C, (void*)&dir_edges};
-        TCB_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_coop, dim3(ctx->bfs_coop_blocks),
-                                             dim3(BFS_BLOCK), args, 0, ctx->stream));
-        ctx->launches++;
+        int* rest = reinterpret_cast<int*>(qb);  // free once the first BFS is done
+        launch_bfs(ctx, row, nb, n, level, qa, qb, chunks, 2 * m, nullptr, bits, rest, parent, 1);
+        // the remainder (kernels exit at once when the first BFS saw everything)
+        TCB_LAUNCH(ctx, k_rest_hook, grid_for(ctx, n, 256), 256, 0, row, nb, (const int*)rest,
+                   (const DevCounters*)C, parent);
+        TCB_CUDA(cudaMemsetAsync(&C->q_len[0], 0, 12 * sizeof(unsigned long long), ctx->stream));
+        TCB_LAUNCH(ctx, k_rest_seed, grid_for(ctx, n, 256), 256, 0, row, (const int*)rest, parent,
+                   level, qa, C);
+        launch_bfs(ctx, row, nb, n, level, qa, qb, chunks, 0, &C->rest_deg, bits, rest, parent,
+                   0);
     }
     ctx->record(2);
 }

@@ -17,8 +17,6 @@ void csr_rows(Context*, const int64_t*, int64_t, int32_t*);
 void csr_edges(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*, int32_t*);
 void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
                 int32_t*, bool);
-void cc_stream_begin(Context*, int64_t);
-void cc_stream_hook(Context*, const int32_t*, const int32_t*, int64_t, int64_t);
 void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
                   int32_t*, int64_t*);
 void bfs_parent(Context*, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t,
@@ -44,7 +42,6 @@ namespace {
 template <typename F>
 int guarded(tcb_context* ctx, F&& f) {
     if (!ctx) return TCB_ERR_INVALID;
-    ctx->cc_ready = false;  // a streamed union-find never outlives its call
     try {
         TCB_CUDA(cudaSetDevice(ctx->device));
         f();
@@ -170,7 +167,7 @@ TCB_API int tcb_context_destroy(tcb_context* ctx) {
     if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
-    for (auto& e : ctx->chunk_ev)
+    for (auto& e : ctx->copy_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
@@ -211,6 +208,23 @@ TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n) {
         require(ms_out != nullptr, "ms_out is null");
         for (int i = 0; i < n && i < TCB_NSTAGES; ++i) ms_out[i] = ctx->stage_ms[i];
     });
+}
+
+TCB_API int tcb_level_records(tcb_context* ctx, int64_t* out, int cap) {
+    int cnt = 0;
+    const int rc = guarded(ctx, [&] {
+        require(out != nullptr || cap == 0, "out is null");
+        const DevCounters& h = *ctx->h_counters;
+        const int nl = int(h.nlev < TCB_LEVEL_RECORDS ? h.nlev : TCB_LEVEL_RECORDS);
+        for (int i = 0; i < nl && i < cap; ++i) {
+            const unsigned long long e = h.lev_rec[2 * i];
+            out[3 * i] = int64_t(e >> 62);
+            out[3 * i + 1] = int64_t(e & ((1ull << 62) - 1)) - int64_t(h.bfs_t0);
+            out[3 * i + 2] = int64_t(h.lev_rec[2 * i + 1]);
+            ++cnt;
+        }
+    });
+    return rc == TCB_OK ? cnt : -rc;
 }
 
 TCB_API int tcb_rmat_generate(tcb_context* ctx, int scale, int64_t edge_factor, double a,
@@ -480,12 +494,9 @@ TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
 }
 
 // host-buffer entries: upload the CSR, derive src, run the fused path (or a
-// shard of it), download the counters (and levels on request)
-// Below this many adjacency entries (256 MB, ~5 ms of PCIe copy) the copy is
-// too short to hide a full union-find: RMAT-16 and the lattice keep the
-// sampled one (measured: RMAT-16 e2e 1.0 -> 1.9 ms with the full hook).
-constexpr int64_t kStreamedCopyMin = int64_t(1) << 26;
-
+// shard of it), download the counters (and levels on request).  The
+// neighbour array (the bulk of the bytes) is copied on a copy stream while
+// the entry->row map is built from the row offsets on the compute stream.
 static int host_entry(tcb_context* ctx, const int64_t* h_row_offsets, const int32_t* h_neighbors,
                       int64_t n, int64_t* h_level_out, int shard, int nshards, tcb_result* out) {
     return guarded(ctx, [&] {
@@ -502,37 +513,23 @@ static int host_entry(tcb_context* ctx, const int64_t* h_row_offsets, const int3
         int64_t* row = ctx->wsT<int64_t>(WS_ROW, n + 1);
         int32_t* nb = ctx->wsT<int32_t>(WS_NB, nnz);
         int32_t* src = ctx->wsT<int32_t>(WS_EDGE_U, nnz);
-        // The row offsets first, then the neighbour array in chunks on a copy
-        // stream; the entry->row map and the component union-find run on the
-        // compute stream under the transfer, chunk by chunk (bfs.cu).
+        if (nnz) {
+            if (!ctx->copy_stream) {
+                TCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+                for (auto& e : ctx->copy_ev)
+                    TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            // the copy may not overtake earlier work on the compute stream
+            TCB_CUDA(cudaEventRecord(ctx->copy_ev[0], ctx->stream));
+            TCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[0], 0));
+            TCB_CUDA(cudaMemcpyAsync(nb, h_neighbors, sizeof(int32_t) * nnz,
+                                     cudaMemcpyHostToDevice, ctx->copy_stream));
+            TCB_CUDA(cudaEventRecord(ctx->copy_ev[1], ctx->copy_stream));
+        }
         TCB_CUDA(cudaMemcpyAsync(row, h_row_offsets, sizeof(int64_t) * (n + 1),
                                  cudaMemcpyHostToDevice, ctx->stream));
         csr_rows(ctx, row, n, src);
-        if (nnz && nnz < kStreamedCopyMin) {
-            // small graphs: one copy; the sampled union-find in bfs_levels is
-            // cheaper than hooking every edge when nothing hides it
-            TCB_CUDA(cudaMemcpyAsync(nb, h_neighbors, sizeof(int32_t) * nnz,
-                                     cudaMemcpyHostToDevice, ctx->stream));
-        } else if (nnz) {
-            if (!ctx->copy_stream) {
-                TCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-                for (auto& e : ctx->chunk_ev)
-                    TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            }
-            const int K = Context::kCopyChunks;
-            // the copy may not overtake earlier work on the compute stream
-            TCB_CUDA(cudaEventRecord(ctx->chunk_ev[K], ctx->stream));
-            TCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[K], 0));
-            cc_stream_begin(ctx, n);
-            for (int c = 0; c < K; ++c) {
-                const int64_t e0 = nnz * c / K, e1 = nnz * (c + 1) / K;
-                TCB_CUDA(cudaMemcpyAsync(nb + e0, h_neighbors + e0, sizeof(int32_t) * (e1 - e0),
-                                         cudaMemcpyHostToDevice, ctx->copy_stream));
-                TCB_CUDA(cudaEventRecord(ctx->chunk_ev[c], ctx->copy_stream));
-                TCB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[c], 0));
-                cc_stream_hook(ctx, src, nb, e0, e1);
-            }
-        }
+        if (nnz) TCB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->copy_ev[1], 0));
         if (ctx->timing) TCB_CUDA(cudaEventRecord(ctx->ev[9], ctx->stream));
         int32_t* level = ctx->wsT<int32_t>(WS_LEVEL, n);
         cetc_device(ctx, row, nb, src, n, m, level, shard, nshards);

@@ -70,6 +70,7 @@ enum Slot : int {
     WS_LISTS,         // intersection: off-level / upper same-level neighbour lists int32[2m]
     WS_CLASS,         // intersection: per-32-entry class bits + word prefixes
     WS_VBEG,          // intersection: per-vertex list starts int64[2(n+1)]
+    WS_BFS_BITS,      // BFS: visited + two frontier bitmaps, 3 x ceil(n/32) words
     WS_NSLOTS
 };
 
@@ -85,6 +86,14 @@ struct DevCounters {
     unsigned long long deg_sum[3];
     unsigned long long deg_max[3];       // largest degree in the next frontier
     unsigned long long nchunks[3];       // heavy-vertex chunks queued this level
+    // components (bfs.cu): the lowest non-isolated id as n - v (max-reduced,
+    // 0 = none), the probe's finished-block count, and the vertices the
+    // first BFS left unvisited (count, degree sum)
+    unsigned long long r0key, probe_done, rest_n, rest_deg;
+    // per-level diagnostics of the first BFS (tcb_level_records): start time,
+    // then (mode << 62 | end time ns) and the next frontier size per level
+    unsigned long long bfs_t0, nlev;
+    unsigned long long lev_rec[2 * TCB_LEVEL_RECORDS];
     unsigned long long scratch[16];
 };
 
@@ -110,12 +119,10 @@ struct Context {
     int tune_hc = 0;   // intersection: ids staged per CTA pass (0 = default)
     int test_flags = 0;  // tcb_set_test_flags: force rarely taken paths (tests only)
     bool isect_events = false;  // events 5/6 bracket the CTA-tier kernel
-    // host-buffer entries: neighbour chunks land on copy_stream while the
-    // union-find hooks the ones already resident (bfs.cu cc_stream_*)
-    static constexpr int kCopyChunks = 8;
+    // host-buffer entries: the neighbour array lands on copy_stream while
+    // the entry->row map is built on the compute stream
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t chunk_ev[kCopyChunks + 1] = {};
-    bool cc_ready = false;  // components already hooked: bfs_levels skips its CC phases
+    cudaEvent_t copy_ev[2] = {};
 
     void* ws(Slot s, size_t bytes) {
         if (bytes == 0) bytes = 16;
