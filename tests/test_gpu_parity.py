@@ -247,10 +247,11 @@ def test_every_intersection_path_rmat16(tuning):
 
 
 def test_hub_outside_dominant_component():
-    """A long cycle (the dominant component, found by the sample vote) plus a
-    star whose hub is not its component's minimum: the hub's remaining
-    neighbours take the warp-cooperative hooking path (k_cc_rest), and a
-    triangle fan on the star exercises the non-dominant component's count."""
+    """A long cycle holding vertex 0 (the first BFS's root) plus a star whose
+    hub is not its component's minimum: the star is left for the remainder
+    union-find, where the hub's row takes the warp-cooperative hooking path
+    (k_rest_hook), and a triangle fan on the star exercises the second BFS
+    and the count on a non-root component."""
     rng = np.random.default_rng(11)
     n_cyc, leaves = 200_000, 5000
     cyc = np.stack([np.arange(n_cyc), (np.arange(n_cyc) + 1) % n_cyc], axis=1)
@@ -304,10 +305,10 @@ def test_capacity_rmat25_matches_forward():
     torch.cuda.empty_cache()
 
 
-def test_host_entry_chunked_copy_rmat22():
-    """tcb_cetc_host on a graph large enough for the chunked neighbour copy
-    with the union-find hooked under it (2m >= 2^26 entries, 8 chunks):
-    identical counts, components and levels to the device-resident path."""
+def test_host_entry_copy_rmat22():
+    """tcb_cetc_host on RMAT-22 (the neighbour array copied on the copy
+    stream under the entry->row map): identical counts, components and
+    levels to the device-resident path."""
     import torch
     dg = C.build_device_graph("rmat22")
     dev = tb.cetc(dg, keep_level=True)
