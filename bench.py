@@ -358,11 +358,16 @@ def main():
     # bytes the CTA-tier kernel must move (owners with d > WT = 256).  With
     # the level rule applied before the intersection (intersect.cu) an edge
     # (owner x, partner p) streams OFF(p) (p's neighbours on another level)
-    # and p's same-level neighbours ranked above x (degree desc, id asc): 4
-    # B/id.  Plus the partner id and its list bounds per cover edge (36 B),
-    # and the owner's OFF(x) ∪ UP(x) staged once per item (<= 1024 partners).
+    # and p's same-level neighbours ranked above x (degree bucket desc, id
+    # asc): 4 B/id.  Plus the partner id and its list bounds per cover edge
+    # (36 B), and the owner's OFF(x) ∪ UP(x) staged once per item (<= 1024
+    # partners).
     cu, cv = full.cover_u.long(), full.cover_v.long()
-    own_u = (du > dv) | ((du == dv) & (cu < cv))
+    # owner order (intersect.cu): degree bucket floor(log2 d) desc, id asc
+    bk = torch.floor(torch.log2(deg.clamp(min=1).double())).long()
+    bu, bv = bk[cu], bk[cv]
+    own_u = (bu > bv) | ((bu == bv) & (cu < cv))
+    del bu, bv
     d_own = torch.where(own_u, du, dv)
     owner = torch.where(own_u, cu, cv)
     partner = torch.where(own_u, cv, cu)
@@ -376,8 +381,8 @@ def main():
     n_off = torch.bincount(srcl[~same], minlength=n)
     s_src, s_nb = srcl[same], nbl[same]
     del srcl, nbl, same, lev
-    # rank: degree desc, id asc (higher value = ranked higher)
-    order = torch.argsort(deg * (n + 1) + (n - torch.arange(n, device=dev)))
+    # rank: degree bucket desc, id asc (higher value = ranked higher)
+    order = torch.argsort(bk * (n + 1) + (n - torch.arange(n, device=dev)))
     rk = torch.empty(n, dtype=torch.long, device=dev)
     rk[order] = torch.arange(n, device=dev)
     del order

@@ -17,7 +17,8 @@
 // (counted in c1) or on L for both.  Every CSR row is split into two lists:
 //     OFF(v) = neighbours on another level (id-sorted),
 //     UP(v)  = neighbours on v's level that rank above v in the owner order
-//              (degree desc, id asc), sorted by degree bucket, largest first,
+//              (degree bucket floor(log2 d) desc, id asc), sorted in that
+//              order (stable counting sort of the id-sorted row by bucket),
 // and an edge (owner x, partner p) has apexes OFF(x)∩OFF(p) (c1) and
 // UP(x)∩UP(p) (same level, ranked above both endpoints).  Every same-level
 // triangle a > b > c (owner order) is therefore found exactly once, at its
@@ -26,9 +27,12 @@
 // the reference's T - c1 and its c2 (every same-level hit, 3 per triangle,
 // _kernels.py:745-748) is 3 x this tally; the counters hold c2 in those
 // units.  Ranking by degree keeps the same-level stream short: p streams
-// only the part of UP(p) in degree buckets >= x's (a prefix, ucnt table),
-// and hubs have few neighbours above them.  Same-level neighbours ranked
-// below the endpoint are never read, and a hit needs no level lookup: the
+// only the part of UP(p) ranked above x — a prefix of the sorted list: the
+// buckets above x's (ucnt table) plus the ids below x in x's own bucket (one
+// binary search per edge, Lists::up_cut) — and hubs have few neighbours
+// above them.  (The bucket order streams within 1% of the ids the exact
+// degree order would, and its sorted lists come from a counting sort.)
+// Same-level neighbours ranked below the endpoint are never read, and a hit needs no level lookup: the
 // list it was streamed from says which tally it belongs to.
 //
 //  1. owner bits: a keep bit per CSR entry (x, y) with level[x]==level[y] &&
@@ -37,7 +41,8 @@
 //     come out contiguous: P[seg_beg[x], seg_end[x]).
 //  2. lists: word prefixes of the class bits give every entry its slot in
 //     the OFF array and every row its UP range (no second scan); UP rows are
-//     counting-sorted by degree bucket (per-row histogram, prefix, scatter).
+//     stably counting-sorted by degree bucket (per-row histogram, prefix,
+//     scatter in row order), so each bucket's run is id-sorted.
 //  3. split points: the id space is cut into F equal ranges; split[v][r] is
 //     the position in OFF(v) of the first id in range r.  An owner whose OFF
 //     list exceeds the table is staged one group of ranges at a time, and
@@ -103,7 +108,8 @@ struct __align__(32) PRec {
     uint32_t ob, ub, noff;
     uint16_t uc[PR_NK];
 };
-static_assert(sizeof(PRec) == 32, "one sector per partner");              // degree buckets: floor(log2 d)
+static_assert(sizeof(PRec) == 32, "one sector per partner");
+constexpr int PR_FULL = 0xFFFF;  // uc entry too large for 16 bits: read ucnt              // degree buckets: floor(log2 d)
 __device__ __forceinline__ int dbucket(int d) { return 31 - __clz(max(d, 1)); }
 
 __device__ __forceinline__ int ceil_log2_dev(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
@@ -254,10 +260,27 @@ struct Lists {
     const int* __restrict__ ucnt;   // [v*NBKT + k] = UP(v) entries with degree bucket >= k
     const PRec* __restrict__ prec;  // per-vertex partner record (CTA tier)
     int rshift;
-    // the part of UP(p) that can hold an apex of owner x (degree bucket kx):
-    // neighbours of p with degree >= 2^kx, a prefix of UP(p)
-    __device__ __forceinline__ int up_prefix(int64_t p, int kx) const {
-        return ucnt[p * NBKT + kx];
+    // The part of UP(p) that can hold an apex of owner x (degree bucket kx):
+    // the entries ranked above x.  UP(p) is sorted by (degree bucket desc, id
+    // asc), the owner order, so they are a prefix: the runs of buckets > kx
+    // ([0, lo)) plus the ids below x in bucket kx's run [lo, hi) — a binary
+    // search (x itself sits in that run: it is p's same-level neighbour).
+    __device__ __forceinline__ int up_cut(uint32_t ub, int lo, int hi, int x) const {
+#ifdef TCB_UPCUT_BUCKET  // measurement-only: stream the whole bucket-kx run
+        return hi;           // (over-streams; counts unchanged: no false hits)
+#endif
+        if (hi - lo <= 1) return lo;  // the run is x alone
+        uint32_t a = ub + uint32_t(lo), z = ub + uint32_t(hi);
+        while (a < z) {
+            const uint32_t mid = a + ((z - a) >> 1);
+            if (L[mid] < x) a = mid + 1; else z = mid;
+        }
+        return int(a - ub);
+    }
+    __device__ __forceinline__ int up_cut(int64_t p, int kx, int x) const {
+        const int hi = ucnt[p * NBKT + kx];
+        const int lo = kx + 1 < NBKT ? ucnt[p * NBKT + kx + 1] : 0;
+        return up_cut(vb[p].y, lo, hi, x);
     }
 };
 
@@ -292,7 +315,10 @@ __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __r
                 a = vinfo[x];
                 b = vinfo[y];
             }
-            keep = a.x == b.x && (a.y > b.y || (a.y == b.y && x < y));
+            // owner order: degree bucket desc, id asc (forward mode: degree
+            // desc, id asc, the order staged() filters by)
+            const int ka = fwd ? a.y : dbucket(a.y), kb = fwd ? b.y : dbucket(b.y);
+            keep = a.x == b.x && (ka > kb || (ka == kb && x < y));
             off = fwd || a.x != b.x;
             sup = !fwd && a.x == b.x && !keep;  // UP: same level, y owns the edge
         }
@@ -393,9 +419,33 @@ __global__ void k_scatter_off(const int32_t* __restrict__ nb, int64_t nnz,
 // costs d/1024 iterations) and gather twice.  Rows of isolated vertices are
 // never read and are skipped.
 constexpr int UP_WARPS = 8;
+#ifndef TCB_UPW
+#define TCB_UPW 4  // long-row UP words whose loads are in flight together
+#endif
+#ifndef TCB_UP_MINB
+#define TCB_UP_MINB 8  // k_build_up is latency-bound: keep 64 warps per SM
+#endif
+
+// Stable counting-sort placement for one 32-entry step of a row (lanes hold
+// consecutive row entries, so ids ascend with the lane): entries of the same
+// bucket keep their lane order and each bucket's run of the UP list stays
+// id-sorted.  h[b] = next free position of bucket b.
+__device__ __forceinline__ int stable_slot(int* h, bool act, int b) {
+    const int lane = int(lane_id());
+    const unsigned peers = __match_any_sync(0xffffffffu, act ? b : NBKT + lane);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (act && lane == leader) {
+        base = h[b];
+        h[b] = base + __popc(peers);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    __syncwarp();
+    return base + __popc(peers & lanemask_lt());
+}
 constexpr int UP_SHORT = 256;
 static_assert(NBKT == 32, "one degree bucket per lane");
-__global__ void __launch_bounds__(UP_WARPS * 32)
+__global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
     k_build_up(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                const uint2* __restrict__ cls, const uint8_t* __restrict__ dbk,
                const uint2* __restrict__ vb, int32_t* __restrict__ L, int* __restrict__ ucnt,
@@ -451,33 +501,62 @@ __global__ void __launch_bounds__(UP_WARPS * 32)
                 if (lane + o < 32) incl += t;
             }
             ucnt[v * NBKT + lane] = incl;
-            if (lane >= PR_K0 && lane < PR_K0 + PR_NK) pr->uc[lane - PR_K0] = uint16_t(incl);
+            if (lane >= PR_K0 && lane < PR_K0 + PR_NK)
+                pr->uc[lane - PR_K0] = uint16_t(min(incl, PR_FULL));
             __syncwarp();
             h[lane] = incl - c;
             __syncwarp();
-            for (int i = lane; i < nbuf; i += 32) {
-                const int pos = atomicAdd(&h[s_b[warp][i]], 1);
-                L[int64_t(u0) + pos] = s_w[warp][i];
+            for (int i0 = 0; i0 < nbuf; i0 += 32) {
+                const int i = i0 + lane;
+                const bool act = i < nbuf;
+                const int pos = stable_slot(h, act, act ? int(s_b[warp][i]) : 0);
+                if (act) L[int64_t(u0) + pos] = s_w[warp][i];
             }
             __syncwarp();
             continue;
         }
         const int64_t j0 = r0 >> 5, j1 = (r1 - 1) >> 5;
+        // Long rows: lanes read 32 class words at a time; every word with UP
+        // bits is then taken by the whole warp (lane = bit), so entries are
+        // visited in row order with coalesced loads and a hub row with few UP
+        // entries costs d/1024 iterations.
+        auto up_words = [&](auto&& visit) {
+            for (int64_t jb = j0; jb <= j1; jb += 32) {
+                const int64_t j = jb + lane;
+                uint32_t m = 0;
+                if (j <= j1) {
+                    m = cls[j].y;
+                    if (j == j0) m &= ~0u << (r0 & 31);
+                    if (j == j1 && ((r1 & 31) != 0)) m &= (1u << (r1 & 31)) - 1u;
+                }
+                unsigned nzw = __ballot_sync(0xffffffffu, m != 0);
+                while (nzw) {  // up to UPW words per round, their loads in flight together
+                    constexpr int UPW = TCB_UPW;
+                    int sl[UPW], w[UPW], b[UPW];
+                    uint32_t upm = 0;  // bit q: this lane's entry of word q is UP
+#pragma unroll
+                    for (int q = 0; q < UPW; ++q) {
+                        sl[q] = 0;
+                        if (nzw) {  // warp-uniform
+                            sl[q] = __ffs(nzw) - 1;
+                            nzw &= nzw - 1;
+                            upm |= ((__shfl_sync(0xffffffffu, m, sl[q]) >> lane) & 1u) << q;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < UPW; ++q)
+                        w[q] = (upm >> q) & 1u ? nb[(jb + sl[q]) * 32 + lane] : 0;
+#pragma unroll
+                    for (int q = 0; q < UPW; ++q) b[q] = (upm >> q) & 1u ? int(dbk[w[q]]) : 0;
+#pragma unroll
+                    for (int q = 0; q < UPW; ++q) visit(((upm >> q) & 1u) != 0, w[q], b[q]);
+                }
+            }
+        };
         // pass 1: bucket histogram
-        for (int64_t jb = j0; jb <= j1; jb += 32) {
-            const int64_t j = jb + lane;
-            uint32_t m = 0;
-            if (j <= j1) {
-                m = cls[j].y;
-                if (j == j0) m &= ~0u << (r0 & 31);
-                if (j == j1 && ((r1 & 31) != 0)) m &= (1u << (r1 & 31)) - 1u;
-            }
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                atomicAdd(&h[dbk[nb[j * 32 + b]]], 1);
-            }
-        }
+        up_words([&](bool up, int, int b) {
+            if (up) atomicAdd(&h[b], 1);
+        });
         __syncwarp();
         // buckets descending: start[k] = entries in buckets > k
         const int c = h[lane];
@@ -488,27 +567,16 @@ __global__ void __launch_bounds__(UP_WARPS * 32)
             if (lane + o < 32) incl += t;
         }
         ucnt[v * NBKT + lane] = incl;
-        if (lane >= PR_K0 && lane < PR_K0 + PR_NK) pr->uc[lane - PR_K0] = uint16_t(incl);
+        if (lane >= PR_K0 && lane < PR_K0 + PR_NK)
+            pr->uc[lane - PR_K0] = uint16_t(min(incl, PR_FULL));
         __syncwarp();
         h[lane] = incl - c;
         __syncwarp();
-        // pass 2: scatter
-        for (int64_t jb = j0; jb <= j1; jb += 32) {
-            const int64_t j = jb + lane;
-            uint32_t m = 0;
-            if (j <= j1) {
-                m = cls[j].y;
-                if (j == j0) m &= ~0u << (r0 & 31);
-                if (j == j1 && ((r1 & 31) != 0)) m &= (1u << (r1 & 31)) - 1u;
-            }
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                const int w = nb[j * 32 + b];
-                const int pos = atomicAdd(&h[dbk[w]], 1);
-                L[int64_t(u0) + pos] = w;
-            }
-        }
+        // pass 2: stable scatter (row order within each bucket)
+        up_words([&](bool up, int w, int b) {
+            const int pos = stable_slot(h, up, b);
+            if (up) L[int64_t(u0) + pos] = w;
+        });
         __syncwarp();
     }
 }
@@ -673,7 +741,7 @@ __global__ void __launch_bounds__(256)
         for (int64_t p = item.y; p < item.z; ++p) {
             const int y = P[p];
             const int64_t y0 = ls.ob(y), y1 = ls.ob(y + 1), y2 = ls.ub(y);
-            const int64_t y3 = y2 + ls.up_prefix(y, kx);
+            const int64_t y3 = y2 + (nx > no ? ls.up_cut(y, kx, x) : 0);
             for (int64_t j = y0; j < y1; ++j) {
                 const int w = ls.L[j];
                 bool hit = false;
@@ -797,7 +865,7 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
                 pos[r] = v0.x;
                 cnt[r] = no ? int(ls.vb[y + 1].x - v0.x) : 0;
                 pos[PPL + r] = v0.y;  // the prefix of UP(y) that can be in UP(x)
-                cnt[PPL + r] = nu ? ls.up_prefix(y, kx) : 0;
+                cnt[PPL + r] = nu ? ls.up_cut(y, kx, x) : 0;
             }
             so += cnt[r];
             su += cnt[PPL + r];
@@ -1058,22 +1126,33 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 if (yy[r] < 0) continue;
                 const int y = yy[r];
                 const int* sy = ls.split + int64_t(y) * (F + 1);
-                // the record's header and the word holding uc[kx - PR_K0]: one sector
+                // the record's header and the words holding uc[kx], uc[kx + 1]: one sector
                 const uint32_t* rw = reinterpret_cast<const uint32_t*>(ls.prec + y);
                 const uint4 hd = *reinterpret_cast<const uint4*>(rw);  // ob, ub, noff, uc[0..1]
-                const bool in_rec = kx >= PR_K0 && kx < PR_K0 + PR_NK;
-                const int ui = kx - PR_K0;
-                const uint32_t uw = in_rec ? rw[3 + (ui >> 1)] : 0u;
                 // range ends at 0 / F come from the record, not the split row
                 const int a = q0 > 0 ? sy[q0] : 0;
                 const int b = q1 == F ? int(hd.z) : sy[q1];
                 s_pos[t] = hd.x + uint32_t(a);
                 s_len[t] = no ? b - a : 0;
-                // the prefix of UP(y) that can be in UP(x) (degree >= 2^kx)
+                // the prefix of UP(y) that can be in UP(x): ranked above x
                 s_pos[PC + t] = hd.y;
-                s_len[PC + t] = !ns ? 0
-                                : in_rec ? int((uw >> ((ui & 1) * 16)) & 0xFFFFu)
-                                         : ls.up_prefix(y, kx);
+                int ucut = 0;
+                if (ns) {
+                    int hi, lo;
+                    const int ui = kx - PR_K0;
+                    if (ui >= 0 && ui + 1 < PR_NK) {
+                        hi = int((rw[3 + (ui >> 1)] >> ((ui & 1) * 16)) & 0xFFFFu);
+                        lo = int((rw[3 + ((ui + 1) >> 1)] >> (((ui + 1) & 1) * 16)) & 0xFFFFu);
+                    } else {
+                        hi = lo = PR_FULL;
+                    }
+                    if (hi == PR_FULL || lo == PR_FULL) {  // outside the record
+                        hi = ls.ucnt[int64_t(y) * NBKT + kx];
+                        lo = kx + 1 < NBKT ? ls.ucnt[int64_t(y) * NBKT + kx + 1] : 0;
+                    }
+                    ucut = ls.up_cut(hd.y, lo, hi, x);
+                }
+                s_len[PC + t] = ucut;
 #ifdef TCB_NOUPSTREAM  // measurement-only: drop the UP slices
                 s_len[PC + t] = 0;
 #endif

@@ -207,7 +207,9 @@ def device_graph(g, device=None) -> DeviceGraph:
     import torch
     if isinstance(g, DeviceGraph):
         return g
-    dg = g._device
+    # any object with the reference Graph's fields works (the reference's own
+    # tricount.Graph included); the device copy is cached when it can be
+    dg = getattr(g, "_device", None)
     if dg is not None and (device is None or dg.device == torch.device(device)):
         return dg
     ctx = _lib.context(torch.device(device).index if device is not None else None)
@@ -218,7 +220,10 @@ def device_graph(g, device=None) -> DeviceGraph:
     src = torch.empty(max(2 * g.m, 1), dtype=torch.int32, device=dev)
     ctx.check(ctx.lib.tcb_csr_rows(ctx.h, _lib.ptr(row), g.n, _lib.ptr(src)))
     dg = DeviceGraph(n=g.n, m=g.m, row_offsets=row, neighbors=nb, src=src[: 2 * g.m])
-    object.__setattr__(g, "_device", dg)
+    try:
+        object.__setattr__(g, "_device", dg)
+    except (AttributeError, TypeError):  # __slots__ without the field
+        pass
     return dg
 
 

@@ -54,7 +54,8 @@ def _partials(case, rank, world):
                 if level[w] != level[a]:
                     c1 += 1
                     t += 1
-                elif deg[w] > deg[x] or (deg[w] == deg[x] and w < x):
+                elif tdist.ranks_above(w, tdist.degree_bucket(deg[w]), x,
+                                       tdist.degree_bucket(deg[x])):
                     # a same-level triangle is kept at the edge whose apex
                     # ranks above both endpoints (intersect.cu); the device
                     # tallies c2 in the reference's units (3 per triangle)
@@ -90,9 +91,11 @@ def test_gloo_world2_shards_sum_to_reference():
 
 
 def test_owner_rule():
-    u = np.array([1, 5, 3]); v = np.array([2, 4, 9])
-    du = np.array([3, 7, 2]); dv = np.array([3, 1, 5])
-    assert tdist.owner_of(u, v, du, dv).tolist() == [1, 5, 9]
+    # degree bucket floor(log2 d) first, ties (same bucket) to the lower id:
+    # (6, 8) with degrees 5 and 7 share bucket 2, so 6 owns it
+    u = np.array([1, 5, 3, 6]); v = np.array([2, 4, 9, 8])
+    du = np.array([3, 7, 2, 5]); dv = np.array([3, 1, 5, 7])
+    assert tdist.owner_of(u, v, du, dv).tolist() == [1, 5, 9, 6]
     # tiny owners shard by id; warp-tier blocks of 64 and CTA-tier blocks of
     # 1024 partners rotate over the ranks
     own = np.array([4, 5, 7, 7, 7, 9, 9])
