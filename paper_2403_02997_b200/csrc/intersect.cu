@@ -432,7 +432,19 @@ constexpr int UP_WARPS = 8;
 // id-sorted.  h[b] = next free position of bucket b.
 __device__ __forceinline__ int stable_slot(int* h, bool act, int b) {
     const int lane = int(lane_id());
+#ifndef TCB_SLOT_BALLOT
     const unsigned peers = __match_any_sync(0xffffffffu, act ? b : NBKT + lane);
+#else
+    // lanes with the same bucket: five ballots over its bits (NBKT = 32)
+    unsigned peers = __ballot_sync(0xffffffffu, act);
+    if (!act) peers = 1u << lane;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const bool bk = (b >> k) & 1;
+        const unsigned v = __ballot_sync(0xffffffffu, bk);
+        if (act) peers &= bk ? v : ~v;
+    }
+#endif
     const int leader = __ffs(peers) - 1;
     int base = 0;
     if (act && lane == leader) {
@@ -458,22 +470,43 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
     int* h = s_h[warp];
     const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t v = gw; v < n; v += nwarps) {
-        const int64_t r0 = row[v], r1 = row[v + 1];
-        if (r1 == r0) continue;
-        const uint2 b0 = vb[v], b1 = vb[v + 1];
-        const uint32_t u0 = b0.y, nup = b1.y - u0;
+    for (int64_t vbase = gw * 32; vbase < n; vbase += nwarps * 32) {
+        // A lane per row first: bounds and records for 32 rows at once; rows
+        // without UP entries (isolated vertices included) end here, and the
+        // warp takes the others one by one.
+        const int64_t lv = vbase + lane;
+        int64_t lr0 = 0, lr1 = 0;
+        uint2 lb0 = make_uint2(0, 0), lb1 = lb0;
+        if (lv < n) {
+            lr0 = row[lv];
+            lr1 = row[lv + 1];
+            lb0 = vb[lv];
+            lb1 = vb[lv + 1];
+        }
+        const bool live = lv < n && lr1 > lr0;
+        if (live) {
+            PRec* pr = prec + lv;
+            pr->ob = lb0.x;
+            pr->ub = lb0.y;
+            pr->noff = lb1.x - lb0.x;
+            if (lb1.y == lb0.y) {  // no UP entries: zero prefix counts
+                int4* uc4 = reinterpret_cast<int4*>(ucnt + lv * NBKT);
+#pragma unroll
+                for (int q = 0; q < NBKT / 4; ++q) uc4[q] = make_int4(0, 0, 0, 0);
+#pragma unroll
+                for (int q = 0; q < PR_NK; ++q) pr->uc[q] = 0;
+            }
+        }
+        unsigned work = __ballot_sync(0xffffffffu, live && lb1.y != lb0.y);
+        while (work) {
+        const int src = __ffs(work) - 1;
+        work &= work - 1;
+        const int64_t v = vbase + src;
+        const int64_t r0 = __shfl_sync(0xffffffffu, lr0, src);
+        const int64_t r1 = __shfl_sync(0xffffffffu, lr1, src);
+        const uint32_t u0 = __shfl_sync(0xffffffffu, lb0.y, src);
+        const uint32_t nup = __shfl_sync(0xffffffffu, lb1.y, src) - u0;
         PRec* pr = prec + v;
-        if (lane == 0) {
-            pr->ob = b0.x;
-            pr->ub = b0.y;
-            pr->noff = b1.x - b0.x;
-        }
-        if (nup == 0) {
-            ucnt[v * NBKT + lane] = 0;
-            if (lane >= PR_K0 && lane < PR_K0 + PR_NK) pr->uc[lane - PR_K0] = 0;
-            continue;
-        }
         h[lane] = 0;
         __syncwarp();
         if (r1 - r0 <= UP_SHORT) {
@@ -578,6 +611,7 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
             if (up) L[int64_t(u0) + pos] = w;
         });
         __syncwarp();
+        }
     }
 }
 
@@ -865,7 +899,10 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
                 pos[r] = v0.x;
                 cnt[r] = no ? int(ls.vb[y + 1].x - v0.x) : 0;
                 pos[PPL + r] = v0.y;  // the prefix of UP(y) that can be in UP(x)
-                cnt[PPL + r] = nu ? ls.up_cut(y, kx, x) : 0;
+                // the whole bucket-kx run: over-streams the ids above x in
+                // it (no false hits: they are not in UP(x)), which costs this
+                // tier less than a search per partner
+                cnt[PPL + r] = nu ? ls.ucnt[int64_t(y) * NBKT + kx] : 0;
             }
             so += cnt[r];
             su += cnt[PPL + r];
@@ -938,13 +975,13 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
                                             int nseg, int k0, int c0, int c1, int tsup,
                                             const Probe& h, uint32_t& co, uint32_t& cs) {
     constexpr int J = CHUNK / 32;
-    int k = k0;
-    int nx = s_seg[k + 1].x;
-    uint32_t base = uint32_t(s_seg[k].y);
     const int i0 = c0 + int(lane_id());
     // this lane's elements j >= jt come from UP slices (stream index >= tsup)
     const int jt = min(J, max(0, (tsup - i0 + 31) >> 5));
     int w[J];
+    int k = k0;
+    int nx = s_seg[k + 1].x;
+    uint32_t base = uint32_t(s_seg[k].y);
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int i = i0 + 32 * j;
