@@ -161,6 +161,11 @@ struct BucketHash {
             b = (b + 1) & bmask;
         }
     }
+    // two-step probe interface shared with CuckooHash (probe_all); a negative
+    // key would match EMPTY, so callers skip padding keys
+    static constexpr bool kNegSafe = false;
+    __device__ __forceinline__ uint32_t first(int) const { return 0u; }
+    __device__ __forceinline__ uint32_t second(int key, uint32_t) const { return hit(key); }
     // The first bucket is resolved without branches; the loop runs only when
     // that bucket is full and does not hold the key (rare at load <= 1/4).
     __device__ __forceinline__ uint32_t hit(int key) const {
@@ -187,6 +192,7 @@ struct BucketHash {
 // chain longer than CUCKOO_KICKS reports failure and the caller falls back
 // to the bucket table (rare at the CTA tier's load <= 3/8).
 constexpr int CUCKOO_KICKS = 64;
+constexpr uint32_t C_EMPTY = 0x7FFFFFFFu;  // cuckoo empty slot: never an id (ids < 2^31 - 1)
 
 struct CuckooHash {
     uint32_t* tab;   // table 1: tab[0, half); table 2: tab[half, 2 half)
@@ -205,20 +211,26 @@ struct CuckooHash {
         uint32_t* slot = tab + h1(e);
         for (int it = 0; it < CUCKOO_KICKS; ++it) {
             const uint32_t old = atomicExch(slot, e);
-            if (old == EMPTY) return true;
+            if (old == C_EMPTY) return true;
             e = old;  // carry the evicted key to its slot in the other table
             slot = slot < tab2 ? tab2 + h2(e) : tab + h1(e);
         }
         return false;
     }
-    // key >= 0, so EMPTY never matches
-    __device__ __forceinline__ uint32_t hit(int key) const {
-#ifdef TCB_NOPROBE  // measurement-only variant: stream without probing
-        return uint32_t(key) == 0x7FFFFFFEu;
-#endif
+    // Two-step probe (probe_all issues a batch of first() reads before any
+    // second()).  C_EMPTY is never an id and a negative (padding) key never
+    // matches a slot, so no guard is needed.
+    static constexpr bool kNegSafe = true;
+    __device__ __forceinline__ uint32_t first(int key) const { return tab[h1(uint32_t(key))]; }
+    // Both reads are independent: a key sits in table 1 or table 2.  (A
+    // table-1 flag telling which misses can skip table 2 cut shared-memory
+    // wavefronts by a third, but the dependent second read made the kernel
+    // 1.25-2x slower: DESIGN.md §8.)
+    __device__ __forceinline__ uint32_t second(int key, uint32_t v) const {
         const uint32_t k = uint32_t(key);
-        return (tab[h1(k)] == k) | (tab2[h2(k)] == k);
+        return (v == k) | (tab2[h2(k)] == k);
     }
+    __device__ __forceinline__ uint32_t hit(int key) const { return second(key, first(key)); }
 };
 
 // c1 / same-level tallies.  `sup` counts UP∩UP hits: each all-horizontal
@@ -943,35 +955,77 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
     tl.flush(C);
 }
 
+#ifdef TCB_STATS  // measurement-only: CTA-tier work counters, printed per call
+__device__ unsigned long long g_cta_stats[8];  // items, passes, slices, elements, chunks, fast
+#define TCB_STAT(i, v) atomicAdd(&g_cta_stats[i], (unsigned long long)(v))
+#else
+#define TCB_STAT(i, v) ((void)0)
+#endif
+
 // ---------------------------------------------------------------------------
 // 6. CTA tier
 //
 // Every partner t has two unread slices, OFF at index t and UP at PC + t
 // (s_pos / s_len).  Each pass takes a count from every slice, and the
-// non-empty ones are compacted into the stream table s_seg: all OFF slices
+// non-empty ones are compacted into the stream table (SegTab): all OFF slices
 // first, then all UP slices, so an element's class is just
-// (stream index >= tsup) and a walk never steps over an empty slice.
-// s_seg[k] = (first stream index of slice k, its base): element i of slice k
-// is L[base + i] (uint32 arithmetic; 2m < 2^32).
+// (stream index >= tsup) and a walk never steps over an empty slice
+// (uint32 list arithmetic; 2m < 2^32).
 
-// Largest k < nseg with s_seg[k].x <= c0 (s_seg[0].x = 0 <= c0): two 32-way
-// ballots over a 2048-entry table and one compare.
-__device__ __forceinline__ int find_segment(const int2* s_seg, int nseg, int c0) {
+// The stream table lives in two int arrays (start[k] = first stream index of
+// slice k, base[k] = its base: element i of slice k is L[base[k] + i]), so
+// strided and consecutive reads of the starts hit distinct banks.
+struct SegTab {
+    int* start;      // NSEG + 1 (start[nseg] = total)
+    uint32_t* base;  // NSEG + 1
+};
+
+// Largest k < nseg with start[k] <= c0 (start[0] = 0 <= c0).  Level 1 samples
+// every 65th start (lane * 65 -> 32 distinct banks), level 2 the 64 starts
+// after the chosen sample in two consecutive 32-wide reads: three ballots,
+// no bank conflicts.
+__device__ __forceinline__ int find_segment(const int* start, int nseg, int c0) {
     const int lane = int(lane_id());
-    const int j = lane * 64;
-    const unsigned b1 = __ballot_sync(0xffffffffu, j < nseg && s_seg[j].x <= c0);
-    const int kb = (31 - __clz(b1)) * 64;
-    const int j2 = kb + lane * 2;
-    const unsigned b2 = __ballot_sync(0xffffffffu, j2 < nseg && s_seg[j2].x <= c0);
-    const int k = kb + 2 * (31 - __clz(b2));
-    return k + ((k + 1 < nseg && s_seg[k + 1].x <= c0) ? 1 : 0);
+    const int j = lane * 65;
+    const unsigned b1 = __ballot_sync(0xffffffffu, j < nseg && start[j] <= c0);
+    const int kb = (31 - __clz(b1)) * 65;
+    const int ja = kb + 1 + lane, jb = kb + 33 + lane;
+    const unsigned ba = __ballot_sync(0xffffffffu, ja < nseg && start[ja] <= c0);
+    const unsigned bb = __ballot_sync(0xffffffffu, jb < nseg && start[jb] <= c0);
+    return bb ? kb + 33 + (31 - __clz(bb)) : ba ? kb + 1 + (31 - __clz(ba)) : kb;
+}
+static_assert(31 * 65 + 64 >= NSEG - 1, "find_segment covers NSEG slices");
+
+// Probe w[0..J): all += hits, sup += hits of elements j >= jt (UP).  The
+// first-step reads of a batch of B keys are issued before any second step.
+template <int J, bool GUARD, typename Probe>
+__device__ __forceinline__ void probe_all(const Probe& h, int (&w)[J], int jt,
+                                          uint32_t& all, uint32_t& sup) {
+#ifndef TCB_PROBE_B
+#define TCB_PROBE_B 8
+#endif
+    constexpr int B = TCB_PROBE_B;
+#pragma unroll
+    for (int j0 = 0; j0 < J; j0 += B) {
+        uint32_t v[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) v[q] = h.first(w[j0 + q]);
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            const int j = j0 + q;
+            if (GUARD && !Probe::kNegSafe && w[j] < 0) continue;
+            const uint32_t hv = h.second(w[j], v[q]);
+            all += hv;
+            sup += j >= jt ? hv : 0u;
+        }
+    }
 }
 
 // A chunk that crosses slice boundaries: each lane walks forward from the
 // chunk's first slice k0; a lane crosses a boundary in few of its J
 // elements.  FULL: the chunk holds CHUNK elements (no bounds checks).
 template <bool FULL, typename Probe>
-__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const int2* s_seg,
+__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const SegTab& sg,
                                             int nseg, int k0, int c0, int c1, int tsup,
                                             const Probe& h, uint32_t& co, uint32_t& cs) {
     constexpr int J = CHUNK / 32;
@@ -980,8 +1034,8 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
     const int jt = min(J, max(0, (tsup - i0 + 31) >> 5));
     int w[J];
     int k = k0;
-    int nx = s_seg[k + 1].x;
-    uint32_t base = uint32_t(s_seg[k].y);
+    int nx = sg.start[k + 1];
+    uint32_t base = sg.base[k];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int i = i0 + 32 * j;
@@ -991,9 +1045,9 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
                 do {
                     TCB_DASSERT(k + 1 < nseg);
                     ++k;
-                    nx = s_seg[k + 1].x;
+                    nx = sg.start[k + 1];
                 } while (nx <= i);
-                base = uint32_t(s_seg[k].y);
+                base = sg.base[k];
             }
 #ifdef TCB_NOLOAD  // measurement-only variant: probe without streaming
             w[j] = int(((base + uint32_t(i)) * 2654435761u) >> 8);
@@ -1003,13 +1057,7 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
         }
     }
     uint32_t all = 0, sup = 0;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-        if (!FULL && w[j] < 0) continue;
-        const uint32_t hv = h.hit(w[j]);
-        all += hv;
-        sup += j >= jt ? hv : 0u;
-    }
+    probe_all<J, !FULL>(h, w, jt, all, sup);
     co += all - sup;
     cs += sup;
 }
@@ -1018,7 +1066,7 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
 // inside one slice takes a warp-uniform fast path with coalesced loads and
 // no per-element bookkeeping.
 template <typename Probe>
-__device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, const int2* s_seg,
+__device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, const SegTab& sg,
                                               int nseg, int total, int tsup, int* s_next,
                                               const Probe& h, Tally& tl) {
     constexpr int J = CHUNK / 32;
@@ -1030,15 +1078,20 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, con
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (c0 >= total) break;
         const int c1 = min(total, c0 + CHUNK);
-        const int k0 = find_segment(s_seg, nseg, c0);
-        TCB_DASSERT(k0 >= 0 && k0 < nseg && s_seg[k0].x <= c0 && c0 < s_seg[k0 + 1].x);
+        const int k0 = find_segment(sg.start, nseg, c0);
+        const int e1 = sg.start[k0 + 1];
+        if (lane == 0) {
+            TCB_STAT(4, 1);
+            TCB_STAT(5, e1 >= c1 ? 1 : 0);
+        }
+        TCB_DASSERT(k0 >= 0 && k0 < nseg && sg.start[k0] <= c0 && c0 < e1);
         uint32_t co = 0, cs = 0;
-        if (s_seg[k0 + 1].x >= c1) {
+        if (e1 >= c1) {
             // fast path: one slice
-            const uint32_t base = uint32_t(s_seg[k0].y) + uint32_t(c0 + lane);
+            const uint32_t base = sg.base[k0] + uint32_t(c0 + lane);
             const int32_t* p = L + base;
             int w[J];
-            uint32_t hits = 0;
+            uint32_t hits = 0, dummy = 0;
             if (c1 - c0 == CHUNK) {
 #ifdef TCB_NOLOAD
 #pragma unroll
@@ -1047,22 +1100,17 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, con
 #pragma unroll
                 for (int j = 0; j < J; ++j) w[j] = p[32 * j];
 #endif
-#pragma unroll
-                for (int j = 0; j < J; ++j) hits += h.hit(w[j]);
+                            probe_all<J, false>(h, w, J, hits, dummy);
             } else {
 #pragma unroll
                 for (int j = 0; j < J; ++j) w[j] = c0 + lane + 32 * j < c1 ? p[32 * j] : -1;
-#pragma unroll
-                for (int j = 0; j < J; ++j) {
-                    if (w[j] < 0) continue;
-                    hits += h.hit(w[j]);
-                }
+                            probe_all<J, true>(h, w, J, hits, dummy);
             }
             if (c0 >= tsup) cs = hits; else co = hits;
         } else if (c1 - c0 == CHUNK) {
-            cross_chunk<true>(L, s_seg, nseg, k0, c0, c1, tsup, h, co, cs);
+            cross_chunk<true>(L, sg, nseg, k0, c0, c1, tsup, h, co, cs);
         } else {
-            cross_chunk<false>(L, s_seg, nseg, k0, c0, c1, tsup, h, co, cs);
+            cross_chunk<false>(L, sg, nseg, k0, c0, c1, tsup, h, co, cs);
         }
         tl.c1 += co;
         tl.sup += cs;
@@ -1112,8 +1160,10 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 DevCounters* C, int hc, int dbg, const int2* __restrict__ vinfo, int fwd) {
     extern __shared__ uint4 smem4[];
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS
-    int2* s_seg = reinterpret_cast<int2*>(tab + C_SLOTS);         // NSEG + 1 (stream table)
-    uint32_t* s_pos = reinterpret_cast<uint32_t*>(s_seg + NSEG + 1);  // NSEG: next unread position
+    SegTab sg;                                                    // stream table
+    sg.start = reinterpret_cast<int*>(tab + C_SLOTS);             // NSEG + 1
+    sg.base = reinterpret_cast<uint32_t*>(sg.start + NSEG + 1);   // NSEG + 1
+    uint32_t* s_pos = sg.base + NSEG + 1;                         // NSEG: next unread position
     int* s_len = reinterpret_cast<int*>(s_pos + NSEG);            // NSEG: unread length
     __shared__ int64_t s_ta[C_THREADS / 32 + 1];
     __shared__ int s_tb[C_THREADS / 32 + 1];
@@ -1215,7 +1265,7 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 TCB_DASSERT(len >= 1 && len <= HC);
                 BucketHash h;
                 h.setup(tab, C_SLOTS);
-                for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = EMPTY;
+                for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = C_EMPTY;
                 if (threadIdx.x == 0) {
                     s_next = 0;
                     s_fail = 0;
@@ -1280,6 +1330,13 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 const int total = tsup + int(to >> 32);
                 const int noff = tn & 0xFFFF;
                 const int nseg = noff + (tn >> 16);
+                if (threadIdx.x == 0) {
+                    TCB_STAT(1, 1);
+                    TCB_STAT(2, nseg);
+                    TCB_STAT(3, total);
+                    TCB_STAT(6, tn >> 16);
+                    TCB_STAT(7, int(to >> 32));
+                }
                 {
                     int e_o = int(eo & 0xFFFFFFFF), e_s = tsup + int(eo >> 32);
                     int n_o = en & 0xFFFF, n_s = noff + (en >> 16);
@@ -1290,7 +1347,9 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         const int k = slot[r];
                         const bool isup = r >= 2;
                         const int e = isup ? e_s : e_o;
-                        s_seg[isup ? n_s : n_o] = make_int2(e, int(s_pos[k] - uint32_t(e)));
+                        const int q = isup ? n_s : n_o;
+                        sg.start[q] = e;
+                        sg.base[q] = s_pos[k] - uint32_t(e);
                         if (consume) {
                             s_pos[k] += uint32_t(c);
                             s_len[k] -= c;
@@ -1303,7 +1362,10 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                             ++n_o;
                         }
                     }
-                    if (threadIdx.x == 0) s_seg[nseg] = make_int2(total, 0);
+                    if (threadIdx.x == 0) {
+                        sg.start[nseg] = total;
+                        sg.base[nseg] = 0;
+                    }
                 }
                 __syncthreads();
                 if (s_fail) {  // rare: rebuild this sub-chunk as a bucket table
@@ -1316,8 +1378,8 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                     __syncthreads();
                 }
                 if (!(dbg & 1)) {
-                    if (!s_fail) stream_chunks(L, s_seg, nseg, total, tsup, &s_next, ch, tl);
-                    else stream_chunks(L, s_seg, nseg, total, tsup, &s_next, h, tl);
+                    if (!s_fail) stream_chunks(L, sg, nseg, total, tsup, &s_next, ch, tl);
+                    else stream_chunks(L, sg, nseg, total, tsup, &s_next, h, tl);
                 }
                 __syncthreads();
             }
@@ -1450,6 +1512,19 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
                debug_flags() | ctx->test_flags,
                (const int2*)vinfo, fwd);
     ctx->record(6);
+#ifdef TCB_STATS
+    {
+        unsigned long long st[8];
+        TCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        TCB_CUDA(cudaMemcpyFromSymbol(st, g_cta_stats, sizeof(st)));
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        TCB_CUDA(cudaMemcpyToSymbol(g_cta_stats, z, sizeof(z)));
+        unsigned long long nci = 0;
+        TCB_CUDA(cudaMemcpy(&nci, nc, sizeof(nci), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "CTA stats: items %llu passes %llu slices %llu (UP %llu) elements %llu (UP %llu) "
+                "chunks %llu fast %llu\n", nci, st[1], st[2], st[6], st[3], st[7], st[4], st[5]);
+    }
+#endif
     TCB_LAUNCH(ctx, k_isect_warp, ctx->isect_warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
                (const unsigned long long*)nw, ls, (const int32_t*)P, fw, C, (const int2*)vinfo,
                fwd);
