@@ -37,7 +37,7 @@ extern "C" {
 
 #define TCB_API __attribute__((visibility("default")))
 
-#define TCB_VERSION 4
+#define TCB_VERSION 5
 
 enum {
     TCB_OK = 0,
@@ -143,6 +143,15 @@ TCB_API int tcb_csr_build(tcb_context* ctx, const int64_t* d_pairs, int64_t k,
                           int64_t n, int64_t* d_row_offsets, int32_t* d_neighbors,
                           int32_t* d_src, int32_t* d_edge_u, int32_t* d_edge_v,
                           int64_t* m_out);
+
+/* Host -> device copy of `bytes` bytes that is fast from PAGEABLE memory
+ * too (numpy arrays, the reference Graph's frozen CSR): pinned sources are
+ * one DMA; pageable ones go through a ring of pinned staging buffers, the
+ * host threads filling chunk i+1 while chunk i is in flight.  Returns after
+ * the copy has landed.  Replaces the upload a ctypes binding would do before
+ * calling the device entries (graph.py device_graph). */
+TCB_API int tcb_copy_to_device(tcb_context* ctx, void* d_dst, const void* h_src,
+                               int64_t bytes);
 
 /* src (per-entry row id) of a CSR: d_src[row[v]..row[v+1]) = v. */
 TCB_API int tcb_csr_rows(tcb_context* ctx, const int64_t* d_row_offsets, int64_t n,

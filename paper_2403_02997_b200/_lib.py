@@ -79,6 +79,7 @@ def load_library(path: Path | None = None):
             "tcb_lattice_generate": ([vp, i64, vp], i32),
             "tcb_csr_build": ([vp, vp, i64, i64, vp, vp, vp, vp, vp, pi64], i32),
             "tcb_csr_rows": ([vp, vp, i64, vp], i32),
+            "tcb_copy_to_device": ([vp, vp, vp, i64], i32),
             "tcb_csr_edges": ([vp, vp, vp, i64, i64, vp, vp], i32),
             "tcb_bfs_levels": ([vp, vp, vp, vp, i64, i64, vp, pi64, pi64], i32),
             "tcb_bfs_parent": ([vp, vp, vp, i64, vp, i64, vp], i32),

@@ -4,6 +4,7 @@
 // kept on the context (tcb_last_error).  The fused driver mirrors tc_cetc
 // (sequential.py:164-168): bfs_label -> cover edges -> intersection, all
 // stream-ordered with a single host synchronisation at the end.
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -169,6 +170,10 @@ TCB_API int tcb_context_destroy(tcb_context* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->copy_ev)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < Context::NSTAGE; ++i) {
+        if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+        if (ctx->stage_buf[i]) cudaFreeHost(ctx->stage_buf[i]);
+    }
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     delete ctx;
     return TCB_OK;
@@ -493,6 +498,77 @@ TCB_API int tcb_cetc_shard(tcb_context* ctx, const int64_t* d_row_offsets,
     });
 }
 
+static void ensure_copy_stream(Context* ctx) {
+    if (ctx->copy_stream) return;
+    TCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->copy_ev) TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// Host -> device on ctx->copy_stream (ordered after the work already queued
+// on ctx->stream).  Pinned source: one DMA.  Pageable source: chunks go
+// through a ring of NSTAGE pinned buffers; all host threads (OpenMP) copy
+// chunk i+1 into its buffer while chunk i's DMA runs, so the transfer runs
+// at min(host memcpy, PCIe) instead of the driver's serial staging.  The
+// caller orders later work after ctx->copy_ev[1].
+static void stage_h2d(Context* ctx, void* d_dst, const void* h_src, int64_t bytes) {
+    ensure_copy_stream(ctx);
+    TCB_CUDA(cudaEventRecord(ctx->copy_ev[0], ctx->stream));
+    TCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[0], 0));
+    constexpr int64_t CH = int64_t(32) << 20;  // 32 MB chunks
+    if (bytes <= CH || is_pinned(h_src)) {
+        TCB_CUDA(cudaMemcpyAsync(d_dst, h_src, size_t(bytes), cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+        TCB_CUDA(cudaEventRecord(ctx->copy_ev[1], ctx->copy_stream));
+        return;
+    }
+    for (int i = 0; i < Context::NSTAGE; ++i) {
+        if (!ctx->stage_buf[i]) {
+            TCB_CUDA(cudaHostAlloc(&ctx->stage_buf[i], size_t(CH), cudaHostAllocDefault));
+            TCB_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+            TCB_CUDA(cudaEventRecord(ctx->stage_ev[i], ctx->copy_stream));
+        }
+    }
+    const char* src = static_cast<const char*>(h_src);
+    char* dst = static_cast<char*>(d_dst);
+    const int64_t nch = (bytes + CH - 1) / CH;
+    for (int64_t c = 0; c < nch; ++c) {
+        const int b = int(c % Context::NSTAGE);
+        const int64_t off = c * CH, len = std::min(CH, bytes - off);
+        TCB_CUDA(cudaEventSynchronize(ctx->stage_ev[b]));  // buffer b's last DMA is done
+        char* stage = static_cast<char*>(ctx->stage_buf[b]);
+        constexpr int64_t PIECE = int64_t(1) << 20;
+        const int64_t npieces = (len + PIECE - 1) / PIECE;
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < npieces; ++q) {
+            const int64_t o = q * PIECE;
+            std::memcpy(stage + o, src + off + o, size_t(std::min(PIECE, len - o)));
+        }
+        TCB_CUDA(cudaMemcpyAsync(dst + off, stage, size_t(len), cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+        TCB_CUDA(cudaEventRecord(ctx->stage_ev[b], ctx->copy_stream));
+    }
+    TCB_CUDA(cudaEventRecord(ctx->copy_ev[1], ctx->copy_stream));
+}
+
+TCB_API int tcb_copy_to_device(tcb_context* ctx, void* d_dst, const void* h_src, int64_t bytes) {
+    return guarded(ctx, [&] {
+        require(bytes >= 0, "negative size");
+        if (bytes == 0) return;
+        require(d_dst != nullptr && h_src != nullptr, "null pointer");
+        stage_h2d(ctx, d_dst, h_src, bytes);
+        TCB_CUDA(cudaEventSynchronize(ctx->copy_ev[1]));
+    });
+}
+
 // host-buffer entries: upload the CSR, derive src, run the fused path (or a
 // shard of it), download the counters (and levels on request).  The
 // neighbour array (the bulk of the bytes) is copied on a copy stream while
@@ -513,19 +589,9 @@ static int host_entry(tcb_context* ctx, const int64_t* h_row_offsets, const int3
         int64_t* row = ctx->wsT<int64_t>(WS_ROW, n + 1);
         int32_t* nb = ctx->wsT<int32_t>(WS_NB, nnz);
         int32_t* src = ctx->wsT<int32_t>(WS_EDGE_U, nnz);
-        if (nnz) {
-            if (!ctx->copy_stream) {
-                TCB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-                for (auto& e : ctx->copy_ev)
-                    TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            }
-            // the copy may not overtake earlier work on the compute stream
-            TCB_CUDA(cudaEventRecord(ctx->copy_ev[0], ctx->stream));
-            TCB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[0], 0));
-            TCB_CUDA(cudaMemcpyAsync(nb, h_neighbors, sizeof(int32_t) * nnz,
-                                     cudaMemcpyHostToDevice, ctx->copy_stream));
-            TCB_CUDA(cudaEventRecord(ctx->copy_ev[1], ctx->copy_stream));
-        }
+        // the neighbour array on the copy stream (after earlier work on the
+        // compute stream; pageable sources through the pinned staging ring)
+        if (nnz) stage_h2d(ctx, nb, h_neighbors, int64_t(sizeof(int32_t)) * nnz);
         TCB_CUDA(cudaMemcpyAsync(row, h_row_offsets, sizeof(int64_t) * (n + 1),
                                  cudaMemcpyHostToDevice, ctx->stream));
         csr_rows(ctx, row, n, src);

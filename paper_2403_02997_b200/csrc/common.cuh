@@ -123,6 +123,10 @@ struct Context {
     // the entry->row map is built on the compute stream
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_ev[2] = {};
+    // pinned staging ring for copies from pageable host memory (stage_h2d)
+    static constexpr int NSTAGE = 4;
+    void* stage_buf[NSTAGE] = {};
+    cudaEvent_t stage_ev[NSTAGE] = {};
 
     void* ws(Slot s, size_t bytes) {
         if (bytes == 0) bytes = 16;

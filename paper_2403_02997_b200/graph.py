@@ -215,8 +215,15 @@ def device_graph(g, device=None) -> DeviceGraph:
     ctx = _lib.context(torch.device(device).index if device is not None else None)
     dev = torch.device("cuda", ctx.device)
     _check_vertex_count(g.n)
-    row = torch.from_numpy(np.ascontiguousarray(g.row_offsets, dtype=np.int64)).to(dev)
-    nb = torch.from_numpy(np.ascontiguousarray(g.neighbors, dtype=np.int32)).to(dev)
+    # the frozen (pageable) numpy arrays go up through the library's pinned
+    # staging ring (tcb_copy_to_device): host copies overlap the DMA
+    row_h = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
+    nb_h = np.ascontiguousarray(g.neighbors, dtype=np.int32)
+    row = torch.empty(g.n + 1, dtype=torch.int64, device=dev)
+    nb = torch.empty(max(len(nb_h), 1), dtype=torch.int32, device=dev)[: len(nb_h)]
+    ctx.check(ctx.lib.tcb_copy_to_device(ctx.h, _lib.ptr(row), row_h.ctypes.data, row_h.nbytes))
+    if nb_h.nbytes:
+        ctx.check(ctx.lib.tcb_copy_to_device(ctx.h, _lib.ptr(nb), nb_h.ctypes.data, nb_h.nbytes))
     src = torch.empty(max(2 * g.m, 1), dtype=torch.int32, device=dev)
     ctx.check(ctx.lib.tcb_csr_rows(ctx.h, _lib.ptr(row), g.n, _lib.ptr(src)))
     dg = DeviceGraph(n=g.n, m=g.m, row_offsets=row, neighbors=nb, src=src[: 2 * g.m])

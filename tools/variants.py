@@ -18,7 +18,7 @@ CSRC = ROOT / "paper_2403_02997_b200" / "csrc"
 OUT = ROOT / "paper_2403_02997_b200" / "lib" / "variants"
 NVCC = "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "--extended-lambda", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+         "--extended-lambda", "-Xcompiler", "-fPIC,-fvisibility=hidden,-fopenmp",
          f"-I{ROOT / 'include'}"]
 
 
@@ -36,7 +36,7 @@ def build(name: str, defs: str, csrc: Path = CSRC):
             raise SystemExit(f"variant {name}: compile failed")
     lib = OUT / f"libtricount_b200_{name}.so"
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart",
-                    "static", "-o", str(lib), *objs], check=True)
+                    "static", "-Xcompiler", "-fopenmp", "-o", str(lib), *objs], check=True)
     print("built", lib)
 
 
