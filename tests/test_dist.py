@@ -131,3 +131,77 @@ def test_gpu_shards_sum_to_total(world):
         for r, p in enumerate(parts):
             h = tb.ops.cetc_host_shard(case.row, case.nb, case.n, r, world)
             assert (h["c1"], h["c2"], h["triangles"]) == (p.c1, p.c2, -1 if world > 1 else h["triangles"])
+
+
+def _nccl_worker(rank, world, port, out):
+    """One rank per GPU over NCCL: the product's distributed entries, each
+    rank on its own GPU with its own replica of the graph."""
+    import torch
+    import paper_2403_02997_b200 as tb
+    from paper_2403_02997_b200 import dm as tdm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                           device_id=torch.device("cuda", rank))
+    try:
+        res = {}
+        for case in CASES:
+            g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+            dg = tb.device_graph(g, device=rank)
+            res[case.name] = (tdist.tc_cetc_distributed(dg), tdm.cetc_dm_distributed(dg))
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_ranks_sum_to_reference():
+    """SURVEY.md §8(e) on real GPUs: owner-block shards + one 16-byte NCCL
+    all-reduce (tc_cetc_distributed), and the CETC-DM cover-set all-gather +
+    all-reduce (cetc_dm_distributed).  Needs two visible GPUs; the round's
+    GPU box has one, so this skips there."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (one rank per GPU)")
+    world = min(torch.cuda.device_count(), 4)
+    out = mp.Manager().dict()
+    mp.start_processes(_nccl_worker, args=(world, _free_port(), out), nprocs=world,
+                       join=True, start_method="spawn")
+    for case in CASES:
+        for r in range(world):
+            assert out[r][case.name] == (case.T, case.T), (case.name, r)
+
+
+def _gloo_gpu_worker(rank, world, port, out):
+    """The product's distributed entries with a real process group: gloo
+    collectives on CPU tensors, every rank's kernels on cuda:0 (the ranks'
+    kernels never wait on each other; only the host-side all-reduce and
+    all-gather join them)."""
+    import torch
+    import paper_2403_02997_b200 as tb
+    from paper_2403_02997_b200 import dm as tdm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        for case in CASES:
+            g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+            dg = tb.device_graph(g, device=0)
+            res[case.name] = (tdist.tc_cetc_distributed(dg), tdm.cetc_dm_distributed(dg))
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_product_distributed_entries_gloo_world2():
+    """tc_cetc_distributed and cetc_dm_distributed (not a restatement) over a
+    world-2 gloo group, both ranks on one GPU: every rank gets T."""
+    out = mp.Manager().dict()
+    mp.start_processes(_gloo_gpu_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    for case in CASES:
+        assert out[0][case.name] == out[1][case.name] == (case.T, case.T), case.name
