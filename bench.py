@@ -558,7 +558,7 @@ def main():
                             "t_ms": stages["bfs"],
                             "frac": (b_bfs / (stages["bfs"] * 1e-3) / 1e9 / peak
                                      if stages["bfs"] > 0 else None),
-                            "note": "the level-synchronous BFS alone (k_bfs_seed + k_bfs_coop)"},
+                            "note": "the BFS kernels alone (k_bfs_probe + k_bfs_coop, both BFS passes)"},
                         "components_ms": stages["components"]}}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
