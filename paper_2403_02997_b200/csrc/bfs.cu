@@ -141,6 +141,7 @@ __global__ void k_bfs_probe(const int64_t* __restrict__ row, int64_t n,
 #define TCB_BFS_BLOCK 512
 #endif
 constexpr int BFS_BLOCK = TCB_BFS_BLOCK;
+constexpr int BFS_WPB = BFS_BLOCK / 32;
 #ifndef TCB_BFS_ALPHA
 #define TCB_BFS_ALPHA 14
 #endif
@@ -153,6 +154,7 @@ constexpr int BFS_HEAVY = 256;     // top-down: longer lists are split into chun
 #ifndef TCB_BFS_LOWDEG
 #define TCB_BFS_LOWDEG 64
 #endif
+
 constexpr int64_t BFS_LOWDEG = TCB_BFS_LOWDEG;  // td_expand<true> when dmax <= this
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(BFS_BLOCK, 2)
     const int nwarps = gthreads >> 5;
     const unsigned lane = lane_id();
     __shared__ long long s_bc[3];  // per-block broadcast of the level counters
+    __shared__ unsigned long long s_agg[3][BFS_WPB];  // per-warp level counters
 
     int L = 0;
     int nf = int(ld_volatile_u64(&C->q_len[0]));
@@ -392,10 +395,27 @@ __global__ void __launch_bounds__(BFS_BLOCK, 2)
         my_deg = warp_sum(my_deg);
         my_dmax = warp_max_u64(my_dmax);
         my_cnt = warp_sum(my_cnt);
+        // one atomic per block per counter (not per warp): on thin levels
+        // same-address atomics, not work, set the level's length
         if (lane == 0) {
-            if (my_deg) atomicAdd(&C->deg_sum[sn], my_deg);
-            if (my_dmax) atomicMax(&C->deg_max[sn], my_dmax);
-            if (my_cnt) atomicAdd(&C->q_len[sn], my_cnt);
+            s_agg[0][threadIdx.x >> 5] = my_deg;
+            s_agg[1][threadIdx.x >> 5] = my_dmax;
+            s_agg[2][threadIdx.x >> 5] = my_cnt;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int k = int(threadIdx.x);
+            unsigned long long a = k < BFS_WPB ? s_agg[0][k] : 0ull;
+            unsigned long long b = k < BFS_WPB ? s_agg[1][k] : 0ull;
+            unsigned long long c = k < BFS_WPB ? s_agg[2][k] : 0ull;
+            a = warp_sum(a);
+            b = warp_max_u64(b);
+            c = warp_sum(c);
+            if (k == 0) {
+                if (a) atomicAdd(&C->deg_sum[sn], a);
+                if (b) atomicMax(&C->deg_max[sn], b);
+                if (c) atomicAdd(&C->q_len[sn], c);
+            }
         }
 
         grid.sync();
