@@ -635,9 +635,18 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
 // list once; the warp takes a long list (> SPLIT_LONG ids) together, one
 // binary search per boundary.  Rows of empty OFF lists stay zero (memset).
 constexpr int SPLIT_LONG = 256;
-__global__ void k_split_points(int64_t n, const int32_t* __restrict__ L,
-                               const uint2* __restrict__ vb, int rshift, int* __restrict__ split) {
+constexpr int SPLIT_WARPS = 8;
+// A warp per 32 consecutive vertices: every row is built in a shared-memory
+// tile (row stride F + 1 = 33 ints: lanes writing the same column hit
+// distinct banks) and the 32 rows, contiguous in the table, are written out
+// with coalesced stores — every row, so no memset of the table is needed.
+__global__ void __launch_bounds__(SPLIT_WARPS * 32)
+    k_split_points(int64_t n, const int32_t* __restrict__ L, const uint2* __restrict__ vb,
+                   int rshift, int* __restrict__ split) {
+    __shared__ int s_tile[SPLIT_WARPS][32 * (F + 1)];
     const int lane = int(lane_id());
+    int* tile = s_tile[threadIdx.x >> 5];
+    int* my = tile + lane * (F + 1);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < n;
          base += stride) {
@@ -648,14 +657,13 @@ __global__ void k_split_points(int64_t n, const int32_t* __restrict__ L,
             b1 = vb[v + 1].x;
         }
         const int len = int(b1 - b0);
-        if (len > 0 && len <= SPLIT_LONG) {
-            int* sp = split + v * (F + 1);
+        if (len <= SPLIT_LONG) {  // empty rows become all zeros
             int q = 0;
             for (int64_t g = b0; g < b1; ++g) {
                 const int r = L[g] >> rshift;
-                for (; q <= r; ++q) sp[q] = int(g - b0);
+                for (; q <= r; ++q) my[q] = int(g - b0);
             }
-            for (; q <= F; ++q) sp[q] = len;
+            for (; q <= F; ++q) my[q] = len;
         }
         unsigned longs = __ballot_sync(0xffffffffu, len > SPLIT_LONG);
         while (longs) {
@@ -663,7 +671,6 @@ __global__ void k_split_points(int64_t n, const int32_t* __restrict__ L,
             longs &= longs - 1;
             const int64_t lb0 = __shfl_sync(0xffffffffu, b0, src_lane);
             const int64_t lb1 = __shfl_sync(0xffffffffu, b1, src_lane);
-            const int64_t lv = base + src_lane;
             for (int q = lane; q <= F; q += 32) {  // first position with id >= q << rshift
                 const int64_t key = int64_t(q) << rshift;
                 int64_t lo = lb0, hi = lb1;
@@ -671,9 +678,14 @@ __global__ void k_split_points(int64_t n, const int32_t* __restrict__ L,
                     const int64_t mid = (lo + hi) >> 1;
                     if (int64_t(L[mid]) < key) lo = mid + 1; else hi = mid;
                 }
-                split[lv * (F + 1) + q] = int(lo - lb0);
+                tile[src_lane * (F + 1) + q] = int(lo - lb0);
             }
         }
+        __syncwarp();
+        const int64_t rows = min(int64_t(32), n - base);
+        int* out = split + base * (F + 1);
+        for (int k = lane; k < rows * (F + 1); k += 32) out[k] = tile[k];
+        __syncwarp();
     }
 }
 
@@ -1477,14 +1489,12 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_list_bounds, grid_for(ctx, n + 1, 256), 256, 0, row, n, ccls,
                (const unsigned long long*)pre, nwords, vb, bits, (const unsigned long long*)prek,
                seg, seg + n);
-    // rows of empty OFF lists stay zero (k_split_points writes only rows
-    // with entries)
-    TCB_CUDA(cudaMemsetAsync(split, 0, size_t(n) * (F + 1) * sizeof(int), ctx->stream));
     TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
                (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P);
     TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
                (const uint8_t*)dbk, (const uint2*)vb, L, ucnt, prec);
-    TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, n, 256), 256, 0, n, (const int32_t*)L,
+    TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, n, SPLIT_WARPS * 32), SPLIT_WARPS * 32, 0, n,
+               (const int32_t*)L,
                (const uint2*)vb, rshift, split);
     TCB_LAUNCH(ctx, k_make_items, grid_for(ctx, n, 256), 256, 0, row, (const int64_t*)seg,
                (const int64_t*)(seg + n), ls, n, witems, citems, titems, nw, nc, nt, shard,
