@@ -103,6 +103,10 @@ TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_s
  * CTA-tier pass use the bucket-table fallback that otherwise runs only when
  * a cuckoo build fails, so the tests reach that path.  0 = normal. */
 #define TCB_TEST_FORCE_FALLBACK 4
+/* Test hook: graphs of <= 2^17 vertices and edges normally take a one-launch
+ * small-graph kernel; this flag (or any nonzero flag / tuning) forces the
+ * general path on them. */
+#define TCB_TEST_GENERAL_PATH 8
 TCB_API int tcb_set_test_flags(tcb_context* ctx, int flags);
 
 /* ---- input synthesis (rmat.py:45-72) ---------------------------------- */

@@ -36,6 +36,9 @@
 
 #include "common.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace cg = cooperative_groups;
 
 namespace tcb {
@@ -609,6 +612,218 @@ static void launch_bfs(Context* ctx, const int64_t* row, const int32_t* nb, int6
     TCB_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_coop, dim3(ctx->bfs_coop_blocks),
                                          dim3(BFS_BLOCK), args, 0, ctx->stream));
     ctx->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// Small graphs (n, m <= SMALL_MAX): the whole cover-edge path in ONE
+// cooperative launch.  On graphs of a few thousand edges the ~25 dependent
+// kernels of the general path cost more than their work (ER-4096: 0.31 ms);
+// here each stage is a grid barrier away from the next:
+//   1. isolated vertices at level 0; union-find hooking every edge (larger
+//      root under the smaller, so each root is its component's minimum);
+//   2. the minima seeded at level 0, multi-source level-synchronous BFS —
+//      the reference's lowest-id-root levels (_kernels.py:137-156);
+//   3. every horizontal edge u < v (_kernels.py:680): the shorter of N(u),
+//      N(v) walked by the warp's lanes, each id binary-searched in the other
+//      list; a common neighbour on another level adds to c1, one on the same
+//      level to c2 (_kernels.py:745-748, the reference's own per-edge rule:
+//      no owner order needed), so T = c1 + c2/3.
+constexpr int64_t SMALL_MAX = int64_t(1) << 17;
+constexpr int SMALL_BLOCK = 512;
+
+__device__ __forceinline__ bool sorted_contains(const int32_t* __restrict__ a, int len, int key) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo < len && a[lo] == key;
+}
+
+// Level-synchronous BFS from the vertices already in qa (q_len[0] of them,
+// at level `base`); returns the number of the last non-empty level.
+__device__ __forceinline__ int small_bfs(cg::grid_group& grid, const int64_t* __restrict__ row,
+                                         const int32_t* __restrict__ nb, int32_t* level, int* qa,
+                                         int* qb, DevCounters* C, int gtid, int gwarp,
+                                         int nwarps) {
+    const int lane = int(lane_id());
+    int* cur = qa;
+    int* nxt = qb;
+    int L = 0;
+    while (true) {
+        const int nf = int(ld_volatile_u64(&C->q_len[L % 3]));
+        if (nf == 0) break;
+        if (gtid == 0) C->q_len[(L + 2) % 3] = 0;  // read two barriers ago, written next level
+        for (int i = gwarp; i < nf; i += nwarps) {
+            const int u = cur[i];
+            const int next = level[u] + 1;
+            for (int64_t p0 = row[u]; p0 < row[u + 1]; p0 += 32) {
+                const int64_t p = p0 + lane;
+                bool claim = false;
+                int w = 0;
+                if (p < row[u + 1]) {
+                    w = nb[p];
+                    claim = level[w] == -1 && atomicCAS(&level[w], -1, next) == -1;
+                }
+                const unsigned long long slot = warp_append(claim, &C->q_len[(L + 1) % 3]);
+                if (claim) nxt[slot] = w;
+            }
+        }
+        grid.sync();
+        int* t = cur;
+        cur = nxt;
+        nxt = t;
+        ++L;
+    }
+    return L - 1;
+}
+
+__global__ void __launch_bounds__(SMALL_BLOCK)
+    k_small_cetc(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int n,
+                 int32_t* level, int* par, int* qa, int* qb, DevCounters* C) {
+    cg::grid_group grid = cg::this_grid();
+    const int gtid = int(blockIdx.x * blockDim.x + threadIdx.x);
+    const int gthreads = int(gridDim.x * blockDim.x);
+    const int lane = int(lane_id());
+    const int gwarp = gtid >> 5, nwarps = gthreads >> 5;
+    // 1. isolated vertices at level 0; r0 = the lowest non-isolated id, the
+    //    minimum of its component (every smaller id is isolated): a root
+    unsigned long long iso = 0, key = 0;
+    for (int v = gtid; v < n; v += gthreads) {
+        const bool isolated = row[v + 1] == row[v];
+        level[v] = isolated ? 0 : -1;
+        iso += isolated;
+        if (!isolated) key = max(key, (unsigned long long)(n - v));
+    }
+    iso = warp_sum(iso);
+    key = warp_max_u64(key);
+    if (lane == 0) {
+        if (iso) atomicAdd(&C->components, iso);
+        if (key) atomicMax(&C->r0key, key);
+    }
+    grid.sync();
+    const int r0 = int(n - int64_t(ld_volatile_u64(&C->r0key)));
+    if (gtid == 0) {
+        level[r0] = 0;
+        qa[0] = r0;
+        C->q_len[0] = 1;
+        C->components += 1;
+    }
+    grid.sync();
+    // 2. BFS from r0 (on the graphs this path sees, usually everything)
+    int max_level = small_bfs(grid, row, nb, level, qa, qb, C, gtid, gwarp, nwarps);
+    // 3. what it left unvisited: min-root union-find over those vertices
+    //    only (hooking the larger root under the smaller, so each root is its
+    //    component's minimum), the roots at level 0, a second BFS
+    for (int v = gtid; v < n; v += gthreads) par[v] = v;
+    if (gtid == 0) C->q_len[0] = C->q_len[1] = C->q_len[2] = 0;
+    grid.sync();
+    for (int u = gwarp; u < n; u += nwarps) {
+        if (level[u] != -1) continue;  // warp-uniform
+        for (int64_t p = row[u] + lane; p < row[u + 1]; p += 32) {
+            const int v = nb[p];
+            if (v > u) hook(u, v, par);
+        }
+    }
+    grid.sync();
+    unsigned long long roots = 0;
+    for (int base = gtid - lane; base < n; base += gthreads) {
+        const int v = base + lane;
+        const bool root = v < n && level[v] == -1 && find_root(v, par) == v;
+        const unsigned long long slot = warp_append(root, &C->q_len[0]);
+        if (root) qa[slot] = v;
+        roots += root;
+    }
+    roots = warp_sum(roots);
+    if (lane == 0 && roots) atomicAdd(&C->components, roots);
+    grid.sync();
+    for (int i = gtid; i < int(ld_volatile_u64(&C->q_len[0])); i += gthreads) level[qa[i]] = 0;
+    grid.sync();
+    max_level = max(max_level, small_bfs(grid, row, nb, level, qa, qb, C, gtid, gwarp, nwarps));
+    if (gtid == 0 && max_level > 0) atomicMax(&C->max_level, (unsigned long long)max_level);
+    // 3. the horizontal edges and their common neighbours
+    unsigned long long c1 = 0, c2 = 0, nh = 0;
+    for (int u = gwarp; u < n; u += nwarps) {
+        const int64_t ub = row[u], ue = row[u + 1];
+        const int lu = level[u];
+        for (int64_t q0 = ub; q0 < ue; q0 += 32) {
+            // the lanes test 32 neighbours at once; the horizontal ones
+            // (v > u on u's level) are then intersected one by one
+            const int64_t q = q0 + lane;
+            int v = 0;
+            int64_t vb = 0, ve = 0;
+            bool hz = false;
+            if (q < ue) {
+                v = nb[q];
+                hz = v > u && level[v] == lu;
+                if (hz) {
+                    vb = row[v];
+                    ve = row[v + 1];
+                }
+            }
+            unsigned hm = __ballot_sync(0xffffffffu, hz);
+            nh += lane == 0 ? __popc(hm) : 0;
+            while (hm) {
+                const int src = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const int64_t b0 = __shfl_sync(0xffffffffu, vb, src);
+                const int64_t b1 = __shfl_sync(0xffffffffu, ve, src);
+                const bool ushort = ue - ub <= b1 - b0;
+                const int32_t* a = nb + (ushort ? ub : b0);
+                const int la = int(ushort ? ue - ub : b1 - b0);
+                const int32_t* b = nb + (ushort ? b0 : ub);
+                const int lb = int(ushort ? b1 - b0 : ue - ub);
+                for (int i = lane; i < la; i += 32) {
+                    const int w = a[i];
+                    if (sorted_contains(b, lb, w)) {
+                        if (level[w] != lu) ++c1; else ++c2;
+                    }
+                }
+            }
+        }
+    }
+    c1 = warp_sum(c1);
+    c2 = warp_sum(c2);
+    nh = warp_sum(nh);
+    if (lane == 0) {
+        if (c1) atomicAdd(&C->c1, c1);
+        if (c2) atomicAdd(&C->c2, c2);
+        if (nh) atomicAdd((unsigned long long*)&C->ncover, nh);
+    }
+}
+
+// The small-graph path (k_small_cetc); false when the graph is too large
+// for it (the caller runs the general path).
+bool small_cetc(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n, int64_t m,
+                int32_t* level) {
+    if (n > SMALL_MAX || m > SMALL_MAX || m == 0 || ctx->tune_wt || ctx->tune_hc ||
+        ctx->test_flags || getenv("TCB_NO_SMALL"))
+        return false;
+    DevCounters* C = ctx->d_counters;
+    int* par = ctx->wsT<int>(WS_COMP, n);
+    int* qa = reinterpret_cast<int*>(ctx->wsT<QEnt>(WS_QUEUE_A, n));
+    int* qb = reinterpret_cast<int*>(ctx->wsT<QEnt>(WS_QUEUE_B, n));
+    if (ctx->small_blocks == 0) {
+        int per_sm = 0;
+        TCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_cetc, SMALL_BLOCK,
+                                                               0));
+        require(per_sm > 0, "small-graph kernel cannot be co-resident");
+        ctx->small_blocks = ctx->num_sms * std::min(per_sm, 2);
+    }
+    // every SM: the per-vertex stages are latency chains, so warps matter
+    // more than the (nearly size-independent) cost of a grid barrier
+    const int blocks = ctx->small_blocks;
+    int ni = int(n);
+    void* args[] = {(void*)&row, (void*)&nb, (void*)&ni, (void*)&level,
+                    (void*)&par, (void*)&qa, (void*)&qb, (void*)&C};
+    ctx->record(0);
+    ctx->record(1);
+    TCB_CUDA(cudaLaunchCooperativeKernel((const void*)k_small_cetc, dim3(blocks),
+                                         dim3(SMALL_BLOCK), args, 0, ctx->stream));
+    ctx->launches++;
+    ctx->record(2);
+    ctx->record(3);
+    return true;
 }
 
 void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,

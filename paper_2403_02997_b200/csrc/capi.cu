@@ -16,6 +16,7 @@ void csr_build(Context*, const int64_t*, int64_t, int64_t, int64_t*, int32_t*, i
                int32_t*, int32_t*, int64_t*);
 void csr_rows(Context*, const int64_t*, int64_t, int32_t*);
 void csr_edges(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*, int32_t*);
+bool small_cetc(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*);
 void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
                 int32_t*, bool);
 void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
@@ -91,6 +92,11 @@ void cetc_device(Context* ctx, const int64_t* row, const int32_t* nb, const int3
     TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
     ctx->isect_events = false;
     if (n == 0) return;
+    // graphs of at most 2^17 vertices and edges: one cooperative launch
+    if (nshards == 1 && small_cetc(ctx, row, nb, n, m, level)) {  // events 0-3
+        ctx->record(4);
+        return;
+    }
     bfs_levels(ctx, row, nb, src, n, m, level, false);  // events 0, 1, 2
     if (m == 0) {
         ctx->record(3);

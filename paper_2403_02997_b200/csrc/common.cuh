@@ -113,6 +113,7 @@ struct Context {
     // occupancy-derived grid sizes, computed on first use (per context, so
     // per thread and per device: no shared mutable state across contexts)
     int bfs_coop_blocks = 0;
+    int small_blocks = 0;  // k_small_cetc grid (one CTA per SM)
     int isect_warp_blocks = 0, isect_cta_blocks = 0;
     int parent_blocks_per_sm = 0;
     int tune_wt = 0;   // intersection: warp-tier max owner degree (0 = default)

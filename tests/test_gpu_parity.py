@@ -233,6 +233,23 @@ def test_every_intersection_path_small(tuning):
         ctx.set_tuning(0, 0)
 
 
+def test_general_path_on_small_cases():
+    """The small cases normally take the one-launch small-graph kernel; with
+    TCB_TEST_GENERAL_PATH they take the general path (owner-order lists,
+    default tiers): both must reproduce the reference."""
+    ctx = tb._lib.context()
+    ctx.set_test_flags(8)  # TCB_TEST_GENERAL_PATH
+    try:
+        for case in SMALL_CASES:
+            g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+            r = tb.cetc(tb.device_graph(g), keep_level=True)
+            assert (r.triangles, r.c1, r.c2) == (case.T, case.c1, case.c2), case.name
+            assert r.ncover == len(case.cover), case.name
+            assert np.array_equal(r.level.cpu().numpy(), case.level), case.name
+    finally:
+        ctx.set_test_flags(0)
+
+
 @pytest.mark.parametrize("tuning", [(64, 64), (16, 512)])
 def test_every_intersection_path_rmat16(tuning):
     gold = config_goldens()["rmat16"]

@@ -2,8 +2,9 @@
 
 The intersection departs from the reference in how it deduplicates
 same-level apexes: the reference keeps an apex w on the cover edge's level
-iff w > max(u, v) (_kernels.py:687); the GPU keeps it iff w ranks above both
-endpoints in (degree desc, id asc) order (intersect.cu header).  Both select
+iff w > max(u, v) (_kernels.py:687); the GPU's general path keeps it iff w
+ranks above both endpoints in (degree bucket desc, id asc) order (intersect.cu
+header).  Both select
 one of the three edges of an all-horizontal triangle, so T and c2 agree —
 this sweep hunts for the inputs where a rank-order bug would hide: heavy
 equal-degree ties (regular and circulant graphs, disjoint equal cliques),
@@ -160,12 +161,25 @@ def _case(gen, seed):
     return n, pairs, row, nb, ref
 
 
+GENERAL_PATH = 8  # tcb_set_test_flags: skip the small-graph kernel (bfs.cu k_small_cetc)
+
+
 def _check_default(n, row, nb, ref, tag):
-    r = tb.cetc_host(row, nb, n, want_level=True)
-    assert np.array_equal(r["level"], ref["level"]), tag
-    assert (r["components"], r["max_level"]) == (ref["components"], ref["max_level"]), tag
-    assert r["ncover"] == len(ref["cover"]), tag
-    assert (r["triangles"], r["c1"], r["c2"]) == (ref["T"], ref["c1"], ref["c2"]), tag
+    """Through the host entry twice: as dispatched (graphs of <= 2^17
+    vertices and edges take the one-launch small-graph kernel) and with the
+    general path forced, so the owner-order dedup is checked on every graph."""
+    ctx = tb._lib.context()
+    for flags in (0, GENERAL_PATH):
+        ctx.set_test_flags(flags)
+        try:
+            r = tb.cetc_host(row, nb, n, want_level=True)
+        finally:
+            ctx.set_test_flags(0)
+        t = (tag, flags)
+        assert np.array_equal(r["level"], ref["level"]), t
+        assert (r["components"], r["max_level"]) == (ref["components"], ref["max_level"]), t
+        assert r["ncover"] == len(ref["cover"]), t
+        assert (r["triangles"], r["c1"], r["c2"]) == (ref["T"], ref["c1"], ref["c2"]), t
 
 
 TUNINGS = [(4, 4), (16, 64), (64, 512), (1024, 16)]
