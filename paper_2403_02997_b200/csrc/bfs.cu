@@ -678,6 +678,110 @@ __device__ __forceinline__ int small_bfs(cg::grid_group& grid, const int64_t* __
     return L - 1;
 }
 
+// Every horizontal edge u < v (_kernels.py:680): the lanes test 32 of
+// N(u)'s entries at once, and each horizontal one is intersected by walking
+// the shorter of N(u), N(v) with the lanes and binary-searching the other
+// list; a common neighbour on another level adds to c1, one on the same
+// level to c2 (_kernels.py:745-748, the reference's own per-edge rule), so
+// T = c1 + c2/3.  Warp per vertex.
+__device__ __forceinline__ void small_count(const int64_t* __restrict__ row,
+                                            const int32_t* __restrict__ nb, int n,
+                                            const int32_t* __restrict__ level, DevCounters* C,
+                                            int gwarp, int nwarps) {
+    const int lane = int(lane_id());
+    unsigned long long c1 = 0, c2 = 0, nh = 0;
+    for (int u = gwarp; u < n; u += nwarps) {
+        const int64_t ub = row[u], ue = row[u + 1];
+        const int lu = level[u];
+        for (int64_t q0 = ub; q0 < ue; q0 += 32) {
+            // the lanes test 32 neighbours at once; the horizontal ones
+            // (v > u on u's level) are then intersected one by one
+            const int64_t q = q0 + lane;
+            int v = 0;
+            int64_t vb = 0, ve = 0;
+            bool hz = false;
+            if (q < ue) {
+                v = nb[q];
+                hz = v > u && level[v] == lu;
+                if (hz) {
+                    vb = row[v];
+                    ve = row[v + 1];
+                }
+            }
+            unsigned hm = __ballot_sync(0xffffffffu, hz);
+            nh += lane == 0 ? __popc(hm) : 0;
+            while (hm) {
+                const int src = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const int64_t b0 = __shfl_sync(0xffffffffu, vb, src);
+                const int64_t b1 = __shfl_sync(0xffffffffu, ve, src);
+                const bool ushort = ue - ub <= b1 - b0;
+                const int32_t* a = nb + (ushort ? ub : b0);
+                const int la = int(ushort ? ue - ub : b1 - b0);
+                const int32_t* b = nb + (ushort ? b0 : ub);
+                const int lb = int(ushort ? b1 - b0 : ue - ub);
+                for (int i = lane; i < la; i += 32) {
+                    const int w = a[i];
+                    if (sorted_contains(b, lb, w)) {
+                        if (level[w] != lu) ++c1; else ++c2;
+                    }
+                }
+            }
+        }
+    }
+    c1 = warp_sum(c1);
+    c2 = warp_sum(c2);
+    nh = warp_sum(nh);
+    if (lane == 0) {
+        if (c1) atomicAdd(&C->c1, c1);
+        if (c2) atomicAdd(&C->c2, c2);
+        if (nh) atomicAdd((unsigned long long*)&C->ncover, nh);
+    }
+}
+
+// The count alone, after the general path's levels, for low-degree graphs
+// (every degree <= LOWDEG_MAX): a thread per vertex u; each horizontal edge
+// u < v is a two-pointer merge of the two sorted rows (the reference's own
+// merge, _kernels.py:681-694, with its per-hit rule: another level -> c1,
+// same level -> c2).
+__global__ void __launch_bounds__(256)
+    k_lowdeg_count(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int n,
+                   const int32_t* __restrict__ level, DevCounters* C) {
+    const int stride = int(gridDim.x * blockDim.x);
+    unsigned long long c1 = 0, c2 = 0, nh = 0;
+    for (int u = int(blockIdx.x * blockDim.x + threadIdx.x); u < n; u += stride) {
+        const int64_t ub = row[u], ue = row[u + 1];
+        const int lu = level[u];
+        for (int64_t q = ub; q < ue; ++q) {
+            const int v = nb[q];
+            if (v <= u || level[v] != lu) continue;
+            ++nh;
+            int64_t i = ub, j = row[v];
+            const int64_t je = row[v + 1];
+            while (i < ue && j < je) {
+                const int a = nb[i], b = nb[j];
+                if (a == b) {
+                    if (level[a] != lu) ++c1; else ++c2;
+                    ++i;
+                    ++j;
+                } else if (a < b) {
+                    ++i;
+                } else {
+                    ++j;
+                }
+            }
+        }
+    }
+    c1 = warp_sum(c1);
+    c2 = warp_sum(c2);
+    nh = warp_sum(nh);
+    if (lane_id() == 0) {
+        if (c1) atomicAdd(&C->c1, c1);
+        if (c2) atomicAdd(&C->c2, c2);
+        if (nh) atomicAdd((unsigned long long*)&C->ncover, nh);
+    }
+}
+
 __global__ void __launch_bounds__(SMALL_BLOCK)
     k_small_cetc(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int n,
                  int32_t* level, int* par, int* qa, int* qb, DevCounters* C) {
@@ -742,63 +846,50 @@ __global__ void __launch_bounds__(SMALL_BLOCK)
     max_level = max(max_level, small_bfs(grid, row, nb, level, qa, qb, C, gtid, gwarp, nwarps));
     if (gtid == 0 && max_level > 0) atomicMax(&C->max_level, (unsigned long long)max_level);
     // 3. the horizontal edges and their common neighbours
-    unsigned long long c1 = 0, c2 = 0, nh = 0;
-    for (int u = gwarp; u < n; u += nwarps) {
-        const int64_t ub = row[u], ue = row[u + 1];
-        const int lu = level[u];
-        for (int64_t q0 = ub; q0 < ue; q0 += 32) {
-            // the lanes test 32 neighbours at once; the horizontal ones
-            // (v > u on u's level) are then intersected one by one
-            const int64_t q = q0 + lane;
-            int v = 0;
-            int64_t vb = 0, ve = 0;
-            bool hz = false;
-            if (q < ue) {
-                v = nb[q];
-                hz = v > u && level[v] == lu;
-                if (hz) {
-                    vb = row[v];
-                    ve = row[v + 1];
-                }
-            }
-            unsigned hm = __ballot_sync(0xffffffffu, hz);
-            nh += lane == 0 ? __popc(hm) : 0;
-            while (hm) {
-                const int src = __ffs(hm) - 1;
-                hm &= hm - 1;
-                const int64_t b0 = __shfl_sync(0xffffffffu, vb, src);
-                const int64_t b1 = __shfl_sync(0xffffffffu, ve, src);
-                const bool ushort = ue - ub <= b1 - b0;
-                const int32_t* a = nb + (ushort ? ub : b0);
-                const int la = int(ushort ? ue - ub : b1 - b0);
-                const int32_t* b = nb + (ushort ? b0 : ub);
-                const int lb = int(ushort ? b1 - b0 : ue - ub);
-                for (int i = lane; i < la; i += 32) {
-                    const int w = a[i];
-                    if (sorted_contains(b, lb, w)) {
-                        if (level[w] != lu) ++c1; else ++c2;
-                    }
-                }
-            }
-        }
-    }
-    c1 = warp_sum(c1);
-    c2 = warp_sum(c2);
-    nh = warp_sum(nh);
-    if (lane == 0) {
-        if (c1) atomicAdd(&C->c1, c1);
-        if (c2) atomicAdd(&C->c2, c2);
-        if (nh) atomicAdd((unsigned long long*)&C->ncover, nh);
-    }
+    small_count(row, nb, n, level, C, gwarp, nwarps);
 }
 
-// The small-graph path (k_small_cetc); false when the graph is too large
-// for it (the caller runs the general path).
+__global__ void k_max_degree(const int64_t* __restrict__ row, int64_t n,
+                             unsigned long long* out) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    unsigned long long d = 0;
+    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+        d = max(d, (unsigned long long)(row[v + 1] - row[v]));
+    d = warp_max_u64(d);
+    if (lane_id() == 0 && d) atomicMax(out, d);
+}
+
+// The one-launch path (k_small_cetc) for graphs of at most 2^17 vertices
+// and edges, and for low-degree graphs of any size (max degree <=
+// LOWDEG_MAX, e.g. the lattice: there the per-edge binary searches cost less
+// than the general path's list build, and the BFS is the same level loop);
+// false otherwise (the caller runs the general path).  Deciding the second
+// case reads the max degree back: one ~10 us round trip on graphs larger
+// than 2^17 edges.
+void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
+                int64_t n, int64_t m, int32_t* level, bool reset_counters);
+constexpr int64_t LOWDEG_MAX = 16;
 bool small_cetc(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n, int64_t m,
                 int32_t* level) {
-    if (n > SMALL_MAX || m > SMALL_MAX || m == 0 || ctx->tune_wt || ctx->tune_hc ||
-        ctx->test_flags || getenv("TCB_NO_SMALL"))
+    if (m == 0 || ctx->tune_wt || ctx->tune_hc || ctx->test_flags || getenv("TCB_NO_SMALL"))
         return false;
+    if (n > SMALL_MAX || m > SMALL_MAX) {
+        if (getenv("TCB_NO_LOWDEG")) return false;
+        unsigned long long* d_dmax = &ctx->d_counters->scratch[11];
+        TCB_CUDA(cudaMemsetAsync(d_dmax, 0, sizeof(unsigned long long), ctx->stream));
+        TCB_LAUNCH(ctx, k_max_degree, grid_for(ctx, n, 256), 256, 0, row, n, d_dmax);
+        unsigned long long dmax = 0;
+        TCB_CUDA(cudaMemcpyAsync(&dmax, d_dmax, sizeof(dmax), cudaMemcpyDeviceToHost, ctx->stream));
+        TCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (dmax > (unsigned long long)LOWDEG_MAX) return false;
+        // low degree, large: the general BFS (direction-optimising, block-
+        // aggregated level counters) for the levels, then the count kernel
+        bfs_levels(ctx, row, nb, nullptr, n, m, level, false);  // events 0, 1, 2
+        ctx->record(3);
+        TCB_LAUNCH(ctx, k_lowdeg_count, ctx->num_sms * 8, 256, 0, row, nb, int(n),
+                   (const int32_t*)level, ctx->d_counters);
+        return true;
+    }
     DevCounters* C = ctx->d_counters;
     int* par = ctx->wsT<int>(WS_COMP, n);
     int* qa = reinterpret_cast<int*>(ctx->wsT<QEnt>(WS_QUEUE_A, n));

@@ -159,6 +159,19 @@ def test_config_parity(name):
     _check_config(name)
 
 
+@pytest.mark.parametrize("name", ["er4096", "lattice2048"])
+def test_config_parity_general_path(name):
+    """ER-4096 (small-graph kernel) and the lattice (low-degree count) again
+    with TCB_TEST_GENERAL_PATH: the owner-order lists and tiers at config
+    scale must give the same outputs."""
+    ctx = tb._lib.context()
+    ctx.set_test_flags(8)
+    try:
+        _check_config(name)
+    finally:
+        ctx.set_test_flags(0)
+
+
 def _check_parent(name):
     """FIFO parents and edge classes at config scale against the C oracle's
     FIFO BFS (itself pinned to the reference on the golden cases)."""
