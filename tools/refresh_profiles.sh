@@ -1,9 +1,10 @@
 # Round-end measurement refresh (run on the GPU box): ncu launch list of the
-# rmat24 step (per-kernel DRAM bytes -> profiles/ncu_traffic.json), bench
-# lines for every config, the reference arm, and a full ncu capture of
-# k_isect_cta.  Outputs under gpurun_out/$TAG; copy the summaries into profiles/.
+# rmat24 step with per-kernel DRAM bytes (-> profiles/ncu_traffic.json), bench
+# lines for every config, a full ncu capture of k_isect_cta, and DRAM bytes of
+# every BFS/components kernel at rmat24 and the lattice.  Outputs under
+# gpurun_out/$TAG; copy the summaries into profiles/.
 set -x
-TAG=${1:-r01}
+TAG=${1:-r02}
 O=gpurun_out/$TAG
 mkdir -p $O
 python tools/profile_step.py rmat24 2 > $O/step_plain.log 2>&1 && \
@@ -11,8 +12,9 @@ python tools/profile_step.py rmat24 2 > $O/step_plain.log 2>&1 && \
 python tools/ncu_traffic.py $O/launches_rmat24.csv rmat24 profiles/ncu_traffic.json "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, python tools/profile_step.py rmat24 2 (last launch of each kernel), $TAG" > /dev/null
 cp profiles/ncu_traffic.json $O/ncu_traffic.json
 python tools/ncu_summary.py launches $O/launches_rmat24.csv > $O/launches_rmat24.txt
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches_lattice.csv python tools/profile_step.py lattice2048 2 > $O/ncu_launch_lattice.log 2>&1
+python tools/ncu_summary.py launches $O/launches_lattice.csv > $O/launches_lattice.txt
 python bench.py > $O/bench_rmat24.json 2> $O/bench_rmat24.err; tail -c 600 $O/bench_rmat24.json
 for c in rmat22 lattice2048 rmat16 er4096; do python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err; done
-python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_isect_cta -c 1 -o $O/cta_r24 python tools/profile_step.py rmat24 1 > $O/ncu_full.log 2>&1
 ls -la $O
