@@ -143,6 +143,9 @@ __global__ void k_bfs_probe(const int64_t* __restrict__ row, int64_t n,
 #ifndef TCB_BFS_BLOCK
 #define TCB_BFS_BLOCK 512
 #endif
+#ifndef TCB_BFS_MINB
+#define TCB_BFS_MINB (1024 / TCB_BFS_BLOCK)  // 1024 threads per SM, <= 64 registers
+#endif
 constexpr int BFS_BLOCK = TCB_BFS_BLOCK;
 constexpr int BFS_WPB = BFS_BLOCK / 32;
 #ifndef TCB_BFS_ALPHA
@@ -315,7 +318,7 @@ __device__ __forceinline__ void bu_step(const int64_t* __restrict__ row,
     }
 }
 
-__global__ void __launch_bounds__(BFS_BLOCK, 2)
+__global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
     k_bfs_coop(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                int32_t* level, QEnt* qa, QEnt* qb, int2* chunks, DevCounters* C,
                int64_t dir_edges, const unsigned long long* dir_edges_p, BfsBits bits,
