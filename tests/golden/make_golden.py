@@ -4,6 +4,7 @@ Run in the build container (where /root/reference exists):
 
     NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py small
     NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py configs [names...]
+    NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py parents [names...]
 
 ``small``   -> tests/golden/small_cases.npz: inputs and every hot-path output
                (CSR, levels, parents, edge classes, components, max_level,
@@ -246,11 +247,36 @@ def make_configs(names):
         path.write_text(json.dumps(data, indent=1, sort_keys=True))
 
 
+def add_parent_digests(names):
+    """Add the reference's FIFO parents and edge classes (bfs_label,
+    bfs.py:76-94) to existing config records as sha256 digests.  The CSR is
+    the oracle's (identical to the reference's normalize at every config where
+    both ran: oracle_csr_matches), wrapped in the reference Graph; only the
+    labeling runs, so RMAT-24 takes seconds, not the CETC-SM hours."""
+    path = GOLDEN / "configs.json"
+    data = json.loads(path.read_text())
+    for name in names:
+        cfg = C.CONFIGS[name]
+        g = _config_graph(cfg, "oracle")
+        assert sha(g.row_offsets.astype(np.int64)) == data[name]["row_offsets_sha"], name
+        assert sha(g.neighbors.astype(np.int32)) == data[name]["neighbors_sha"], name
+        t0 = time.time()
+        lab = tc.bfs_label(g)
+        assert sha(lab.level.astype(np.int32)) == data[name]["level_sha"], name
+        data[name]["parent_sha"] = sha(lab.parent.astype(np.int64))
+        data[name]["edge_class_sha"] = sha(lab.edge_class.astype(np.int8))
+        print(name, "bfs_label", round(time.time() - t0, 1), "s", data[name]["parent_sha"][:12])
+        path.write_text(json.dumps(data, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what == "small":
         make_small()
     elif what == "configs":
         make_configs(sys.argv[2:] or ["er4096", "rmat16", "lattice2048"])
+    elif what == "parents":
+        add_parent_digests(sys.argv[2:] or ["er4096", "rmat16", "lattice2048", "rmat22",
+                                            "rmat24"])
     else:
         raise SystemExit(f"unknown target {what}")

@@ -173,13 +173,18 @@ def test_config_parity_general_path(name):
 
 
 def _check_parent(name):
-    """FIFO parents and edge classes at config scale against the C oracle's
-    FIFO BFS (itself pinned to the reference on the golden cases)."""
+    """FIFO parents and edge classes at config scale against the reference's
+    own bfs_label (sha256 digests in configs.json, tests/golden/make_golden.py
+    parents) and the C oracle's FIFO BFS."""
     import torch
     dg = C.build_device_graph(name)
     level, _, max_level = tb.ops.bfs_levels(dg)
     parent = tb.ops.bfs_parent(dg, level, max_level)
     classes = tb.ops.edge_classes(dg, level, parent)
+    gold = config_goldens().get(name, {})
+    if "parent_sha" in gold:
+        assert sha(parent.cpu().numpy().astype(np.int64)) == gold["parent_sha"]
+        assert sha(classes.cpu().numpy().astype(np.int8)) == gold["edge_class_sha"]
     row, nb = dg.row_offsets.cpu().numpy(), dg.neighbors.cpu().numpy()
     o_level, o_parent, _, _ = oracle.bfs_levels(row, nb, dg.n)
     assert np.array_equal(level.cpu().numpy(), o_level)
