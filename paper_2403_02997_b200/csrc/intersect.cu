@@ -832,8 +832,9 @@ __global__ void __launch_bounds__(256)
 constexpr int JW = 8;           // elements per lane per warp-tier round
 constexpr int W_SEG = 2 * PW;   // slices per warp item
 
+template <typename Probe>
 __device__ __forceinline__ void warp_stream(const int32_t* __restrict__ L, const int2* seg,
-                                            int total, int tsup, const BucketHash& h, Tally& tl) {
+                                            int total, int tsup, const Probe& h, Tally& tl) {
     const int lane = int(lane_id());
     int kc = 0;  // warp-uniform: the slice holding c0
     for (int c0 = 0; c0 < total; c0 += 32 * JW) {
@@ -876,7 +877,7 @@ __device__ __forceinline__ void warp_stream(const int32_t* __restrict__ L, const
 __global__ void __launch_bounds__(W_WARPS * 32, 4)
     k_isect_warp(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                  Lists ls, const int32_t* __restrict__ P, unsigned long long* fetch,
-                 DevCounters* C, const int2* __restrict__ vinfo, int fwd) {
+                 DevCounters* C, const int2* __restrict__ vinfo, int fwd, int dbg) {
     extern __shared__ uint4 smem4[];
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
@@ -901,9 +902,28 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
         const int slots = max(16, 4 << ceil_log2_dev(nx));
         BucketHash h;
         h.setup(tab, slots);
+        // a two-table cuckoo set (load <= 1/4): branch-free two-read probes
+        // (the bucket table's probe loop cost 1 ms more at RMAT-24); a failed
+        // kick chain rebuilds the item's table as buckets
+        CuckooHash ch;
+        ch.setup(tab, slots);
+        for (int i = lane; i < slots; i += 32) tab[i] = C_EMPTY;
+        __syncwarp();
+        bool fail = false;
         for (int i = lane; i < nx; i += 32) {
             const int w = i < no ? ls.L[o0 + i] : ls.L[s0 + (i - no)];
-            if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
+            if (staged(vinfo, w, x, dx, fwd) && !ch.insert(w)) fail = true;
+        }
+        const bool use_cuckoo =
+            !__any_sync(0xffffffffu, fail) && !(dbg & TCB_TEST_FORCE_FALLBACK);
+        __syncwarp();
+        if (!use_cuckoo) {
+            for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
+            __syncwarp();
+            for (int i = lane; i < nx; i += 32) {
+                const int w = i < no ? ls.L[o0 + i] : ls.L[s0 + (i - no)];
+                if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
+            }
         }
         // slices of partners lane and lane + 32: OFF (c0, c1), UP (c2, c3)
         // slices of partners lane + 32 r: OFF (cnt[r]), UP prefix (cnt[PPL + r])
@@ -959,7 +979,8 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
             if (lane == 0) seg[noff + (tn >> 16)] = make_int2(total, 0);
         }
         __syncwarp();
-        warp_stream(ls.L, seg, total, tsup, h, tl);
+        if (use_cuckoo) warp_stream(ls.L, seg, total, tsup, ch, tl);
+        else warp_stream(ls.L, seg, total, tsup, h, tl);
         __syncwarp();
         for (int i = lane; i < slots; i += 32) tab[i] = EMPTY;
         __syncwarp();
@@ -1537,7 +1558,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
 #endif
     TCB_LAUNCH(ctx, k_isect_warp, ctx->isect_warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
                (const unsigned long long*)nw, ls, (const int32_t*)P, fw, C, (const int2*)vinfo,
-               fwd);
+               fwd, ctx->test_flags);
     TCB_LAUNCH(ctx, k_isect_tiny, ctx->num_sms * 8, 256, 0, (const longlong4*)titems,
                (const unsigned long long*)nt, ls, (const int32_t*)P, C, (const int2*)vinfo, fwd);
 }
