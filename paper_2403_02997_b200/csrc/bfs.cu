@@ -335,9 +335,18 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
     __shared__ unsigned long long s_agg[3][BFS_WPB];  // per-warp level counters
 
     int L = 0;
-    int nf = int(ld_volatile_u64(&C->q_len[0]));
-    const int mf = int(ld_volatile_u64(&C->deg_sum[0]));
-    int dmax = int(ld_volatile_u64(&C->deg_max[0]));
+    // the seed's counters, read once per block (all threads loading one
+    // address serialise in its L2 slice)
+    if (threadIdx.x == 0) {
+        s_bc[0] = (long long)ld_volatile_u64(&C->q_len[0]);
+        s_bc[1] = (long long)ld_volatile_u64(&C->deg_sum[0]);
+        s_bc[2] = (long long)ld_volatile_u64(&C->deg_max[0]);
+    }
+    __syncthreads();
+    int nf = int(s_bc[0]);
+    const int mf = int(s_bc[1]);
+    int dmax = int(s_bc[2]);
+    __syncthreads();
     // directed entries of unvisited vertices (the second BFS reads its total
     // from the device: the remainder's degree sum)
     int mu = int((dir_edges_p ? int64_t(*dir_edges_p) : dir_edges) - mf);
@@ -653,8 +662,14 @@ __device__ __forceinline__ int small_bfs(cg::grid_group& grid, const int64_t* __
     int* cur = qa;
     int* nxt = qb;
     int L = 0;
+    __shared__ int s_nf;
     while (true) {
-        const int nf = int(ld_volatile_u64(&C->q_len[L % 3]));
+        // one load per block (every thread loading one address serialises
+        // in its L2 slice), shared through shared memory
+        if (threadIdx.x == 0) s_nf = int(ld_volatile_u64(&C->q_len[L % 3]));
+        __syncthreads();
+        const int nf = s_nf;
+        __syncthreads();
         if (nf == 0) break;
         if (gtid == 0) C->q_len[(L + 2) % 3] = 0;  // read two barriers ago, written next level
         for (int i = gwarp; i < nf; i += nwarps) {
@@ -809,7 +824,10 @@ __global__ void __launch_bounds__(SMALL_BLOCK)
         if (key) atomicMax(&C->r0key, key);
     }
     grid.sync();
-    const int r0 = int(n - int64_t(ld_volatile_u64(&C->r0key)));
+    __shared__ unsigned long long s_r0;
+    if (threadIdx.x == 0) s_r0 = ld_volatile_u64(&C->r0key);
+    __syncthreads();
+    const int r0 = int(n - int64_t(s_r0));
     if (gtid == 0) {
         level[r0] = 0;
         qa[0] = r0;
@@ -844,7 +862,9 @@ __global__ void __launch_bounds__(SMALL_BLOCK)
     roots = warp_sum(roots);
     if (lane == 0 && roots) atomicAdd(&C->components, roots);
     grid.sync();
-    for (int i = gtid; i < int(ld_volatile_u64(&C->q_len[0])); i += gthreads) level[qa[i]] = 0;
+    if (threadIdx.x == 0) s_r0 = ld_volatile_u64(&C->q_len[0]);
+    __syncthreads();
+    for (int i = gtid; i < int(s_r0); i += gthreads) level[qa[i]] = 0;
     grid.sync();
     max_level = max(max_level, small_bfs(grid, row, nb, level, qa, qb, C, gtid, gwarp, nwarps));
     if (gtid == 0 && max_level > 0) atomicMax(&C->max_level, (unsigned long long)max_level);
