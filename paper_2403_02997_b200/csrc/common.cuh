@@ -200,6 +200,20 @@ inline int grid_for(const Context* ctx, int64_t items, int block, int per_sm = 8
 #endif
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+// A device-written scalar every thread of a kernel needs: one load per block,
+// shared through shared memory (one load per warp would send thousands of
+// requests for one address to a single L2 slice, several microseconds per
+// kernel).  Contains a __syncthreads: call from block-uniform code.
+template <typename T>
+__device__ __forceinline__ T block_load(const T* p) {
+    __shared__ T s_val;
+    if (threadIdx.x == 0) s_val = *(volatile const T*)p;
+    __syncthreads();
+    const T v = s_val;
+    __syncthreads();
+    return v;
+}
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

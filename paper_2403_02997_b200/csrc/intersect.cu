@@ -311,7 +311,7 @@ __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __r
                              uint32_t* __restrict__ bits, uint2* __restrict__ cls) {
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const unsigned lane = lane_id();
-    const bool packed = *nopack == 0;
+    const bool packed = block_load(nopack) == 0;
     for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; base < nnz;
          base += gthreads) {
         const int64_t e = base + lane;
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(256)
     k_isect_tiny(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                  Lists ls, const int32_t* __restrict__ P, DevCounters* C,
                  const int2* __restrict__ vinfo, int fwd) {
-    const int64_t nitems = int64_t(*nitems_p);
+    const int64_t nitems = int64_t(block_load(nitems_p));
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     uint32_t n1 = 0, ns = 0;
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < nitems; it += stride) {
@@ -886,7 +886,7 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
                 warp * (W_SEG + 1);
     for (int i = lane; i < W_SLOTS; i += 32) tab[i] = EMPTY;
     __syncwarp();
-    const unsigned long long nitems = *nitems_p;
+    const unsigned long long nitems = block_load(nitems_p);
     Tally tl;
     while (true) {
         unsigned long long it = 0;
@@ -1204,7 +1204,7 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     __shared__ int s_next;
     __shared__ int s_fail;
     const int32_t* __restrict__ L = ls.L;
-    const unsigned long long nitems = *nitems_p;
+    const unsigned long long nitems = block_load(nitems_p);
 #ifdef TCB_NOSTREAM  // measurement-only variant: item setup and staging without streaming
     dbg |= 1;
 #endif

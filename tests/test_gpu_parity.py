@@ -380,3 +380,23 @@ def test_concurrent_calls_from_threads():
         c = cases[i % len(cases)]
         assert t == th == c.T, c.name
         assert level == c.level.tolist(), c.name
+
+
+@pytest.mark.parametrize("nbytes", [0, 4, 1 << 20, (96 << 20) + 12])
+def test_copy_to_device_pageable_and_pinned(nbytes):
+    """tcb_copy_to_device: pinned sources are one DMA, pageable ones go through
+    the 32 MB staging ring (96 MB + 12 bytes: three full chunks and a tail);
+    both must land byte-exact (the drop-in upload of a reference Graph)."""
+    import torch
+    ctx = tb._lib.context()
+    rng = np.random.default_rng(nbytes)
+    host = rng.integers(0, 256, size=nbytes, dtype=np.uint8)
+    for pinned in (False, True):
+        src = host
+        if pinned:
+            t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+            t.numpy()[:] = host
+            src = t.numpy()
+        dev = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+        ctx.check(ctx.lib.tcb_copy_to_device(ctx.h, tb._lib.ptr(dev), src.ctypes.data, nbytes))
+        assert np.array_equal(dev[:nbytes].cpu().numpy(), host), pinned
