@@ -104,7 +104,7 @@ TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_s
  * a cuckoo build fails, so the tests reach that path.  0 = normal. */
 #define TCB_TEST_FORCE_FALLBACK 4
 /* Test hook: graphs of <= 2^17 vertices and edges normally take a one-launch
- * small-graph kernel, and graphs of max degree <= 16 a merge count after the
+ * small-graph kernel, and graphs of max degree <= 32 a merge count after the
  * general BFS; this flag (or any nonzero flag / tuning) forces the general
  * path on them. */
 #define TCB_TEST_GENERAL_PATH 8

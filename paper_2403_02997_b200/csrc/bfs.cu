@@ -891,7 +891,10 @@ __global__ void k_max_degree(const int64_t* __restrict__ row, int64_t n,
 // than 2^17 edges.
 void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
                 int64_t n, int64_t m, int32_t* level, bool reset_counters);
-constexpr int64_t LOWDEG_MAX = 16;
+#ifndef TCB_LOWDEG_MAX
+#define TCB_LOWDEG_MAX 32  // ER-like graphs up to mean degree ~16 (tools/path_probe.py)
+#endif
+constexpr int64_t LOWDEG_MAX = TCB_LOWDEG_MAX;
 bool small_cetc(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n, int64_t m,
                 int32_t* level) {
     if (m == 0 || ctx->tune_wt || ctx->tune_hc || ctx->test_flags || getenv("TCB_NO_SMALL"))
