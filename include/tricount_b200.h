@@ -37,7 +37,7 @@ extern "C" {
 
 #define TCB_API __attribute__((visibility("default")))
 
-#define TCB_VERSION 5
+#define TCB_VERSION 6
 
 enum {
     TCB_OK = 0,
@@ -279,6 +279,22 @@ TCB_API int tcb_degree_order(tcb_context* ctx, const int64_t* d_row_offsets,
                              const int32_t* d_neighbors, const int32_t* d_src,
                              int64_t n, int64_t m, int64_t* d_row_out,
                              int32_t* d_neighbors_out, int32_t* d_src_out);
+
+/* ---- split hybrid (CETC-Seq-S/-SD/-SR, sequential.py:186-238) --------- */
+/* _split_by_level (sequential.py:186-193): G0 = the horizontal edges
+ * (level[u] == level[v]) as a CSR: d_row0 int64[n+1], d_nb0 / d_src0
+ * (nullable) capacity 2m int32; *m0_out = G0's undirected edges. */
+TCB_API int tcb_split_by_level(tcb_context* ctx, const int64_t* d_row_offsets,
+                               const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
+                               int64_t m, const int32_t* d_level, int64_t* d_row0,
+                               int32_t* d_nb0, int32_t* d_src0, int64_t* m0_out);
+
+/* split_cross_count_k (_kernels.py:786-805): triangles with one horizontal
+ * edge and both others level-spanning, i.e. sum over G0's edges u < v of
+ * |N1(u) ∩ N1(v)| with G1 = the level-spanning edges of the levels given. */
+TCB_API int tcb_split_cross_count(tcb_context* ctx, const int64_t* d_row_offsets,
+                                  const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
+                                  int64_t m, const int32_t* d_level, int64_t* cross_out);
 
 /* Host-buffer entry, the call a binding of cetc_count_k's argument list
  * (row, nb, n; _kernels.py:669) makes: uploads the CSR, derives src, runs

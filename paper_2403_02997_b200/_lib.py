@@ -80,6 +80,10 @@ def load_library(path: Path | None = None):
             "tcb_csr_build": ([vp, vp, i64, i64, vp, vp, vp, vp, vp, pi64], i32),
             "tcb_csr_rows": ([vp, vp, i64, vp], i32),
             "tcb_copy_to_device": ([vp, vp, vp, i64], i32),
+            "tcb_split_by_level": ([vp, vp, vp, vp, i64, i64, vp, vp, vp, vp,
+                                    ctypes.POINTER(ctypes.c_int64)], i32),
+            "tcb_split_cross_count": ([vp, vp, vp, vp, i64, i64, vp,
+                                       ctypes.POINTER(ctypes.c_int64)], i32),
             "tcb_csr_edges": ([vp, vp, vp, i64, i64, vp, vp], i32),
             "tcb_bfs_levels": ([vp, vp, vp, vp, i64, i64, vp, pi64, pi64], i32),
             "tcb_bfs_parent": ([vp, vp, vp, i64, vp, i64, vp], i32),

@@ -17,6 +17,8 @@ void csr_build(Context*, const int64_t*, int64_t, int64_t, int64_t*, int32_t*, i
 void csr_rows(Context*, const int64_t*, int64_t, int32_t*);
 void csr_edges(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*, int32_t*);
 bool small_cetc(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int32_t*);
+void split_by_level(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
+                    const int32_t*, int64_t*, int32_t*, int32_t*, int64_t*);
 void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
                 int32_t*, bool);
 void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
@@ -433,6 +435,39 @@ TCB_API int tcb_forward_count(tcb_context* ctx, const int64_t* d_row_offsets,
         require_sizes(n, m);
         require(triangles_out != nullptr, "triangles_out is null");
         forward_device(ctx, d_row_offsets, d_neighbors, d_src, n, m, triangles_out);
+    });
+}
+
+TCB_API int tcb_split_by_level(tcb_context* ctx, const int64_t* d_row_offsets,
+                               const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
+                               int64_t m, const int32_t* d_level, int64_t* d_row0,
+                               int32_t* d_nb0, int32_t* d_src0, int64_t* m0_out) {
+    return guarded(ctx, [&] {
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
+        require(m0_out != nullptr && d_row0 != nullptr, "null output");
+        require(m == 0 || (d_level != nullptr && d_nb0 != nullptr), "null input/output");
+        split_by_level(ctx, d_row_offsets, d_neighbors, d_src, n, m, d_level, d_row0, d_nb0,
+                       d_src0, m0_out);
+    });
+}
+
+TCB_API int tcb_split_cross_count(tcb_context* ctx, const int64_t* d_row_offsets,
+                                  const int32_t* d_neighbors, const int32_t* d_src, int64_t n,
+                                  int64_t m, const int32_t* d_level, int64_t* cross_out) {
+    return guarded(ctx, [&] {
+        require(m >= 0, "negative size");
+        require_sizes(n, m);
+        require(cross_out != nullptr, "cross_out is null");
+        TCB_CUDA(cudaMemsetAsync(ctx->d_counters, 0, sizeof(DevCounters), ctx->stream));
+        if (n > 0 && m > 0) {
+            require(d_level != nullptr, "null levels");
+            cetc_intersect_owner(ctx, d_row_offsets, d_neighbors, d_src, d_level, n, m, 0, 1, 2);
+        }
+        fetch_counters(ctx);
+        if (ctx->h_counters->c2 != 0)
+            throw Error(TCB_ERR_ASSERT, "cross count: same-level tally must be zero");
+        *cross_out = int64_t(ctx->h_counters->c1);
     });
 }
 

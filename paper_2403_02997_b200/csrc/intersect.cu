@@ -307,8 +307,11 @@ struct Lists {
 constexpr int KEY_DB = 22;  // degree bits of the packed key; level gets the top 10
 __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
                              const int2* __restrict__ vinfo, const uint32_t* __restrict__ key32,
-                             const unsigned long long* __restrict__ nopack, int64_t nnz, int fwd,
-                             uint32_t* __restrict__ bits, uint2* __restrict__ cls) {
+                             const unsigned long long* __restrict__ nopack, int64_t nnz,
+                             int mode, uint32_t* __restrict__ bits, uint2* __restrict__ cls) {
+    // mode bit 0: forward (every entry OFF); bit 1: cross only (no UP class:
+    // split_cross_count_k, the triangles with one horizontal edge)
+    const int fwd = mode & 1, xonly = mode >> 1;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const unsigned lane = lane_id();
     const bool packed = block_load(nopack) == 0;
@@ -332,7 +335,7 @@ __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __r
             const int ka = fwd ? a.y : dbucket(a.y), kb = fwd ? b.y : dbucket(b.y);
             keep = a.x == b.x && (ka > kb || (ka == kb && x < y));
             off = fwd || a.x != b.x;
-            sup = !fwd && a.x == b.x && !keep;  // UP: same level, y owns the edge
+            sup = !fwd && !xonly && a.x == b.x && !keep;  // UP: same level, y owns the edge
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         const unsigned mo = __ballot_sync(0xffffffffu, off);
@@ -350,12 +353,12 @@ __global__ void k_owner_bits(const int32_t* __restrict__ src, const int32_t* __r
 // and each owner its segment [seg_beg, seg_end) (k_list_bounds).
 uint32_t* owner_bits(Context* ctx, const int32_t* src, const int32_t* nb, const int2* vinfo,
                      const uint32_t* key32, const unsigned long long* nopack, int64_t nnz,
-                     int fwd, uint2* cls) {
+                     int mode, uint2* cls) {
     const int64_t nwords = (nnz + 31) / 32;
     uint32_t* bits = ctx->wsT<uint32_t>(WS_QUEUE_A, nwords + 1);
     TCB_CUDA(cudaMemsetAsync(bits + nwords, 0, sizeof(uint32_t), ctx->stream));
     TCB_LAUNCH(ctx, k_owner_bits, grid_for(ctx, nnz, 256), 256, 0, src, nb, vinfo, key32, nopack,
-               nnz, fwd, bits, cls);
+               nnz, mode, bits, cls);
     return bits;
 }
 
@@ -1436,9 +1439,14 @@ static int debug_flags() {
 #endif
 }
 
+// fwd: 0 = the cover-edge count, 1 = the forward count (every entry OFF,
+// owners stage only their higher-ranked neighbours), 2 = the cross count of
+// the split hybrid (split_cross_count_k: no UP class, so c1 only).
 void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
                           const int32_t* level, int64_t n, int64_t m, int shard, int nshards,
                           int fwd) {
+    const int xonly = fwd == 2 ? 1 : 0;
+    if (xonly) fwd = 0;
     if (n == 0 || m == 0) return;
     DevCounters* C = ctx->d_counters;
     const int64_t nnz = 2 * m;
@@ -1490,7 +1498,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo, key32, dbk,
                nopack);
     TCB_CUDA(cudaMemsetAsync(cls + nwords, 0, sizeof(uint2), ctx->stream));
-    const uint32_t* bits = owner_bits(ctx, src, nb, vinfo, key32, nopack, nnz, fwd, cls);
+    const uint32_t* bits =
+        owner_bits(ctx, src, nb, vinfo, key32, nopack, nnz, fwd | (xonly << 1), cls);
     scan_apply(
         ctx, nwords, [bits] __device__(int64_t j) -> int64_t { return __popc(bits[j]); },
         [prek] __device__(int64_t j, int64_t pos, int64_t) { prek[j] = (unsigned long long)pos; },

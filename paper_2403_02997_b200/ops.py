@@ -158,6 +158,39 @@ def cetc(dg: DeviceGraph, keep_level: bool = False, keep_cover: bool = False) ->
         **d)
 
 
+def split_by_level(dg: DeviceGraph, level) -> DeviceGraph:
+    """_split_by_level (sequential.py:186-193): the horizontal subgraph G0
+    (edges with equal levels) as a DeviceGraph of its own (tcb_split_by_level)."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    row0 = torch.empty(dg.n + 1, dtype=torch.int64, device=dg.device)
+    nb0 = torch.empty(max(2 * dg.m, 1), dtype=torch.int32, device=dg.device)
+    src0 = torch.empty(max(2 * dg.m, 1), dtype=torch.int32, device=dg.device)
+    m0 = ctypes.c_int64(0)
+    ctx.check(ctx.lib.tcb_split_by_level(ctx.h, _lib.ptr(dg.row_offsets), _lib.ptr(dg.neighbors),
+                                         _lib.ptr(dg.src), dg.n, dg.m, _lib.ptr(level),
+                                         _lib.ptr(row0), _lib.ptr(nb0), _lib.ptr(src0),
+                                         ctypes.byref(m0)))
+    m0 = int(m0.value)
+    return DeviceGraph(n=dg.n, m=m0, row_offsets=row0, neighbors=nb0[: 2 * m0],
+                       src=src0[: 2 * m0])
+
+
+def split_cross_count(dg: DeviceGraph, level) -> int:
+    """split_cross_count_k (_kernels.py:786-805) for the split of `dg` by
+    `level`: triangles with one horizontal edge and two level-spanning ones
+    (tcb_split_cross_count: the owner-staged intersection of the OFF lists)."""
+    import torch
+    ctx = _lib.context(dg.device.index)
+    level = level.to(device=dg.device, dtype=torch.int32).contiguous()
+    t = ctypes.c_int64(0)
+    ctx.check(ctx.lib.tcb_split_cross_count(ctx.h, _lib.ptr(dg.row_offsets),
+                                            _lib.ptr(dg.neighbors), _lib.ptr(dg.src), dg.n,
+                                            dg.m, _lib.ptr(level), ctypes.byref(t)))
+    return int(t.value)
+
+
 def forward_count(dg: DeviceGraph) -> int:
     """Forward triangle count on the GPU (tcb_forward_count; the forward
     branch of tc_cetc_fe, sequential.py:176-183)."""

@@ -10,16 +10,13 @@ charged to the call.
 * ``CETC-Seq-D``: the same after ``degree_order`` on the GPU.
 * ``CETC-Seq-FE``: covering ratio below ``COVER_RATIO_THRESHOLD`` -> cover-edge
   counting, else the forward count (``tcb_cetc_fe``).
-* ``CETC-Seq-S`` / ``-SD`` / ``-SR``: the split hybrid counts the triangles
-  with one horizontal edge (``split_cross_count_k`` over G0 x G1,
-  _kernels.py:787-805) plus the triangles of the horizontal subgraph G0
-  (forward-hashed on G0, recursively split for -SR).  Those two terms are
-  exactly the cover-edge pass's two tallies — one horizontal edge with an
-  off-level apex is c1, and a G0 triangle is the same-level tally (counted
-  once, at the edge whose apex ranks above both endpoints: the forward count
-  on G0 in owner order; c2 = 3 T(G0)) — so the GPU computes both in one
-  fused pass and returns c1 + c2/3; the CPU split into two graphs exists to
-  cut merge work, which the OFF/UP list intersection already avoids.
+* ``CETC-Seq-S`` / ``-SD`` / ``-SR``: the split hybrid as the reference
+  runs it (sequential.py:186-238): BFS levels, G0 = the horizontal edges as
+  a CSR of its own (``tcb_split_by_level``), the forward count of G0
+  (``tcb_forward_count``) plus the cross count (``tcb_split_cross_count``:
+  split_cross_count_k, triangles with one G0 edge and two level-spanning
+  ones); -SD after degree relabeling, -SR re-splitting G0 while it holds
+  more than the threshold of the edges and shrinks.
 """
 from __future__ import annotations
 
@@ -52,24 +49,52 @@ def tc_cetc_fe(g: Graph, threshold: float = COVER_RATIO_THRESHOLD) -> int:
     return int(r.triangles)
 
 
+# sequential.py:62: the split recursion bottoms out below this many edges
+SPLIT_RECURSION_FLOOR = 1024
+
+
+def _split_count(dg) -> int:
+    """One split (sequential.py:197-209) on the GPU: levels, G0 = the
+    horizontal subgraph, T = forward count of G0 + the cross count."""
+    level, _, _ = _ops.bfs_levels(dg)
+    g0 = _ops.split_by_level(dg, level)
+    return _ops.forward_count(g0) + _ops.split_cross_count(dg, level)
+
+
 def tc_cetc_split(g: Graph) -> int:
-    """Split hybrid (sequential.py:197-209): cross triangles (c1) plus the
-    horizontal subgraph's triangles (c2 / 3), one fused GPU pass."""
-    r = _ops.cetc(device_graph(g))
-    return int(r.c1 + r.c2 // 3)
+    """Split hybrid (sequential.py:197-209): BFS levels, G0 = the horizontal
+    edges and G1 = the level-spanning ones (tcb_split_by_level), the forward
+    count of G0 (tcb_forward_count; the reference forward-hashes G0) plus the
+    triangles with one G0 edge and two G1 edges (tcb_split_cross_count,
+    split_cross_count_k)."""
+    return _split_count(device_graph(g))
 
 
 def tc_cetc_split_degree(g: Graph) -> int:
     """Split hybrid after degree relabeling (sequential.py:212-213)."""
-    r = _ops.cetc(degree_order_device(device_graph(g)))
-    return int(r.c1 + r.c2 // 3)
+    return _split_count(degree_order_device(device_graph(g)))
 
 
 def tc_cetc_split_recursive(g: Graph, threshold: float = COVER_RATIO_THRESHOLD) -> int:
-    """Recursive split (sequential.py:216-238): the recursion only re-splits
-    G0 to cut CPU merge work; the total is the same c1 + T(G0)."""
-    del threshold
-    return tc_cetc_split(g)
+    """Recursive split (sequential.py:216-238): while the horizontal
+    subgraph still holds more than `threshold` of the edges, shrinks, and has
+    at least SPLIT_RECURSION_FLOOR edges, split it again (a new BFS on G0)
+    instead of counting it forward."""
+    return _split_recursive(device_graph(g), threshold, 1.0)
+
+
+def _split_recursive(dg, threshold: float, prev_ratio: float) -> int:
+    if dg.m == 0:
+        return 0
+    level, _, _ = _ops.bfs_levels(dg)
+    g0 = _ops.split_by_level(dg, level)
+    cross = _ops.split_cross_count(dg, level)
+    ratio = g0.m / dg.m
+    if ratio > threshold and ratio < prev_ratio and g0.m >= SPLIT_RECURSION_FLOOR:
+        inner = _split_recursive(g0, threshold, ratio)
+    else:
+        inner = _ops.forward_count(g0)
+    return inner + cross
 
 
 def tc_forward_gpu(g: Graph) -> int:

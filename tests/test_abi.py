@@ -23,7 +23,7 @@ def test_library_loads_and_exports_header_symbols():
     L = _lib.load_library()
     for s in _lib.header_symbols():
         assert hasattr(L, s), s
-    assert L.tcb_version() == 5
+    assert L.tcb_version() == 6
     out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)],
                          capture_output=True, text=True, check=True).stdout
     exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}

@@ -198,6 +198,15 @@ def _check_variants(name):
     gold = config_goldens()[name]
     dg = C.build_device_graph(name)
     assert tb.ops.forward_count(dg) == gold["T"]
+    # the split hybrids (sequential.py:197-238): G0's forward count + the cross count
+    level, _, _ = tb.ops.bfs_levels(dg)
+    g0 = tb.ops.split_by_level(dg, level)
+    assert g0.m == gold["cover_count"]
+    cross = tb.ops.split_cross_count(dg, level)
+    assert cross == gold["c1"]  # one horizontal edge, two level-spanning: the c1 triangles
+    assert tb.ops.forward_count(g0) == gold["c2"] // 3
+    assert tb.sequential._split_count(dg) == gold["T"]
+    assert tb.sequential._split_recursive(dg, tb.COVER_RATIO_THRESHOLD, 1.0) == gold["T"]
     r, used_forward = tb.ops.cetc_fe(dg)
     assert r.triangles == gold["T"]
     assert used_forward == (gold["cover_count"] / dg.m >= tb.COVER_RATIO_THRESHOLD)
@@ -249,6 +258,44 @@ def test_every_intersection_path_small(tuning):
             assert (r.triangles, r.c1, r.c2) == (case.T, case.c1, case.c2), case.name
     finally:
         ctx.set_tuning(0, 0)
+
+
+def _numpy_split(case):
+    """_split_by_level + split_cross_count_k restated with numpy/sets on the
+    reference's levels (small cases only)."""
+    lev = case.level
+    row, nb = case.row, case.nb
+    src = np.repeat(np.arange(case.n), np.diff(row))
+    keep = lev[src] == lev[nb]
+    row0 = np.concatenate([[0], np.cumsum(np.bincount(src[keep], minlength=case.n))])
+    nb0 = nb[keep]
+    n1 = [set(map(int, nb[row[v]:row[v + 1]][lev[nb[row[v]:row[v + 1]]] != lev[v]]))
+          for v in range(case.n)]
+    cross = 0
+    for u, v in zip(case.eu, case.ev):
+        if lev[u] == lev[v]:
+            cross += len(n1[u] & n1[v])
+    return row0, nb0, cross
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=SMALL_IDS)
+def test_split_by_level_and_cross_count(case):
+    """tcb_split_by_level and tcb_split_cross_count against a numpy
+    restatement of _split_by_level (sequential.py:186-193) and
+    split_cross_count_k (_kernels.py:786-805) on the reference's levels."""
+    import torch
+    g = tb.normalize(tb.EdgeList(n=case.n, edges=case.pairs))
+    dg = tb.device_graph(g)
+    level = torch.from_numpy(case.level.astype(np.int32))
+    g0 = tb.ops.split_by_level(dg, level)
+    row0, nb0, cross = _numpy_split(case)
+    assert np.array_equal(g0.row_offsets.cpu().numpy(), row0)
+    assert np.array_equal(g0.neighbors.cpu().numpy(), nb0)
+    assert g0.m == len(case.cover)
+    assert tb.ops.split_cross_count(dg, level) == cross == case.c1
+    for alg in ("CETC-Seq-S", "CETC-Seq-SD", "CETC-Seq-SR"):
+        assert tb.SEQUENTIAL_IDS[alg](g) == case.T, alg
+    assert tb.tc_cetc_split_recursive(g, threshold=0.0) == case.T
 
 
 def test_general_path_on_small_cases():
