@@ -255,6 +255,121 @@ __device__ __forceinline__ void td_expand(const int64_t* __restrict__ row,
     }
 }
 
+// Two levels per grid barrier (thin, low-degree top-down levels: the
+// lattice's 2,047 levels are latency chains plus a barrier each).  From the
+// level-L frontier every neighbour w is LOWERED to L+1 (atomicMin on the
+// level as unsigned: unvisited, -1, is the largest value) and whoever lowers
+// it expands it at once, lowering its neighbours to L+2.  When the barrier
+// is reached every vertex at distance L+1 is adjacent to the frontier, so it
+// holds L+1 and was expanded exactly once (one lane sees the old value above
+// L+1); every vertex holding L+2 is adjacent to an L+1 vertex and not to the
+// frontier, so L+2 is its distance.  A vertex first lowered to L+2 is queued
+// for the next step; if it is later lowered to L+1 (a "demotion") its queue
+// entry is stale and harmless: all its neighbours already hold <= L+2 and
+// lowering them to L+3 does nothing.  n2 = pushes - demotions is the exact
+// size of the L+2 set.
+#ifndef TCB_BFS_TWO
+#define TCB_BFS_TWO 1  // low-degree path: frontier <= TCB_BFS_TWO x warps (0: off)
+#endif
+constexpr int TWO_SERIAL = 6;  // L+1 rows up to this long: expanded by their lane
+
+struct TwoAcc {
+    unsigned n1 = 0, deg1 = 0, n2 = 0;  // per thread; n2 wraps: pushes - demotions
+};
+
+__device__ __forceinline__ unsigned lower_level(int32_t* level, int w, unsigned l) {
+    return atomicMin(reinterpret_cast<unsigned*>(level) + w, l);
+}
+
+__device__ __forceinline__ void two_expand(const int64_t* __restrict__ row,
+                                           const int32_t* __restrict__ nb, int b, int e,
+                                           int32_t* level, int L, QEnt* nxt,
+                                           unsigned long long* qlen, TwoAcc& a,
+                                           unsigned long long& my_deg,
+                                           unsigned long long& my_dmax) {
+    const unsigned lane = lane_id();
+    const unsigned l1 = unsigned(L + 1), l2 = unsigned(L + 2);
+    for (int p0 = b; p0 < e; p0 += 32) {
+        const int p = p0 + int(lane);
+        int rw = 0, dw = 0;
+        unsigned old = 0;
+        if (p < e) {
+            const int w = nb[p];
+            rw = int(row[w]);
+            dw = int(row[w + 1]) - rw;
+            old = lower_level(level, w, l1);
+        }
+        // short rows: every lane its own w, one batch of loads and atomics.
+        // w's entries are loaded while its atomic is in flight (whether or not
+        // it was lowered), so the second hop starts with the compare.
+        int x[TWO_SERIAL];
+#pragma unroll
+        for (int j = 0; j < TWO_SERIAL; ++j) x[j] = p < e && j < dw ? nb[rw + j] : -1;
+        const bool low = p < e && old > l1;
+        if (low) {
+            a.n1 += 1;
+            a.deg1 += unsigned(dw);
+            if (old == l2) a.n2 -= 1;  // demoted: its L+2 queue entry is stale
+        }
+        const bool small = low && dw <= TWO_SERIAL;
+        if (__any_sync(0xffffffffu, small)) {
+            int rx[TWO_SERIAL], dx[TWO_SERIAL];
+            unsigned pm = 0;
+#pragma unroll
+            for (int j = 0; j < TWO_SERIAL; ++j) {
+                rx[j] = dx[j] = 0;
+                if (small && x[j] >= 0) {
+                    rx[j] = int(row[x[j]]);
+                    dx[j] = int(row[x[j] + 1]) - rx[j];
+                    if (lower_level(level, x[j], l2) == 0xFFFFFFFFu) pm |= 1u << j;
+                }
+            }
+            const int c = __popc(pm);
+            const int inc = warp_inclusive_scan(c);
+            const int tot = __shfl_sync(0xffffffffu, inc, 31);
+            if (tot) {
+                unsigned long long base = 0;
+                if (lane == 31) base = atomicAdd(qlen, (unsigned long long)tot);
+                base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(inc - c);
+#pragma unroll
+                for (int j = 0; j < TWO_SERIAL; ++j) {
+                    if (!((pm >> j) & 1u)) continue;
+                    nxt[base++] = QEnt{x[j], dx[j], (long long)rx[j]};
+                    a.n2 += 1;
+                    my_deg += unsigned(dx[j]);
+                    my_dmax = max(my_dmax, (unsigned long long)dx[j]);
+                }
+            }
+        }
+        // longer rows: the warp expands them one at a time, lane per entry
+        unsigned big = __ballot_sync(0xffffffffu, low && dw > TWO_SERIAL);
+        while (big) {
+            const int sl = __ffs(big) - 1;
+            big &= big - 1;
+            const int bb = __shfl_sync(0xffffffffu, rw, sl);
+            const int ee = bb + __shfl_sync(0xffffffffu, dw, sl);
+            for (int q0 = bb; q0 < ee; q0 += 32) {
+                const int q = q0 + int(lane);
+                bool claim = false;
+                int xv = 0, rxv = 0, dxv = 0;
+                if (q < ee) {
+                    xv = nb[q];
+                    rxv = int(row[xv]);
+                    dxv = int(row[xv + 1]) - rxv;
+                    claim = lower_level(level, xv, l2) == 0xFFFFFFFFu;
+                }
+                const unsigned long long slot = warp_append(claim, qlen);
+                if (claim) {
+                    nxt[slot] = QEnt{xv, dxv, (long long)rxv};
+                    a.n2 += 1;
+                    my_deg += unsigned(dxv);
+                    my_dmax = max(my_dmax, (unsigned long long)dxv);
+                }
+            }
+        }
+    }
+}
+
 // Does v (row [b, e)) have a neighbour in the frontier bitmap?  int4 loads,
 // the four bit tests of a load issued together; stops at the first hit.
 __device__ __forceinline__ bool bu_scan(const int32_t* __restrict__ nb, int64_t b, int64_t e,
@@ -322,7 +437,7 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
     k_bfs_coop(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                int32_t* level, QEnt* qa, QEnt* qb, int2* chunks, DevCounters* C,
                int64_t dir_edges, const unsigned long long* dir_edges_p, BfsBits bits,
-               int* rest, int* parent, int collect) {
+               int* rest, int* parent, int collect, int two_max) {
     cg::grid_group grid = cg::this_grid();
     // 2m < 2^31 (require_sizes): every count below fits 32 bits, which
     // keeps the persistent kernel within 64 registers (2 CTAs per SM)
@@ -331,10 +446,11 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
     const int gwarp = gtid >> 5;
     const int nwarps = gthreads >> 5;
     const unsigned lane = lane_id();
-    __shared__ long long s_bc[3];  // per-block broadcast of the level counters
-    __shared__ unsigned long long s_agg[3][BFS_WPB];  // per-warp level counters
+    __shared__ long long s_bc[6];  // per-block broadcast of the level counters
+    __shared__ unsigned long long s_agg[6][BFS_WPB];  // per-warp level counters
 
-    int L = 0;
+    int L = 0;  // level of the current frontier
+    int s = 0;  // step (counter slots rotate by step; a two-level step is one)
     // the seed's counters, read once per block (all threads loading one
     // address serialise in its L2 slice)
     if (threadIdx.x == 0) {
@@ -357,18 +473,31 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
     if (collect && gtid == 0) C->bfs_t0 = globaltimer_ns();
 
     while (nf > 0) {
-        const int sc = L % 3, sn = (L + 1) % 3;
-        // Slot (L+2)%3 is written by step L+1 (after the next barrier) and was
-        // last read right after barrier L-1, so clear it during this step.
+        const int sc = s % 3, sn = (s + 1) % 3;
+        // Slot (s+2)%3 is written by step s+1 (after the next barrier) and was
+        // last read right after barrier s-1, so clear it during this step.
         if (gtid == 0) {
-            const int sr = (L + 2) % 3;
+            const int sr = (s + 2) % 3;
             C->q_len[sr] = 0;
             C->deg_sum[sr] = 0;
             C->deg_max[sr] = 0;
             C->nchunks[sr] = 0;
+            C->two_n1[sr] = 0;
+            C->two_n2[sr] = 0;
+            C->two_deg1[sr] = 0;
         }
         unsigned long long my_deg = 0, my_dmax = 0, my_cnt = 0;
-        if (td) {
+        TwoAcc ta;
+        // block-uniform: every block reads the same broadcast counters
+        const bool two = two_max > 0 && td && dmax <= BFS_LOWDEG &&
+                         int64_t(nf) <= int64_t(nwarps) * two_max;
+        if (two) {
+            for (int i = gwarp; i < nf; i += nwarps) {
+                const QEnt q = cur[i];
+                two_expand(row, nb, int(q.b), int(q.b) + q.d, level, L, nxt, &C->q_len[sn], ta,
+                           my_deg, my_dmax);
+            }
+        } else if (td) {
             const bool heavy = dmax > BFS_HEAVY;
             for (int i = gwarp; i < nf; i += nwarps) {
                 const QEnt q = cur[i];
@@ -412,24 +541,45 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
         my_cnt = warp_sum(my_cnt);
         // one atomic per block per counter (not per warp): on thin levels
         // same-address atomics, not work, set the level's length
+        const int nagg = two ? 6 : 3;
         if (lane == 0) {
             s_agg[0][threadIdx.x >> 5] = my_deg;
             s_agg[1][threadIdx.x >> 5] = my_dmax;
             s_agg[2][threadIdx.x >> 5] = my_cnt;
         }
+        if (two) {
+            // n2 as a signed per-thread difference, widened before the sums
+            const unsigned long long a1 = warp_sum((unsigned long long)ta.n1);
+            const unsigned long long a2 =
+                warp_sum((unsigned long long)(long long)int(ta.n2));
+            const unsigned long long a3 = warp_sum((unsigned long long)ta.deg1);
+            if (lane == 0) {
+                s_agg[3][threadIdx.x >> 5] = a1;
+                s_agg[4][threadIdx.x >> 5] = a2;
+                s_agg[5][threadIdx.x >> 5] = a3;
+            }
+        }
         __syncthreads();
         if (threadIdx.x < 32) {
             const int k = int(threadIdx.x);
-            unsigned long long a = k < BFS_WPB ? s_agg[0][k] : 0ull;
-            unsigned long long b = k < BFS_WPB ? s_agg[1][k] : 0ull;
-            unsigned long long c = k < BFS_WPB ? s_agg[2][k] : 0ull;
-            a = warp_sum(a);
-            b = warp_max_u64(b);
-            c = warp_sum(c);
+            unsigned long long v[6];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) v[r] = r < nagg && k < BFS_WPB ? s_agg[r][k] : 0ull;
+            v[0] = warp_sum(v[0]);
+            v[1] = warp_max_u64(v[1]);
+            v[2] = warp_sum(v[2]);
+            if (two) {
+                v[3] = warp_sum(v[3]);
+                v[4] = warp_sum(v[4]);
+                v[5] = warp_sum(v[5]);
+            }
             if (k == 0) {
-                if (a) atomicAdd(&C->deg_sum[sn], a);
-                if (b) atomicMax(&C->deg_max[sn], b);
-                if (c) atomicAdd(&C->q_len[sn], c);
+                if (v[0]) atomicAdd(&C->deg_sum[sn], v[0]);
+                if (v[1]) atomicMax(&C->deg_max[sn], v[1]);
+                if (v[2]) atomicAdd(&C->q_len[sn], v[2]);
+                if (v[3]) atomicAdd(&C->two_n1[sn], v[3]);
+                if (v[4]) atomicAdd(&C->two_n2[sn], v[4]);
+                if (v[5]) atomicAdd(&C->two_deg1[sn], v[5]);
             }
         }
 
@@ -439,42 +589,63 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
             s_bc[0] = (long long)ld_volatile_u64(&C->q_len[sn]);
             s_bc[1] = (long long)ld_volatile_u64(&C->deg_sum[sn]);
             s_bc[2] = (long long)ld_volatile_u64(&C->deg_max[sn]);
+            if (two) {
+                s_bc[3] = (long long)ld_volatile_u64(&C->two_n1[sn]);
+                s_bc[4] = (long long)ld_volatile_u64(&C->two_n2[sn]);
+                s_bc[5] = (long long)ld_volatile_u64(&C->two_deg1[sn]);
+            }
         }
         __syncthreads();
-        const int nf_next = int(s_bc[0]);
+        int nf_next = int(s_bc[0]);
         const int mf_next = int(s_bc[1]);
         dmax = int(s_bc[2]);
+        // levels this step produced: L+1 (and L+2 in a two-level step)
+        const int nlev = two ? 2 : 1;
+        const long long n1 = two ? s_bc[3] : nf_next;
+        const long long n2 = two ? s_bc[4] : 0;
+        const int deg1 = two ? int(s_bc[5]) : 0;
         __syncthreads();
+        if (two && n2 == 0) nf_next = 0;  // only stale entries queued
 #ifdef TCB_CHECKS
         if (gtid == 0 && (L < 40 || (L & 255) == 0)) {
             unsigned long long now;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
             printf("BFS L=%d mode=%s nf=%lld nf_next=%lld mf_next=%lld dmax=%lld t_ns=%llu\n", L,
-                   td ? "TD" : "BU", (long long)nf, (long long)nf_next, (long long)mf_next,
-                   (long long)dmax, now);
+                   two ? "TD2" : td ? "TD" : "BU", (long long)nf, (long long)nf_next,
+                   (long long)mf_next, (long long)dmax, now);
         }
 #endif
-        if (collect && gtid == 0 && L < TCB_LEVEL_RECORDS) {  // first BFS only
-            C->lev_rec[2 * L] = (td ? 0ull : 1ull << 62) | globaltimer_ns();
-            C->lev_rec[2 * L + 1] = (unsigned long long)nf_next;
-            C->nlev = L + 1;
+        if (collect && gtid == 0) {  // first BFS only
+            const unsigned long long t = (td ? 0ull : 1ull << 62) | globaltimer_ns();
+            if (L < TCB_LEVEL_RECORDS) {
+                C->lev_rec[2 * L] = t;
+                C->lev_rec[2 * L + 1] = (unsigned long long)(two ? n1 : nf_next);
+                C->nlev = L + 1;
+            }
+            if (two && L + 1 < TCB_LEVEL_RECORDS) {
+                C->lev_rec[2 * L + 2] = t;
+                C->lev_rec[2 * L + 3] = (unsigned long long)n2;
+                C->nlev = L + 2;
+            }
         }
-        if (nf_next > 0) max_level = L + 1;
-        mu -= mf_next;
+        if (n1 > 0) max_level = L + 1;
+        if (n2 > 0) max_level = L + 2;
+        mu -= deg1 + mf_next;
         bool next_td;
         if (td)
             next_td = !(mf_next > mu / BFS_ALPHA);
         else
             next_td = (nf_next < int(n / BFS_BETA)) && (nf_next < nf);
+        const int Lf = L + nlev;  // the next frontier's level
 
         if (nf_next > 0 && !next_td && td) {
-            // entering bottom-up: visited and level-(L+1) bitmaps from the levels
-            uint32_t* fn = bits.fb[(L + 1) & 1];
+            // entering bottom-up: visited and level-Lf bitmaps from the levels
+            uint32_t* fn = bits.fb[Lf & 1];
             for (int j = gwarp; j < int(bits.nw); j += nwarps) {
                 const int v = j * 32 + int(lane);
                 const int lv = v < n ? level[v] : 0;
                 const unsigned vm = __ballot_sync(0xffffffffu, lv != -1);
-                const unsigned fm = __ballot_sync(0xffffffffu, v < n && lv == L + 1);
+                const unsigned fm = __ballot_sync(0xffffffffu, v < n && lv == Lf);
                 if (lane == 0) {
                     bits.vis[j] = vm;
                     fn[j] = fm;
@@ -482,8 +653,8 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
             }
             grid.sync();
         } else if (nf_next > 0 && next_td && !td) {
-            // leaving bottom-up: the level-(L+1) frontier bitmap as a queue
-            const uint32_t* fn = bits.fb[(L + 1) & 1];
+            // leaving bottom-up: the level-Lf frontier bitmap as a queue
+            const uint32_t* fn = bits.fb[Lf & 1];
             unsigned long long* qc = &C->scratch[4];
             for (int j = gwarp; j < int(bits.nw); j += nwarps) {
                 const uint32_t fm = fn[j];
@@ -506,7 +677,8 @@ __global__ void __launch_bounds__(BFS_BLOCK, TCB_BFS_MINB)
         }
         td = next_td;
         nf = nf_next;
-        ++L;
+        L = Lf;
+        ++s;
     }
     if (gtid == 0 && max_level) atomicMax(&C->max_level, max_level);
     if (!collect) return;
@@ -609,7 +781,7 @@ __global__ void k_rest_seed(const int64_t* __restrict__ row, const int* __restri
 static void launch_bfs(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n,
                        int32_t* level, QEnt* qa, QEnt* qb, int2* chunks, int64_t dir_edges,
                        const unsigned long long* dir_edges_p, BfsBits bits, int* rest,
-                       int* parent, int collect) {
+                       int* parent, int collect, int two_max) {
     DevCounters* C = ctx->d_counters;
     if (ctx->bfs_coop_blocks == 0) {
         int per_sm = 0;
@@ -620,7 +792,7 @@ static void launch_bfs(Context* ctx, const int64_t* row, const int32_t* nb, int6
     void* args[] = {(void*)&row,   (void*)&nb,          (void*)&n,    (void*)&level,
                     (void*)&qa,    (void*)&qb,          (void*)&chunks, (void*)&C,
                     (void*)&dir_edges, (void*)&dir_edges_p, (void*)&bits,  (void*)&rest,
-                    (void*)&parent, (void*)&collect};
+                    (void*)&parent, (void*)&collect, (void*)&two_max};
     TCB_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_coop, dim3(ctx->bfs_coop_blocks),
                                          dim3(BFS_BLOCK), args, 0, ctx->stream));
     ctx->launches++;
@@ -890,7 +1062,7 @@ __global__ void k_max_degree(const int64_t* __restrict__ row, int64_t n,
 // case reads the max degree back: one ~10 us round trip on graphs larger
 // than 2^17 edges.
 void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
-                int64_t n, int64_t m, int32_t* level, bool reset_counters);
+                int64_t n, int64_t m, int32_t* level, bool reset_counters, int two_max);
 #ifndef TCB_LOWDEG_MAX
 #define TCB_LOWDEG_MAX 32  // ER-like graphs up to mean degree ~16 (tools/path_probe.py)
 #endif
@@ -910,7 +1082,8 @@ bool small_cetc(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n, 
         if (dmax > (unsigned long long)LOWDEG_MAX) return false;
         // low degree, large: the general BFS (direction-optimising, block-
         // aggregated level counters) for the levels, then the count kernel
-        bfs_levels(ctx, row, nb, nullptr, n, m, level, false);  // events 0, 1, 2
+        // (two levels per grid barrier on its thin levels: every row is short)
+        bfs_levels(ctx, row, nb, nullptr, n, m, level, false, TCB_BFS_TWO);  // events 0, 1, 2
         ctx->record(3);
         TCB_LAUNCH(ctx, k_lowdeg_count, ctx->num_sms * 8, 256, 0, row, nb, int(n),
                    (const int32_t*)level, ctx->d_counters);
@@ -944,7 +1117,7 @@ bool small_cetc(Context* ctx, const int64_t* row, const int32_t* nb, int64_t n, 
 }
 
 void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32_t* src,
-                int64_t n, int64_t m, int32_t* level, bool reset_counters) {
+                int64_t n, int64_t m, int32_t* level, bool reset_counters, int two_max) {
     (void)src;
     require(n < (int64_t(1) << 31), "vertex ids must fit int32");
     DevCounters* C = ctx->d_counters;
@@ -962,15 +1135,19 @@ void bfs_levels(Context* ctx, const int64_t* row, const int32_t* nb, const int32
         BfsBits bits{bw, {bw + nw, bw + 2 * nw}, nw};
         int2* chunks = ctx->wsT<int2>(WS_MISC, 2 * m / BFS_HEAVY + n + 1);
         int* rest = reinterpret_cast<int*>(qb);  // free once the first BFS is done
-        launch_bfs(ctx, row, nb, n, level, qa, qb, chunks, 2 * m, nullptr, bits, rest, parent, 1);
+        launch_bfs(ctx, row, nb, n, level, qa, qb, chunks, 2 * m, nullptr, bits, rest, parent, 1,
+                   two_max);
         // the remainder (kernels exit at once when the first BFS saw everything)
         TCB_LAUNCH(ctx, k_rest_hook, grid_for(ctx, n, 256), 256, 0, row, nb, (const int*)rest,
                    (const DevCounters*)C, parent);
-        TCB_CUDA(cudaMemsetAsync(&C->q_len[0], 0, 12 * sizeof(unsigned long long), ctx->stream));
+        TCB_CUDA(cudaMemsetAsync(&C->q_len[0], 0,
+                                 size_t(reinterpret_cast<char*>(&C->two_deg1[3]) -
+                                        reinterpret_cast<char*>(&C->q_len[0])),
+                                 ctx->stream));
         TCB_LAUNCH(ctx, k_rest_seed, grid_for(ctx, n, 256), 256, 0, row, (const int*)rest, parent,
                    level, qa, C);
         launch_bfs(ctx, row, nb, n, level, qa, qb, chunks, 0, &C->rest_deg, bits, rest, parent,
-                   0);
+                   0, two_max);
     }
     ctx->record(2);
 }

@@ -20,7 +20,7 @@ bool small_cetc(Context*, const int64_t*, const int32_t*, int64_t, int64_t, int3
 void split_by_level(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
                     const int32_t*, int64_t*, int32_t*, int32_t*, int64_t*);
 void bfs_levels(Context*, const int64_t*, const int32_t*, const int32_t*, int64_t, int64_t,
-                int32_t*, bool);
+                int32_t*, bool, int two_max = 0);
 void cover_select(Context*, const int32_t*, const int32_t*, const int32_t*, int64_t, int32_t*,
                   int32_t*, int64_t*);
 void bfs_parent(Context*, const int64_t*, const int32_t*, int64_t, const int32_t*, int64_t,

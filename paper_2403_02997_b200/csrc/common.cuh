@@ -86,6 +86,10 @@ struct DevCounters {
     unsigned long long deg_sum[3];
     unsigned long long deg_max[3];       // largest degree in the next frontier
     unsigned long long nchunks[3];       // heavy-vertex chunks queued this level
+    // two-level steps (bfs.cu): vertices lowered to L+1, the exact size of
+    // the L+2 set (pushes minus demotions, two's complement), degree sum of
+    // the L+1 set
+    unsigned long long two_n1[3], two_n2[3], two_deg1[3];
     // components (bfs.cu): the lowest non-isolated id as n - v (max-reduced,
     // 0 = none), the probe's finished-block count, and the vertices the
     // first BFS left unvisited (count, degree sum)
