@@ -86,12 +86,19 @@ constexpr int WT = TCB_WT;            // warp tier: owner degree <= WT
 constexpr int W_SLOTS = 4 * WT;       // per-warp bucket table: load <= 1/4
 constexpr int W_WARPS = 8;
 constexpr int PW = TCB_PW;            // partners per warp item
-constexpr int C_THREADS = 512;        // 2 CTAs per SM
+#ifndef TCB_C_THREADS
+#define TCB_C_THREADS 512
+#endif
+constexpr int C_THREADS = TCB_C_THREADS;  // 512: 2 CTAs per SM
 constexpr int HC = TCB_HC;            // staged ids per CTA item
 #ifndef TCB_C_SLOTS
 #define TCB_C_SLOTS 16384
 #endif
 constexpr int C_SLOTS = TCB_C_SLOTS;  // cuckoo slots (64 KB): load <= HC / C_SLOTS = 3/8
+#ifndef TCB_INSERT_U
+#define TCB_INSERT_U 4
+#endif
+constexpr int INSERT_U = TCB_INSERT_U;  // staged ids loaded per thread before their inserts
 constexpr int PC = 2 * C_THREADS;     // partners per CTA item
 constexpr int NSEG = 2 * PC;          // stream slices: partner t -> OFF slice t, UP slice PC + t
 constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per lane)
@@ -100,6 +107,10 @@ constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr int NBKT = 32;
+#ifndef TCB_UPCUT_ROUNDS
+#define TCB_UPCUT_ROUNDS 2
+#endif
+constexpr int UPCUT_ROUNDS = TCB_UPCUT_ROUNDS;  // interpolation windows before the binary search
 // Per-vertex partner record for the CTA tier: one 32-byte sector with the
 // list starts, the OFF size and the UP prefix counts of the degree buckets
 // CTA-tier owners have (|UP(v)| <= sqrt(2m) < 2^16 since 2m < 2^32).
@@ -272,6 +283,7 @@ struct Lists {
     const int* __restrict__ ucnt;   // [v*NBKT + k] = UP(v) entries with degree bucket >= k
     const PRec* __restrict__ prec;  // per-vertex partner record (CTA tier)
     int rshift;
+    int idmax;  // n: ids lie in [0, idmax)
     // The part of UP(p) that can hold an apex of owner x (degree bucket kx):
     // the entries ranked above x.  UP(p) is sorted by (degree bucket desc, id
     // asc), the owner order, so they are a prefix: the runs of buckets > kx
@@ -283,6 +295,45 @@ struct Lists {
 #endif
         if (hi - lo <= 1) return lo;  // the run is x alone
         uint32_t a = ub + uint32_t(lo), z = ub + uint32_t(hi);
+#ifndef TCB_UPCUT_BINARY
+        // Interpolation first: x is a member of the id-sorted run L[a, z), so
+        // one aligned 8-id window (a 32-byte sector) around the interpolated
+        // position usually holds it; otherwise the window's end values shrink
+        // the range and the id bounds.  After UPCUT_ROUNDS windows the binary
+        // search below finishes (skewed id distributions).  A binary search
+        // alone is log2(run) dependent sector reads per cover edge.
+        uint32_t va = 0, vz = uint32_t(idmax);  // ids of L[a, z) lie in [va, vz]
+#pragma unroll 1
+        for (int it = 0; it < UPCUT_ROUNDS && z - a > 1; ++it) {
+            const float f = float(uint32_t(x) - va) / float(max(vz - va, 1u));
+            const uint32_t est = min(a + uint32_t(f * float(z - a)), z - 1);
+            const uint32_t w0 = est & ~7u;
+            const int4 q0 = *reinterpret_cast<const int4*>(L + w0);
+            const int4 q1 = *reinterpret_cast<const int4*>(L + w0 + 4);
+            const int v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            int lt = 0, vmin = 0x7FFFFFFF, vmax = -1;
+            bool ge = false, le = false;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool ok = w0 + i >= a && w0 + i < z;
+                lt += ok && v[i] < x;
+                ge |= ok && v[i] >= x;
+                le |= ok && v[i] <= x;
+                if (ok) {
+                    vmin = min(vmin, v[i]);
+                    vmax = max(vmax, v[i]);
+                }
+            }
+            if (ge && le) return int(max(w0, a) + uint32_t(lt) - ub);  // x is in the window
+            if (!ge) {  // every valid id is below x
+                a = min(w0 + 8, z);
+                va = uint32_t(vmax);
+            } else {    // every valid id is above x
+                z = max(w0, a);
+                vz = uint32_t(vmin);
+            }
+        }
+#endif
         while (a < z) {
             const uint32_t mid = a + ((z - a) >> 1);
             if (L[mid] < x) a = mid + 1; else z = mid;
@@ -1153,6 +1204,33 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, con
     }
 }
 
+#ifdef TCB_TMA_STAGE
+// Measured variant: the owner's staged ids arrive by a TMA
+// bulk copy (cp.async.bulk, 1-D) in the stream-table area, which is idle
+// until the pass's table is built, and are hashed from shared memory.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+constexpr int STG_CAP = 4096;  // ints: the stream table's 16 KB
+#endif
+
 // Block-wide exclusive scan of a (int64, int) pair (one value per thread).
 __device__ __forceinline__ void block_scan_pair(int64_t a, int b, int64_t& ea, int& eb,
                                                 int64_t& ta, int& tb, int64_t* sa, int* sb) {
@@ -1208,6 +1286,15 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     __shared__ int s_fail;
     const int32_t* __restrict__ L = ls.L;
     const unsigned long long nitems = block_load(nitems_p);
+#ifdef TCB_TMA_STAGE
+    __shared__ __align__(8) uint64_t s_bar;
+    uint32_t tma_parity = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+#endif
 #ifdef TCB_NOSTREAM  // measurement-only variant: item setup and staging without streaming
     dbg |= 1;
 #endif
@@ -1301,6 +1388,24 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 TCB_DASSERT(len >= 1 && len <= HC);
                 BucketHash h;
                 h.setup(tab, C_SLOTS);
+#ifdef TCB_TMA_STAGE
+                // the pass's id ranges [A0, A1) and (single pass) [B0, B1) of L,
+                // widened to 16-byte boundaries for the bulk copies
+                const int64_t A0 = phase == 2 ? xo0 : p0 + cb;
+                const int64_t A1 = phase == 2 ? xo1 : p0 + cb + len;
+                const int64_t B0 = xs0, B1 = phase == 2 ? xs1 : xs0;
+                const int64_t a0 = A0 & ~int64_t(3), b0 = B0 & ~int64_t(3);
+                const int na = A1 > A0 ? int(((A1 + 3) & ~int64_t(3)) - a0) : 0;
+                const int nb2 = B1 > B0 ? int(((B1 + 3) & ~int64_t(3)) - b0) : 0;
+                const bool use_tma = na + nb2 <= STG_CAP;
+                int* stg = sg.start;
+                if (use_tma && threadIdx.x == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&s_bar, uint32_t(na + nb2) * 4u);
+                    if (na) bulk_g2s(stg, L + a0, uint32_t(na) * 4u, &s_bar);
+                    if (nb2) bulk_g2s(stg + na, L + b0, uint32_t(nb2) * 4u, &s_bar);
+                }
+#endif
                 for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = C_EMPTY;
                 if (threadIdx.x == 0) {
                     s_next = 0;
@@ -1309,15 +1414,38 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 __syncthreads();
                 CuckooHash ch;
                 ch.setup(tab, C_SLOTS);
+#ifdef TCB_TMA_STAGE
+                if (use_tma) {
+                    mbar_wait(&s_bar, tma_parity);
+                    tma_parity ^= 1u;
+                }
+                const int oa = int(A0 - a0), ob2 = na + int(B0 - b0);
+                auto owner_id = [&](int i) -> int {  // i-th staged id of this sub-chunk
+                    const int k = cb + i;
+                    if (use_tma) return phase == 2 ? (k < no ? stg[oa + k] : stg[ob2 + (k - no)]) : stg[oa + i];
+                    return phase == 2 ? (k < no ? L[xo0 + k] : L[xs0 + (k - no)]) : L[p0 + k];
+                };
+#else
                 auto owner_id = [&](int i) -> int {  // i-th staged id of this sub-chunk
                     const int k = cb + i;
                     return phase == 2 ? (k < no ? L[xo0 + k] : L[xs0 + (k - no)]) : L[p0 + k];
                 };
+#endif
+                // INSERT_U staged ids are loaded before their inserts (one
+                // exposed load latency per batch instead of one per id)
                 if (!(dbg & 2))
-                    for (int i = threadIdx.x; i < len; i += C_THREADS) {
-                        const int w = owner_id(i);
-                        if (!staged(vinfo, w, x, dx, fwd)) continue;
-                        if (!ch.insert(w)) s_fail = 1;
+                    for (int i0 = threadIdx.x; i0 < len; i0 += INSERT_U * C_THREADS) {
+                        int w[INSERT_U];
+#pragma unroll
+                        for (int q = 0; q < INSERT_U; ++q) {
+                            const int i = i0 + q * C_THREADS;
+                            w[q] = i < len ? owner_id(i) : -1;
+                        }
+#pragma unroll
+                        for (int q = 0; q < INSERT_U; ++q) {
+                            if (w[q] < 0 || !staged(vinfo, w[q], x, dx, fwd)) continue;
+                            if (!ch.insert(w[q])) s_fail = 1;
+                        }
                     }
                 if ((dbg & TCB_TEST_FORCE_FALLBACK) && threadIdx.x == 0) s_fail = 1;
                 // this pass's count from each slice of partners 2t, 2t+1
@@ -1408,7 +1536,9 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                     for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = EMPTY;
                     __syncthreads();
                     for (int i = threadIdx.x; i < len; i += C_THREADS) {
-                        const int w = owner_id(i);
+                        const int k = cb + i;  // from L: the stream table is built by now
+                        const int w =
+                            phase == 2 ? (k < no ? L[xo0 + k] : L[xs0 + (k - no)]) : L[p0 + k];
                         if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
                     }
                     __syncthreads();
@@ -1460,7 +1590,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
     int* split = ctx->wsT<int>(WS_COVER_V, size_t(n) * (F + 1));
-    int32_t* L = ctx->wsT<int32_t>(WS_LISTS, nnz);
+    int32_t* L = ctx->wsT<int32_t>(WS_LISTS, nnz + 8);  // + one up_cut window
     const size_t cls_bytes = (size_t(nwords + 1) * sizeof(uint2) + 15) / 16 * 16;
     char* cbuf = static_cast<char*>(
         ctx->ws(WS_CLASS, cls_bytes + 2 * size_t(nwords + 1) * sizeof(unsigned long long)));
@@ -1491,7 +1621,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     unsigned long long* fc = &C->scratch[8];
     int64_t* d_ncover = reinterpret_cast<int64_t*>(&C->ncover);
     const int rshift = max(0, bits_for(n) - LOG_F);
-    Lists ls{L, vb, split, ucnt, prec, rshift};
+    Lists ls{L, vb, split, ucnt, prec, rshift, int(n)};
 
     unsigned long long* nopack = &C->scratch[13];
     TCB_CUDA(cudaMemsetAsync(nopack, 0, sizeof(unsigned long long), ctx->stream));
