@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
 }
 
 #ifdef TCB_STATS  // measurement-only: CTA-tier work counters, printed per call
-__device__ unsigned long long g_cta_stats[8];  // items, passes, slices, elements, chunks, fast
+__device__ unsigned long long g_cta_stats[16];  // items, passes, slices, elements, chunks, fast
 #define TCB_STAT(i, v) atomicAdd(&g_cta_stats[i], (unsigned long long)(v))
 #else
 #define TCB_STAT(i, v) ((void)0)
@@ -1500,6 +1500,7 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                     TCB_STAT(3, total);
                     TCB_STAT(6, tn >> 16);
                     TCB_STAT(7, int(to >> 32));
+                    TCB_STAT(8 + lg, tsup);  // OFF elements by the owner's range-group level
                 }
                 {
                     int e_o = int(eo & 0xFFFFFFFF), e_s = tsup + int(eo >> 32);
@@ -1684,15 +1685,16 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     ctx->record(6);
 #ifdef TCB_STATS
     {
-        unsigned long long st[8];
+        unsigned long long st[16];
         TCB_CUDA(cudaStreamSynchronize(ctx->stream));
         TCB_CUDA(cudaMemcpyFromSymbol(st, g_cta_stats, sizeof(st)));
-        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const unsigned long long z[16] = {};
         TCB_CUDA(cudaMemcpyToSymbol(g_cta_stats, z, sizeof(z)));
         unsigned long long nci = 0;
         TCB_CUDA(cudaMemcpy(&nci, nc, sizeof(nci), cudaMemcpyDeviceToHost));
         fprintf(stderr, "CTA stats: items %llu passes %llu slices %llu (UP %llu) elements %llu (UP %llu) "
-                "chunks %llu fast %llu\n", nci, st[1], st[2], st[6], st[3], st[7], st[4], st[5]);
+                "chunks %llu fast %llu; OFF elements by lg: %llu %llu %llu %llu %llu %llu\n", nci, st[1],
+                st[2], st[6], st[3], st[7], st[4], st[5], st[8], st[9], st[10], st[11], st[12], st[13]);
     }
 #endif
     TCB_LAUNCH(ctx, k_isect_warp, ctx->isect_warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,
