@@ -35,6 +35,16 @@
 // Same-level neighbours ranked below the endpoint are never read, and a hit needs no level lookup: the
 // list it was streamed from says which tally it belongs to.
 //
+// UP lists hold RANKS, not ids: rank(v) = v's position in the owner order over
+// all vertices (k_rank_*: one stable counting pass by degree bucket), stored
+// with bit 31 set so no UP value equals an OFF id (the thread and warp tiers
+// keep both classes in one set).  Counting needs equality only, the sorted
+// UP list is then simply ascending, and everything ranked above an owner x
+// lies in [0, rank(x)): for a CTA-tier owner (degree > 256) that is the few
+// hundred thousand hubs, so UP(x) is staged as a BITMAP over [0, rank(x)) —
+// one shared-memory read per streamed element, exact, no hashing and no kick
+// chains — while OFF(x) keeps the cuckoo set.
+//
 //  1. owner bits: a keep bit per CSR entry (x, y) with level[x]==level[y] &&
 //     owns(x, y), and the OFF/UP class bits.  A word-level prefix of the keep
 //     bits compacts the kept entries in row order, so each owner's partners
@@ -53,10 +63,11 @@
 //     shard's partner blocks are listed (dist.py shard_of).
 //  5. k_isect_tiny / k_isect_warp: one thread / warp per item; the warp tier
 //     keeps a per-warp bucket hash of OFF(x) ∪ UP(x) (4-entry buckets).
-//  6. k_isect_cta: one CTA per item; the group's slice of OFF(x) (and, in
-//     group 0, UP(x)) staged in a two-table cuckoo set; the partners' slices
-//     (two per partner) are flattened into one element stream (block scan of
-//     lengths) that warps consume in CHUNK-element grabs.
+//  6. k_isect_cta: one CTA per item; the group's slice of OFF(x) staged in a
+//     two-table cuckoo set and, in group 0, UP(x) in a rank bitmap beside it;
+//     the partners' slices (two per partner) are flattened into one element
+//     stream (block scan of lengths; the UP part starts at a CHUNK multiple)
+//     that warps consume in CHUNK-element grabs, each of one class.
 //
 // Forward mode (fwd, tcb_forward_count): every entry is classed OFF, owners
 // stage only the neighbours ranked above them, and every hit is a triangle
@@ -65,6 +76,7 @@
 #include "scan.cuh"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace tcb {
 
@@ -106,6 +118,8 @@ constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+constexpr uint32_t UP_TAG = 0x80000000u;  // UP lists hold UP_TAG | rank (never EMPTY: rank < n < 2^31 - 1)
+constexpr int PAD = -1;                   // padding key of a partial chunk (== EMPTY: never a value)
 constexpr int NBKT = 32;
 #ifndef TCB_UPCUT_ROUNDS
 #define TCB_UPCUT_ROUNDS 2
@@ -283,52 +297,56 @@ struct Lists {
     const int* __restrict__ ucnt;   // [v*NBKT + k] = UP(v) entries with degree bucket >= k
     const PRec* __restrict__ prec;  // per-vertex partner record (CTA tier)
     int rshift;
-    int idmax;  // n: ids lie in [0, idmax)
-    // The part of UP(p) that can hold an apex of owner x (degree bucket kx):
-    // the entries ranked above x.  UP(p) is sorted by (degree bucket desc, id
-    // asc), the owner order, so they are a prefix: the runs of buckets > kx
-    // ([0, lo)) plus the ids below x in bucket kx's run [lo, hi) — a binary
-    // search (x itself sits in that run: it is p's same-level neighbour).
-    __device__ __forceinline__ int up_cut(uint32_t ub, int lo, int hi, int x) const {
-#ifdef TCB_UPCUT_BUCKET  // measurement-only: stream the whole bucket-kx run
-        return hi;           // (over-streams; counts unchanged: no false hits)
-#endif
+    const uint32_t* __restrict__ rnk;  // rnk[v] = UP_TAG | rank of v in the owner order
+    const int* __restrict__ rb;        // bucket k's ranks: [rb[31 - k], rb[32 - k])
+    // UP values of bucket k lie in [rank_lo(k), rank_hi(k)) (tagged)
+    __device__ __forceinline__ uint32_t rank_lo(int k) const { return UP_TAG | uint32_t(rb[31 - k]); }
+    __device__ __forceinline__ uint32_t rank_hi(int k) const { return UP_TAG | uint32_t(rb[32 - k]); }
+    // The part of UP(p) that can hold an apex of owner x (degree bucket kx,
+    // tagged rank xk): the entries ranked above x.  UP(p) ascends in rank, so
+    // they are a prefix: the runs of buckets > kx ([0, lo), from the ucnt
+    // table) plus the ranks below xk in bucket kx's run [lo, hi) — a search
+    // (x itself sits in that run: it is p's same-level neighbour).  Tagged
+    // ranks compare like the ranks, signed or unsigned (bit 31 set in all).
+    // [va, vz): the rank range of bucket kx (rank_lo / rank_hi).
+    __device__ __forceinline__ int up_cut(uint32_t ub, int lo, int hi, int xk, uint32_t va,
+                                          uint32_t vz) const {
         if (hi - lo <= 1) return lo;  // the run is x alone
         uint32_t a = ub + uint32_t(lo), z = ub + uint32_t(hi);
 #ifndef TCB_UPCUT_BINARY
-        // Interpolation first: x is a member of the id-sorted run L[a, z), so
-        // one aligned 8-id window (a 32-byte sector) around the interpolated
-        // position usually holds it; otherwise the window's end values shrink
-        // the range and the id bounds.  After UPCUT_ROUNDS windows the binary
-        // search below finishes (skewed id distributions).  A binary search
-        // alone is log2(run) dependent sector reads per cover edge.
-        uint32_t va = 0, vz = uint32_t(idmax);  // ids of L[a, z) lie in [va, vz]
+        // Interpolation first: xk is a member of the sorted run L[a, z), whose
+        // ranks spread over the bucket's range, so one aligned 8-value window
+        // (a 32-byte sector) around the interpolated position usually holds
+        // it; otherwise the window's end values shrink the range and the
+        // value bounds.  After UPCUT_ROUNDS windows the binary search below
+        // finishes.  A binary search alone is log2(run) dependent sector
+        // reads per cover edge.
 #pragma unroll 1
         for (int it = 0; it < UPCUT_ROUNDS && z - a > 1; ++it) {
-            const float f = float(uint32_t(x) - va) / float(max(vz - va, 1u));
+            const float f = float(uint32_t(xk) - va) / float(max(vz - va, 1u));
             const uint32_t est = min(a + uint32_t(f * float(z - a)), z - 1);
             const uint32_t w0 = est & ~7u;
             const int4 q0 = *reinterpret_cast<const int4*>(L + w0);
             const int4 q1 = *reinterpret_cast<const int4*>(L + w0 + 4);
             const int v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-            int lt = 0, vmin = 0x7FFFFFFF, vmax = -1;
+            int lt = 0, vmin = 0x7FFFFFFF, vmax = int(0x80000000u);
             bool ge = false, le = false;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const bool ok = w0 + i >= a && w0 + i < z;
-                lt += ok && v[i] < x;
-                ge |= ok && v[i] >= x;
-                le |= ok && v[i] <= x;
+                lt += ok && v[i] < xk;
+                ge |= ok && v[i] >= xk;
+                le |= ok && v[i] <= xk;
                 if (ok) {
                     vmin = min(vmin, v[i]);
                     vmax = max(vmax, v[i]);
                 }
             }
-            if (ge && le) return int(max(w0, a) + uint32_t(lt) - ub);  // x is in the window
-            if (!ge) {  // every valid id is below x
+            if (ge && le) return int(max(w0, a) + uint32_t(lt) - ub);  // xk is in the window
+            if (!ge) {  // every valid value is below xk
                 a = min(w0 + 8, z);
                 va = uint32_t(vmax);
-            } else {    // every valid id is above x
+            } else {    // every valid value is above xk
                 z = max(w0, a);
                 vz = uint32_t(vmin);
             }
@@ -336,14 +354,14 @@ struct Lists {
 #endif
         while (a < z) {
             const uint32_t mid = a + ((z - a) >> 1);
-            if (L[mid] < x) a = mid + 1; else z = mid;
+            if (L[mid] < xk) a = mid + 1; else z = mid;
         }
         return int(a - ub);
     }
-    __device__ __forceinline__ int up_cut(int64_t p, int kx, int x) const {
+    __device__ __forceinline__ int up_cut(int64_t p, int kx, int xk) const {
         const int hi = ucnt[p * NBKT + kx];
         const int lo = kx + 1 < NBKT ? ucnt[p * NBKT + kx + 1] : 0;
-        return up_cut(vb[p].y, lo, hi, x);
+        return up_cut(vb[p].y, lo, hi, xk, rank_lo(kx), rank_hi(kx));
     }
 };
 
@@ -437,6 +455,82 @@ __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restri
     }
 }
 
+// Ranks in the owner order (degree bucket desc, id asc) over all vertices:
+// one stable counting pass by digit 31 - bucket over the ids in order, the
+// shape of a radix-sort pass (csr.cu) with the key implicit.  rnk[v] =
+// UP_TAG | rank; rb[d] = first rank of digit d (bucket 31 - d), rb[32] = n.
+constexpr int RK_BLOCK = 256;
+constexpr int RK_WARPS = RK_BLOCK / 32;
+constexpr int RK_ROUNDS = 16;
+constexpr int64_t RK_TILE = int64_t(RK_BLOCK) * RK_ROUNDS;
+__global__ void __launch_bounds__(RK_BLOCK)
+    k_rank_hist(const uint8_t* __restrict__ dbk, int64_t n, int64_t* __restrict__ hist,
+                int64_t ntiles) {
+    __shared__ unsigned h[NBKT];
+    if (threadIdx.x < NBKT) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = int64_t(blockIdx.x) * RK_TILE;
+#pragma unroll 4
+    for (int j = 0; j < RK_ROUNDS; ++j) {
+        const int64_t i = base + int64_t(j) * RK_BLOCK + threadIdx.x;
+        const unsigned d = i < n ? 31u - dbk[i] : unsigned(NBKT);
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d < NBKT && lane_id() == unsigned(__ffs(peers) - 1))
+            atomicAdd(&h[d], unsigned(__popc(peers)));
+    }
+    __syncthreads();
+    if (threadIdx.x < NBKT) hist[int64_t(threadIdx.x) * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(RK_BLOCK)
+    k_rank_assign(const uint8_t* __restrict__ dbk, int64_t n, const int64_t* __restrict__ offs,
+                  int64_t ntiles, uint32_t* __restrict__ rnk, int* __restrict__ rb) {
+    __shared__ unsigned cnt[RK_WARPS][NBKT + 1];
+    __shared__ int64_t base_off[NBKT];
+    const int w = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    for (int i = threadIdx.x; i < RK_WARPS * (NBKT + 1); i += RK_BLOCK) (&cnt[0][0])[i] = 0;
+    if (threadIdx.x < NBKT) {
+        base_off[threadIdx.x] = offs[int64_t(threadIdx.x) * ntiles + blockIdx.x];
+        if (blockIdx.x == 0) rb[threadIdx.x] = int(offs[int64_t(threadIdx.x) * ntiles]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) rb[NBKT] = int(n);
+    __syncthreads();
+    // warp w owns the contiguous run [wbase, wbase + 32 RK_ROUNDS) of the
+    // tile: (round, lane) is id order
+    const int64_t wbase = int64_t(blockIdx.x) * RK_TILE + int64_t(w) * 32 * RK_ROUNDS;
+    unsigned dig[RK_ROUNDS], pos[RK_ROUNDS];
+#pragma unroll
+    for (int r = 0; r < RK_ROUNDS; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        const unsigned d = i < n ? 31u - dbk[i] : unsigned(NBKT);
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned old = cnt[w][d];
+        __syncwarp();
+        if (lane == unsigned(__ffs(peers) - 1)) cnt[w][d] = old + __popc(peers);
+        __syncwarp();
+        dig[r] = d;
+        pos[r] = old + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+    if (threadIdx.x < NBKT) {  // per digit: exclusive prefix over the warps
+        unsigned run = 0;
+#pragma unroll
+        for (int ww = 0; ww < RK_WARPS; ++ww) {
+            const unsigned t = cnt[ww][threadIdx.x];
+            cnt[ww][threadIdx.x] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RK_ROUNDS; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        if (i < n)
+            rnk[i] = UP_TAG | uint32_t(base_off[dig[r]] + cnt[w][dig[r]] + pos[r]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // 2. OFF / UP lists.  The OFF array comes first; UP starts at NOFF (the
 //    class total, pre[nw] low half).  ob/sb hold absolute positions in L.
@@ -526,8 +620,8 @@ static_assert(NBKT == 32, "one degree bucket per lane");
 __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
     k_build_up(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                const uint2* __restrict__ cls, const uint8_t* __restrict__ dbk,
-               const uint2* __restrict__ vb, int32_t* __restrict__ L, int* __restrict__ ucnt,
-               PRec* __restrict__ prec) {
+               const uint32_t* __restrict__ rnk, const uint2* __restrict__ vb,
+               int32_t* __restrict__ L, int* __restrict__ ucnt, PRec* __restrict__ prec) {
     __shared__ int s_h[UP_WARPS][NBKT];
     __shared__ int s_w[UP_WARPS][UP_SHORT];
     __shared__ uint8_t s_b[UP_WARPS][UP_SHORT];
@@ -585,7 +679,7 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
                     const int w = nb[e];
                     const int b = dbk[w];
                     const int q = nbuf + __popc(bal & lanemask_lt());
-                    s_w[warp][q] = w;
+                    s_w[warp][q] = int(rnk[w]);  // the list holds tagged ranks
                     s_b[warp][q] = uint8_t(b);
                     atomicAdd(&h[b], 1);
                 }
@@ -619,7 +713,7 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
         // bits is then taken by the whole warp (lane = bit), so entries are
         // visited in row order with coalesced loads and a hub row with few UP
         // entries costs d/1024 iterations.
-        auto up_words = [&](auto&& visit) {
+        auto up_words = [&](auto want_rank, auto&& visit) {
             for (int64_t jb = j0; jb <= j1; jb += 32) {
                 const int64_t j = jb + lane;
                 uint32_t m = 0;
@@ -647,13 +741,17 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
                         w[q] = (upm >> q) & 1u ? nb[(jb + sl[q]) * 32 + lane] : 0;
 #pragma unroll
                     for (int q = 0; q < UPW; ++q) b[q] = (upm >> q) & 1u ? int(dbk[w[q]]) : 0;
+                    if (decltype(want_rank)::value) {  // the scatter pass writes tagged ranks
+#pragma unroll
+                        for (int q = 0; q < UPW; ++q) w[q] = (upm >> q) & 1u ? int(rnk[w[q]]) : 0;
+                    }
 #pragma unroll
                     for (int q = 0; q < UPW; ++q) visit(((upm >> q) & 1u) != 0, w[q], b[q]);
                 }
             }
         };
         // pass 1: bucket histogram
-        up_words([&](bool up, int, int b) {
+        up_words(std::false_type{}, [&](bool up, int, int b) {
             if (up) atomicAdd(&h[b], 1);
         });
         __syncwarp();
@@ -672,7 +770,7 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
         h[lane] = incl - c;
         __syncwarp();
         // pass 2: stable scatter (row order within each bucket)
-        up_words([&](bool up, int w, int b) {
+        up_words(std::true_type{}, [&](bool up, int w, int b) {
             const int pos = stable_slot(h, up, b);
             if (up) L[int64_t(u0) + pos] = w;
         });
@@ -789,10 +887,12 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
             continue;
         }
         // fewest range groups G (power of two <= F) whose OFF slices all fit
-        // HC; group 0 also stages UP(x) (not range-split: it is degree-sorted)
+        // HC; group 0 also stages UP(x) (not range-split: it is rank-sorted)
+        // (UP(x) is staged beside them as a rank bitmap, or after them in
+        // rank windows: it takes no table slots)
         const int* sx = ls.split + x * (F + 1);
         int lg = 0;
-        if (st > hc) {
+        if (st - nup > hc) {
             for (lg = 1; lg < LOG_F; ++lg) {
                 const int step = F >> lg;
                 int mx = 0;
@@ -842,18 +942,19 @@ __global__ void __launch_bounds__(256)
         const int no = int(o1 - o0), nx = no + int(ls.ub(x + 1) - s0);
         const int dx = vinfo[x].y;
         const int kx = dbucket(dx);
+        const int xk = nx > no ? int(ls.rnk[x]) : 0;  // tagged rank: the UP cut's key
         int a[TINY];
 #pragma unroll
         for (int i = 0; i < TINY; ++i) {
-            int w = -1;
+            int w = PAD;
             if (i < nx) w = i < no ? ls.L[o0 + i] : ls.L[s0 + (i - no)];
-            if (w >= 0 && !staged(vinfo, w, x, dx, fwd)) w = -1;
+            if (w != PAD && !staged(vinfo, w, x, dx, fwd)) w = PAD;
             a[i] = w;
         }
         for (int64_t p = item.y; p < item.z; ++p) {
             const int y = P[p];
             const int64_t y0 = ls.ob(y), y1 = ls.ob(y + 1), y2 = ls.ub(y);
-            const int64_t y3 = y2 + (nx > no ? ls.up_cut(y, kx, x) : 0);
+            const int64_t y3 = y2 + (nx > no ? ls.up_cut(y, kx, xk) : 0);
             for (int64_t j = y0; j < y1; ++j) {
                 const int w = ls.L[j];
                 bool hit = false;
@@ -902,7 +1003,7 @@ __device__ __forceinline__ void warp_stream(const int32_t* __restrict__ L, const
 #pragma unroll
         for (int j = 0; j < JW; ++j) {
             const int i = i0 + 32 * j;
-            w[j] = -1;
+            w[j] = PAD;
             if (i < c1) {
                 if (nx <= i) {
                     do {
@@ -919,7 +1020,7 @@ __device__ __forceinline__ void warp_stream(const int32_t* __restrict__ L, const
         uint32_t hm = 0;
 #pragma unroll
         for (int j = 0; j < JW; ++j)
-            if (w[j] >= 0 && h.hit(w[j])) hm |= 1u << j;
+            if (w[j] != PAD && h.hit(w[j])) hm |= 1u << j;
         const int jt = (tsup - i0 + 31) >> 5;  // elements j >= jt are UP
         const uint32_t sm = jt <= 0 ? ~0u : (jt >= JW ? 0u : ~0u << jt);
         const uint32_t sup = __popc(hm & sm);
@@ -1055,9 +1156,10 @@ __device__ unsigned long long g_cta_stats[16];  // items, passes, slices, elemen
 // Every partner t has two unread slices, OFF at index t and UP at PC + t
 // (s_pos / s_len).  Each pass takes a count from every slice, and the
 // non-empty ones are compacted into the stream table (SegTab): all OFF slices
-// first, then all UP slices, so an element's class is just
-// (stream index >= tsup) and a walk never steps over an empty slice
-// (uint32 list arithmetic; 2m < 2^32).
+// first, then all UP slices from the next CHUNK multiple on, so every chunk
+// a warp grabs is of one class (OFF: probe the cuckoo set; UP: probe the
+// rank bitmap) and a walk never steps over an empty slice (uint32 list
+// arithmetic; 2m < 2^32).
 
 // The stream table lives in two int arrays (start[k] = first stream index of
 // slice k, base[k] = its base: element i of slice k is L[base[k] + i]), so
@@ -1083,27 +1185,45 @@ __device__ __forceinline__ int find_segment(const int* start, int nseg, int c0) 
 }
 static_assert(31 * 65 + 64 >= NSEG - 1, "find_segment covers NSEG slices");
 
-// Probe w[0..J): all += hits, sup += hits of elements j >= jt (UP).  The
-// first-step reads of a batch of B keys are issued before any second step.
+// UP(x) of a CTA-tier owner as a bitmap over a window of ranks: bit
+// (rank - window base) of bm.  Everything in UP(x), and everything a partner
+// streams against it (the exact cut), ranks above x, so the window [0,
+// rank(x)) holds them all: one LDS.32 per probe, exact, nothing to hash.
+struct BitmapSet {
+    uint32_t* bm;
+    uint32_t wbase;  // UP_TAG | first rank of the window (a multiple of 32)
+    static constexpr bool kNegSafe = false;  // a padding key indexes outside the window
+    __device__ __forceinline__ void set(int key) const {
+        const uint32_t i = uint32_t(key) - wbase;
+        atomicOr(&bm[i >> 5], 1u << (i & 31));
+    }
+    __device__ __forceinline__ uint32_t first(int key) const {
+        return bm[(uint32_t(key) - wbase) >> 5];
+    }
+    __device__ __forceinline__ uint32_t second(int key, uint32_t v) const {
+        return (v >> (uint32_t(key) & 31u)) & 1u;
+    }
+};
+
+// Probe w[0..J): hits += members.  The first-step reads of a batch of B keys
+// are issued before any second step.  GUARD: the chunk may hold PAD keys.
 template <int J, bool GUARD, typename Probe>
-__device__ __forceinline__ void probe_all(const Probe& h, int (&w)[J], int jt,
-                                          uint32_t& all, uint32_t& sup) {
+__device__ __forceinline__ void probe_all(const Probe& h, int (&w)[J], uint32_t& hits) {
 #ifndef TCB_PROBE_B
 #define TCB_PROBE_B 8
 #endif
     constexpr int B = TCB_PROBE_B;
+    constexpr bool SKIP = GUARD && !Probe::kNegSafe;
 #pragma unroll
     for (int j0 = 0; j0 < J; j0 += B) {
         uint32_t v[B];
 #pragma unroll
-        for (int q = 0; q < B; ++q) v[q] = h.first(w[j0 + q]);
+        for (int q = 0; q < B; ++q) v[q] = SKIP && w[j0 + q] == PAD ? 0u : h.first(w[j0 + q]);
 #pragma unroll
         for (int q = 0; q < B; ++q) {
             const int j = j0 + q;
-            if (GUARD && !Probe::kNegSafe && w[j] < 0) continue;
-            const uint32_t hv = h.second(w[j], v[q]);
-            all += hv;
-            sup += j >= jt ? hv : 0u;
+            if (SKIP && w[j] == PAD) continue;
+            hits += h.second(w[j], v[q]);
         }
     }
 }
@@ -1113,12 +1233,10 @@ __device__ __forceinline__ void probe_all(const Probe& h, int (&w)[J], int jt,
 // elements.  FULL: the chunk holds CHUNK elements (no bounds checks).
 template <bool FULL, typename Probe>
 __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const SegTab& sg,
-                                            int nseg, int k0, int c0, int c1, int tsup,
-                                            const Probe& h, uint32_t& co, uint32_t& cs) {
+                                            int nseg, int k0, int c0, int c1, const Probe& h,
+                                            uint32_t& hits) {
     constexpr int J = CHUNK / 32;
     const int i0 = c0 + int(lane_id());
-    // this lane's elements j >= jt come from UP slices (stream index >= tsup)
-    const int jt = min(J, max(0, (tsup - i0 + 31) >> 5));
     int w[J];
     int k = k0;
     int nx = sg.start[k + 1];
@@ -1126,7 +1244,7 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int i = i0 + 32 * j;
-        w[j] = -1;
+        w[j] = PAD;
         if (FULL || i < c1) {
             if (nx <= i) {
                 do {
@@ -1143,20 +1261,59 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
 #endif
         }
     }
-    uint32_t all = 0, sup = 0;
-    probe_all<J, !FULL>(h, w, jt, all, sup);
-    co += all - sup;
-    cs += sup;
+    probe_all<J, !FULL>(h, w, hits);
 }
 
-// Warps consume the flattened stream in CHUNK grabs.  A chunk that lies
-// inside one slice takes a warp-uniform fast path with coalesced loads and
-// no per-element bookkeeping.
+// One chunk [c0, c1) of one class.  A chunk that lies inside one slice takes
+// a warp-uniform fast path with coalesced loads and no per-element
+// bookkeeping.
+template <typename Probe>
+__device__ __forceinline__ uint32_t chunk_hits(const int32_t* __restrict__ L, const SegTab& sg,
+                                               int nseg, int c0, int c1, const Probe& h) {
+    constexpr int J = CHUNK / 32;
+    const int lane = int(lane_id());
+    const int k0 = find_segment(sg.start, nseg, c0);
+    const int e1 = sg.start[k0 + 1];
+    if (lane == 0) {
+        TCB_STAT(4, 1);
+        TCB_STAT(5, e1 >= c1 ? 1 : 0);
+    }
+    TCB_DASSERT(k0 >= 0 && k0 < nseg && sg.start[k0] <= c0 && c0 < e1);
+    uint32_t hits = 0;
+    if (e1 >= c1) {
+        // fast path: one slice
+        const uint32_t base = sg.base[k0] + uint32_t(c0 + lane);
+        const int32_t* p = L + base;
+        int w[J];
+        if (c1 - c0 == CHUNK) {
+#ifdef TCB_NOLOAD
+#pragma unroll
+            for (int j = 0; j < J; ++j) w[j] = int(((base + 32u * j) * 2654435761u) >> 8);
+#else
+#pragma unroll
+            for (int j = 0; j < J; ++j) w[j] = p[32 * j];
+#endif
+            probe_all<J, false>(h, w, hits);
+        } else {
+#pragma unroll
+            for (int j = 0; j < J; ++j) w[j] = c0 + lane + 32 * j < c1 ? p[32 * j] : PAD;
+            probe_all<J, true>(h, w, hits);
+        }
+    } else if (c1 - c0 == CHUNK) {
+        cross_chunk<true>(L, sg, nseg, k0, c0, c1, h, hits);
+    } else {
+        cross_chunk<false>(L, sg, nseg, k0, c0, c1, h, hits);
+    }
+    return hits;
+}
+
+// Warps consume the flattened stream in CHUNK grabs: [0, tsup) are the OFF
+// slices, [roundup(tsup, CHUNK), total) the UP slices, so a grab (a CHUNK
+// multiple) never mixes the classes.
 template <typename Probe>
 __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, const SegTab& sg,
                                               int nseg, int total, int tsup, int* s_next,
-                                              const Probe& h, Tally& tl) {
-    constexpr int J = CHUNK / 32;
+                                              const Probe& h, const BitmapSet& bm, Tally& tl) {
     TCB_DASSERT(nseg <= NSEG && total >= 0);
     const int lane = int(lane_id());
     while (true) {
@@ -1164,72 +1321,10 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, con
         if (lane == 0) c0 = atomicAdd(s_next, CHUNK);
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (c0 >= total) break;
-        const int c1 = min(total, c0 + CHUNK);
-        const int k0 = find_segment(sg.start, nseg, c0);
-        const int e1 = sg.start[k0 + 1];
-        if (lane == 0) {
-            TCB_STAT(4, 1);
-            TCB_STAT(5, e1 >= c1 ? 1 : 0);
-        }
-        TCB_DASSERT(k0 >= 0 && k0 < nseg && sg.start[k0] <= c0 && c0 < e1);
-        uint32_t co = 0, cs = 0;
-        if (e1 >= c1) {
-            // fast path: one slice
-            const uint32_t base = sg.base[k0] + uint32_t(c0 + lane);
-            const int32_t* p = L + base;
-            int w[J];
-            uint32_t hits = 0, dummy = 0;
-            if (c1 - c0 == CHUNK) {
-#ifdef TCB_NOLOAD
-#pragma unroll
-                for (int j = 0; j < J; ++j) w[j] = int(((base + 32u * j) * 2654435761u) >> 8);
-#else
-#pragma unroll
-                for (int j = 0; j < J; ++j) w[j] = p[32 * j];
-#endif
-                            probe_all<J, false>(h, w, J, hits, dummy);
-            } else {
-#pragma unroll
-                for (int j = 0; j < J; ++j) w[j] = c0 + lane + 32 * j < c1 ? p[32 * j] : -1;
-                            probe_all<J, true>(h, w, J, hits, dummy);
-            }
-            if (c0 >= tsup) cs = hits; else co = hits;
-        } else if (c1 - c0 == CHUNK) {
-            cross_chunk<true>(L, sg, nseg, k0, c0, c1, tsup, h, co, cs);
-        } else {
-            cross_chunk<false>(L, sg, nseg, k0, c0, c1, tsup, h, co, cs);
-        }
-        tl.c1 += co;
-        tl.sup += cs;
+        if (c0 >= tsup) tl.sup += chunk_hits(L, sg, nseg, c0, min(total, c0 + CHUNK), bm);
+        else tl.c1 += chunk_hits(L, sg, nseg, c0, min(tsup, c0 + CHUNK), h);
     }
 }
-
-#ifdef TCB_TMA_STAGE
-// Measured variant: the owner's staged ids arrive by a TMA
-// bulk copy (cp.async.bulk, 1-D) in the stream-table area, which is idle
-// until the pass's table is built, and are hashed from shared memory.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return uint32_t(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                     "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    }
-}
-constexpr int STG_CAP = 4096;  // ints: the stream table's 16 KB
-#endif
 
 // Block-wide exclusive scan of a (int64, int) pair (one value per thread).
 __device__ __forceinline__ void block_scan_pair(int64_t a, int b, int64_t& ea, int& eb,
@@ -1265,15 +1360,23 @@ __device__ __forceinline__ void block_scan_pair(int64_t a, int b, int64_t& ea, i
     tb = sb[NW];
 }
 
+// Cuckoo slots for len staged ids: a power of two with load <= 3/8
+// (len <= HC -> <= C_SLOTS).
+__device__ __forceinline__ int cuckoo_slots(int len) {
+    return len == 0 ? 0 : max(64, 1 << ceil_log2_dev((len * 8 + 2) / 3));
+}
+static_assert((HC * 8 + 2) / 3 <= C_SLOTS, "HC ids fit the table at load 3/8");
+
 #ifndef TCB_CTA_PER_SM
 #define TCB_CTA_PER_SM 2
 #endif
 __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     k_isect_cta(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                 Lists ls, const int32_t* __restrict__ P, unsigned long long* fetch,
-                DevCounters* C, int hc, int dbg, const int2* __restrict__ vinfo, int fwd) {
+                DevCounters* C, int hc, int bmw_cap, int dbg, const int2* __restrict__ vinfo,
+                int fwd) {
     extern __shared__ uint4 smem4[];
-    uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS
+    uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS: cuckoo set | bitmap
     SegTab sg;                                                    // stream table
     sg.start = reinterpret_cast<int*>(tab + C_SLOTS);             // NSEG + 1
     sg.base = reinterpret_cast<uint32_t*>(sg.start + NSEG + 1);   // NSEG + 1
@@ -1286,15 +1389,6 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     __shared__ int s_fail;
     const int32_t* __restrict__ L = ls.L;
     const unsigned long long nitems = block_load(nitems_p);
-#ifdef TCB_TMA_STAGE
-    __shared__ __align__(8) uint64_t s_bar;
-    uint32_t tma_parity = 0;
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-#endif
 #ifdef TCB_NOSTREAM  // measurement-only variant: item setup and staging without streaming
     dbg |= 1;
 #endif
@@ -1319,6 +1413,11 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         const int no = int(xo1 - xo0), ns = int(xs1 - xs0);
         const int dx = vinfo[x].y;
         const int kx = dbucket(dx);
+        // x's tagged rank: every value of UP(x), and every value a partner
+        // streams against it, is below it
+        const uint32_t xk = ns ? ls.rnk[x] : UP_TAG;
+        const uint32_t xr = xk & ~UP_TAG;
+        const uint32_t va0 = ns ? ls.rank_lo(kx) : 0u, vz0 = ns ? ls.rank_hi(kx) : 0u;
         const int np = int(item.z - item.y);
         // partners t and t + C_THREADS of this thread: both ids are loaded
         // before either partner's rows, so the two dependent chains overlap
@@ -1360,7 +1459,7 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                         hi = ls.ucnt[int64_t(y) * NBKT + kx];
                         lo = kx + 1 < NBKT ? ls.ucnt[int64_t(y) * NBKT + kx + 1] : 0;
                     }
-                    ucut = ls.up_cut(hd.y, lo, hi, x);
+                    ucut = ls.up_cut(hd.y, lo, hi, int(xk), va0, vz0);
                 }
                 s_len[PC + t] = ucut;
 #ifdef TCB_NOUPSTREAM  // measurement-only: drop the UP slices
@@ -1371,184 +1470,216 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
 #endif
             }
         }
-        // Passes: one when both owner slices fit the table; otherwise the
-        // OFF slice then UP(x), each in sub-chunks of hc ids.  An OFF
-        // sub-chunk [.., vhi] is matched against every partner's next unread
-        // OFF part (id-sorted); every UP sub-chunk sees the partners' whole UP
-        // prefixes (degree-sorted, so not split by id; each apex still sits in
-        // exactly one sub-chunk).
-        const bool single = no + ns <= hc;
-        for (int phase = single ? 2 : 0; phase < 3; ++phase) {
-            if (phase == 2 && !single) break;
-            const int64_t p0 = phase == 1 ? xs0 : xo0;
-            const int64_t p1 = phase == 0 ? xo1 : xs1;  // phase 2: [xo0, xo1) ∪ [xs0, xs1)
-            const int plen = phase == 2 ? no + ns : int(p1 - p0);
-            for (int cb = 0; cb < plen; cb += hc) {
-                const int len = min(hc, plen - cb);
-                TCB_DASSERT(len >= 1 && len <= HC);
-                BucketHash h;
-                h.setup(tab, C_SLOTS);
-#ifdef TCB_TMA_STAGE
-                // the pass's id ranges [A0, A1) and (single pass) [B0, B1) of L,
-                // widened to 16-byte boundaries for the bulk copies
-                const int64_t A0 = phase == 2 ? xo0 : p0 + cb;
-                const int64_t A1 = phase == 2 ? xo1 : p0 + cb + len;
-                const int64_t B0 = xs0, B1 = phase == 2 ? xs1 : xs0;
-                const int64_t a0 = A0 & ~int64_t(3), b0 = B0 & ~int64_t(3);
-                const int na = A1 > A0 ? int(((A1 + 3) & ~int64_t(3)) - a0) : 0;
-                const int nb2 = B1 > B0 ? int(((B1 + 3) & ~int64_t(3)) - b0) : 0;
-                const bool use_tma = na + nb2 <= STG_CAP;
-                int* stg = sg.start;
-                if (use_tma && threadIdx.x == 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_expect_tx(&s_bar, uint32_t(na + nb2) * 4u);
-                    if (na) bulk_g2s(stg, L + a0, uint32_t(na) * 4u, &s_bar);
-                    if (nb2) bulk_g2s(stg + na, L + b0, uint32_t(nb2) * 4u, &s_bar);
-                }
-#endif
-                for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = C_EMPTY;
-                if (threadIdx.x == 0) {
-                    s_next = 0;
-                    s_fail = 0;
-                }
-                __syncthreads();
-                CuckooHash ch;
-                ch.setup(tab, C_SLOTS);
-#ifdef TCB_TMA_STAGE
-                if (use_tma) {
-                    mbar_wait(&s_bar, tma_parity);
-                    tma_parity ^= 1u;
-                }
-                const int oa = int(A0 - a0), ob2 = na + int(B0 - b0);
-                auto owner_id = [&](int i) -> int {  // i-th staged id of this sub-chunk
-                    const int k = cb + i;
-                    if (use_tma) return phase == 2 ? (k < no ? stg[oa + k] : stg[ob2 + (k - no)]) : stg[oa + i];
-                    return phase == 2 ? (k < no ? L[xo0 + k] : L[xs0 + (k - no)]) : L[p0 + k];
-                };
-#else
-                auto owner_id = [&](int i) -> int {  // i-th staged id of this sub-chunk
-                    const int k = cb + i;
-                    return phase == 2 ? (k < no ? L[xo0 + k] : L[xs0 + (k - no)]) : L[p0 + k];
-                };
-#endif
-                // INSERT_U staged ids are loaded before their inserts (one
-                // exposed load latency per batch instead of one per id)
-                if (!(dbg & 2))
-                    for (int i0 = threadIdx.x; i0 < len; i0 += INSERT_U * C_THREADS) {
-                        int w[INSERT_U];
-#pragma unroll
-                        for (int q = 0; q < INSERT_U; ++q) {
-                            const int i = i0 + q * C_THREADS;
-                            w[q] = i < len ? owner_id(i) : -1;
-                        }
-#pragma unroll
-                        for (int q = 0; q < INSERT_U; ++q) {
-                            if (w[q] < 0 || !staged(vinfo, w[q], x, dx, fwd)) continue;
-                            if (!ch.insert(w[q])) s_fail = 1;
-                        }
+        // Passes.  One (phase 2) when the cuckoo set of the OFF slice and the
+        // bitmap of [0, rank(x)) fit the table area side by side — hubs have
+        // small ranks, low-degree owners few OFF ids.  Otherwise the OFF
+        // slice in sub-chunks of hc ids (phase 0: a sub-chunk [.., vhi] is
+        // matched against every partner's next unread OFF part, id-sorted),
+        // then UP(x) in rank windows of the whole area (phase 1: a window is
+        // matched against every partner's next unread UP part, rank-sorted).
+        const int bw = ns ? int((((xr + 31u) >> 5) + 3u) & ~3u) : 0;  // bitmap words of [0, xr)
+        const int cs1 = cuckoo_slots(min(no, HC));
+        const bool single = no <= hc && (ns == 0 || (bw <= bmw_cap && cs1 + bw <= C_SLOTS));
+        int phase = single ? 2 : 0;
+        int cb = 0;        // phase 0: staged OFF ids done
+        uint32_t wb = 0;   // phase 1: the window's first rank
+        int ud = 0;        // phase 1: staged UP values done
+        while (true) {
+            if (phase == 0 && cb >= no) phase = 1;
+            if (phase == 1 && (ns == 0 || wb >= xr)) break;
+            // this pass: OFF ids L[ob0, ob0 + olen) in a cuckoo set of cs
+            // slots, UP values L[ub0, ub0 + ulen) in a bitmap of bwn words
+            // over the ranks [wb, wend)
+            int64_t ob0 = xo0, ub0 = xs0;
+            int olen = 0, ulen = 0, cs = 0, bwn = 0;
+            uint32_t wend = xr;
+            bool last = true;
+            if (phase == 2) {
+                olen = no;
+                ulen = ns;
+                cs = cs1;
+                bwn = bw;
+            } else if (phase == 0) {
+                ob0 = xo0 + cb;
+                olen = min(hc, no - cb);
+                cs = cuckoo_slots(olen);
+                last = cb + olen >= no;
+            } else {
+                wend = min(xr, wb + 32u * uint32_t(bmw_cap));
+                bwn = int((((wend - wb + 31u) >> 5) + 3u) & ~3u);
+                last = wend >= xr;
+                ub0 = xs0 + ud;
+                if (last) {
+                    ulen = ns - ud;
+                } else {  // the staged values below the window's end
+                    int64_t lo = ub0, hi = xs1;
+                    const int key = int(UP_TAG | wend);
+                    while (lo < hi) {
+                        const int64_t mid = lo + ((hi - lo) >> 1);
+                        if (L[mid] < key) lo = mid + 1; else hi = mid;
                     }
-                if ((dbg & TCB_TEST_FORCE_FALLBACK) && threadIdx.x == 0) s_fail = 1;
-                // this pass's count from each slice of partners 2t, 2t+1
-                // (slots 0, 1: OFF; 2, 3: UP), then the stream table
-                const bool last = cb + len >= plen;
-                const bool consume = phase != 1 || last;  // UP prefixes are re-streamed
-                const int vhi = phase == 2 ? 0 : L[p0 + cb + len - 1];
-                int cnt[4];
-                int slot[4];
-                {
-                    const int t2 = 2 * threadIdx.x;
-                    slot[0] = t2;
-                    slot[1] = t2 + 1;
-                    slot[2] = PC + t2;
-                    slot[3] = PC + t2 + 1;
+                    ulen = int(lo - ub0);
+                }
+            }
+            TCB_DASSERT(olen <= HC && cs + bwn <= C_SLOTS);
+            {
+                uint4* t4 = reinterpret_cast<uint4*>(tab);
+                const uint4 e4 = make_uint4(C_EMPTY, C_EMPTY, C_EMPTY, C_EMPTY);
+                for (int i = threadIdx.x; i < (cs >> 2); i += C_THREADS) t4[i] = e4;
+                uint4* b4 = reinterpret_cast<uint4*>(tab + cs);
+                for (int i = threadIdx.x; i < (bwn >> 2); i += C_THREADS)
+                    b4[i] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            if (threadIdx.x == 0) {
+                s_next = 0;
+                s_fail = 0;
+            }
+            __syncthreads();
+            CuckooHash ch;
+            ch.setup(tab, max(cs, 64));
+            BucketHash h;
+            h.setup(tab, max(cs, 64));
+            const BitmapSet bm{tab + cs, UP_TAG | wb};
+            // INSERT_U staged values are loaded before their inserts (one
+            // exposed load latency per batch instead of one per value)
+            if (!(dbg & 2)) {
+                for (int i0 = threadIdx.x; i0 < olen; i0 += INSERT_U * C_THREADS) {
+                    int w[INSERT_U];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int k = slot[r];
-                        int c = 0;
-                        if ((k & (PC - 1)) < np) {
-                            const int ln = s_len[k];
-                            if (phase == 2 || (ln > 0 && (r >> 1) == phase && (last || phase == 1))) {
-                                c = ln;
-                            } else if (ln > 0 && (r >> 1) == phase) {
-                                // OFF ids <= vhi in the unread part
-                                uint32_t lo = s_pos[k], hi = s_pos[k] + uint32_t(ln);
-                                while (lo < hi) {
-                                    const uint32_t mid = lo + ((hi - lo) >> 1);
-                                    if (L[mid] <= vhi) lo = mid + 1; else hi = mid;
-                                }
-                                c = int(lo - s_pos[k]);
+                    for (int q = 0; q < INSERT_U; ++q) {
+                        const int i = i0 + q * C_THREADS;
+                        w[q] = i < olen ? L[ob0 + i] : PAD;
+                    }
+#pragma unroll
+                    for (int q = 0; q < INSERT_U; ++q) {
+                        if (w[q] == PAD || !staged(vinfo, w[q], x, dx, fwd)) continue;
+                        if (!ch.insert(w[q])) s_fail = 1;
+                    }
+                }
+                for (int i0 = threadIdx.x; i0 < ulen; i0 += INSERT_U * C_THREADS) {
+                    int w[INSERT_U];
+#pragma unroll
+                    for (int q = 0; q < INSERT_U; ++q) {
+                        const int i = i0 + q * C_THREADS;
+                        w[q] = i < ulen ? L[ub0 + i] : PAD;
+                    }
+#pragma unroll
+                    for (int q = 0; q < INSERT_U; ++q) {
+                        if (w[q] == PAD) continue;
+                        TCB_DASSERT(uint32_t(w[q]) >= bm.wbase &&
+                                    uint32_t(w[q]) - bm.wbase < 32u * uint32_t(bwn));
+                        bm.set(w[q]);
+                    }
+                }
+            }
+            if ((dbg & TCB_TEST_FORCE_FALLBACK) && threadIdx.x == 0) s_fail = 1;
+            // this pass's count from each slice of partners 2t, 2t+1
+            // (slots 0, 1: OFF; 2, 3: UP), then the stream table
+            const int vhi = phase == 0 && !last ? L[ob0 + olen - 1] : 0;
+            const int vend = int(UP_TAG | wend);
+            int cnt[4];
+            int slot[4];
+            {
+                const int t2 = 2 * threadIdx.x;
+                slot[0] = t2;
+                slot[1] = t2 + 1;
+                slot[2] = PC + t2;
+                slot[3] = PC + t2 + 1;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int k = slot[r];
+                    int c = 0;
+                    if ((k & (PC - 1)) < np) {
+                        const int ln = s_len[k];
+                        const int cls = r >> 1;  // 0: OFF slice, 1: UP slice
+                        if (phase == 2 || (ln > 0 && cls == phase && last)) {
+                            c = ln;
+                        } else if (ln > 0 && cls == phase) {
+                            // the unread part's OFF ids <= vhi / UP values
+                            // below the window's end
+                            uint32_t lo = s_pos[k], hi = s_pos[k] + uint32_t(ln);
+                            while (lo < hi) {
+                                const uint32_t mid = lo + ((hi - lo) >> 1);
+                                const int v = L[mid];
+                                if (cls ? v < vend : v <= vhi) lo = mid + 1; else hi = mid;
                             }
+                            c = int(lo - s_pos[k]);
                         }
-                        cnt[r] = c;
                     }
+                    cnt[r] = c;
                 }
-                int64_t eo;  // exclusive element prefix: OFF low 32 bits, UP high
-                int en;      // exclusive non-empty prefix: OFF low 16 bits, UP high
-                int64_t to;
-                int tn;
-                block_scan_pair(int64_t(cnt[0] + cnt[1]) | (int64_t(cnt[2] + cnt[3]) << 32),
-                                int(cnt[0] > 0) + int(cnt[1] > 0) +
-                                    ((int(cnt[2] > 0) + int(cnt[3] > 0)) << 16),
-                                eo, en, to, tn, s_ta, s_tb);
-                const int tsup = int(to & 0xFFFFFFFF);        // OFF elements come first
-                const int total = tsup + int(to >> 32);
-                const int noff = tn & 0xFFFF;
-                const int nseg = noff + (tn >> 16);
-                if (threadIdx.x == 0) {
-                    TCB_STAT(1, 1);
-                    TCB_STAT(2, nseg);
-                    TCB_STAT(3, total);
-                    TCB_STAT(6, tn >> 16);
-                    TCB_STAT(7, int(to >> 32));
-                    TCB_STAT(8 + lg, tsup);  // OFF elements by the owner's range-group level
-                }
-                {
-                    int e_o = int(eo & 0xFFFFFFFF), e_s = tsup + int(eo >> 32);
-                    int n_o = en & 0xFFFF, n_s = noff + (en >> 16);
+            }
+            int64_t eo;  // exclusive element prefix: OFF low 32 bits, UP high
+            int en;      // exclusive non-empty prefix: OFF low 16 bits, UP high
+            int64_t to;
+            int tn;
+            block_scan_pair(int64_t(cnt[0] + cnt[1]) | (int64_t(cnt[2] + cnt[3]) << 32),
+                            int(cnt[0] > 0) + int(cnt[1] > 0) +
+                                ((int(cnt[2] > 0) + int(cnt[3] > 0)) << 16),
+                            eo, en, to, tn, s_ta, s_tb);
+            const int tsup = int(to & 0xFFFFFFFF);  // OFF elements: [0, tsup)
+            const int tup = int(to >> 32);          // UP elements: [ubase, total)
+            const int ubase = tup ? (tsup + CHUNK - 1) / CHUNK * CHUNK : tsup;
+            const int total = ubase + tup;
+            const int noff = tn & 0xFFFF;
+            const int nseg = noff + (tn >> 16);
+            if (threadIdx.x == 0) {
+                TCB_STAT(1, 1);
+                TCB_STAT(2, nseg);
+                TCB_STAT(3, tsup + tup);
+                TCB_STAT(6, tn >> 16);
+                TCB_STAT(7, tup);
+                TCB_STAT(8 + lg, tsup);  // OFF elements by the owner's range-group level
+            }
+            {
+                int e_o = int(eo & 0xFFFFFFFF), e_s = ubase + int(eo >> 32);
+                int n_o = en & 0xFFFF, n_s = noff + (en >> 16);
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int c = cnt[r];
-                        if (c == 0) continue;
-                        const int k = slot[r];
-                        const bool isup = r >= 2;
-                        const int e = isup ? e_s : e_o;
-                        const int q = isup ? n_s : n_o;
-                        sg.start[q] = e;
-                        sg.base[q] = s_pos[k] - uint32_t(e);
-                        if (consume) {
-                            s_pos[k] += uint32_t(c);
-                            s_len[k] -= c;
-                        }
-                        if (isup) {
-                            e_s += c;
-                            ++n_s;
-                        } else {
-                            e_o += c;
-                            ++n_o;
-                        }
+                for (int r = 0; r < 4; ++r) {
+                    const int c = cnt[r];
+                    if (c == 0) continue;
+                    const int k = slot[r];
+                    const bool isup = r >= 2;
+                    const int e = isup ? e_s : e_o;
+                    const int q = isup ? n_s : n_o;
+                    sg.start[q] = e;
+                    sg.base[q] = s_pos[k] - uint32_t(e);
+                    s_pos[k] += uint32_t(c);
+                    s_len[k] -= c;
+                    if (isup) {
+                        e_s += c;
+                        ++n_s;
+                    } else {
+                        e_o += c;
+                        ++n_o;
                     }
-                    if (threadIdx.x == 0) {
-                        sg.start[nseg] = total;
-                        sg.base[nseg] = 0;
-                    }
+                }
+                if (threadIdx.x == 0) {
+                    sg.start[nseg] = total;
+                    sg.base[nseg] = 0;
+                }
+            }
+            __syncthreads();
+            if (s_fail) {  // rare: rebuild the OFF sub-chunk as a bucket table
+                for (int i = threadIdx.x; i < cs; i += C_THREADS) tab[i] = EMPTY;
+                __syncthreads();
+                for (int i = threadIdx.x; i < olen; i += C_THREADS) {
+                    const int w = L[ob0 + i];
+                    if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
                 }
                 __syncthreads();
-                if (s_fail) {  // rare: rebuild this sub-chunk as a bucket table
-                    for (int i = threadIdx.x; i < C_SLOTS; i += C_THREADS) tab[i] = EMPTY;
-                    __syncthreads();
-                    for (int i = threadIdx.x; i < len; i += C_THREADS) {
-                        const int k = cb + i;  // from L: the stream table is built by now
-                        const int w =
-                            phase == 2 ? (k < no ? L[xo0 + k] : L[xs0 + (k - no)]) : L[p0 + k];
-                        if (staged(vinfo, w, x, dx, fwd)) h.insert(w);
-                    }
-                    __syncthreads();
-                }
-                if (!(dbg & 1)) {
-                    if (!s_fail) stream_chunks(L, sg, nseg, total, tsup, &s_next, ch, tl);
-                    else stream_chunks(L, sg, nseg, total, tsup, &s_next, h, tl);
-                }
-                __syncthreads();
+            }
+            if (!(dbg & 1)) {
+                if (!s_fail) stream_chunks(L, sg, nseg, total, tsup, &s_next, ch, bm, tl);
+                else stream_chunks(L, sg, nseg, total, tsup, &s_next, h, bm, tl);
+            }
+            __syncthreads();
+            if (phase == 2) break;
+            if (phase == 0) {
+                cb += olen;
+            } else {
+                wb = wend;
+                ud += ulen;
             }
         }
         // an item whose staged slices are empty runs no pass: without this
@@ -1583,11 +1714,14 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     const int64_t nnz = 2 * m;
     require(nnz < (int64_t(1) << 32), "intersection: 2m must be below 2^32");
     const int64_t nwords = (nnz + 31) / 32;
-    // per vertex: int2 vinfo, packed key, degree bucket
-    char* mbuf = static_cast<char*>(ctx->ws(WS_MISC, size_t(n) * (8 + 4 + 1) + 64));
+    // per vertex: int2 vinfo, packed key, tagged rank, degree bucket; then the
+    // rank bounds of the buckets
+    char* mbuf = static_cast<char*>(ctx->ws(WS_MISC, size_t(n) * (8 + 4 + 4 + 1) + 256));
     int2* vinfo = reinterpret_cast<int2*>(mbuf);
     uint32_t* key32 = reinterpret_cast<uint32_t*>(mbuf + size_t(n) * 8);
-    uint8_t* dbk = reinterpret_cast<uint8_t*>(mbuf + size_t(n) * 12);
+    uint32_t* rnk = reinterpret_cast<uint32_t*>(mbuf + size_t(n) * 12);
+    uint8_t* dbk = reinterpret_cast<uint8_t*>(mbuf + size_t(n) * 16);
+    int* rb = reinterpret_cast<int*>(mbuf + (size_t(n) * 17 + 15) / 16 * 16);  // NBKT + 1
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
     int* split = ctx->wsT<int>(WS_COVER_V, size_t(n) * (F + 1));
@@ -1608,6 +1742,9 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     // tuning knobs (tcb_set_tuning; tests shrink them to reach every path)
     const int wt = ctx->tune_wt > 0 ? min(ctx->tune_wt, WT) : WT;
     const int hc = ctx->tune_hc > 0 ? max(4, min(ctx->tune_hc, HC)) : HC;
+    // bitmap words per UP pass: the whole table area; tests shrink it with hc
+    // (a multiple of 4) to reach the rank-window passes
+    const int bmw_cap = ctx->tune_hc > 0 ? min(C_SLOTS, (hc + 3) / 4 * 4) : C_SLOTS;
     const int tiny = min(TINY, wt);
     const int64_t wcap = n + m / PW + 1;
     const int64_t ccap = (2 * m / (wt + 1) + 2 + m / PC) * F;
@@ -1622,12 +1759,21 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     unsigned long long* fc = &C->scratch[8];
     int64_t* d_ncover = reinterpret_cast<int64_t*>(&C->ncover);
     const int rshift = max(0, bits_for(n) - LOG_F);
-    Lists ls{L, vb, split, ucnt, prec, rshift, int(n)};
+    Lists ls{L, vb, split, ucnt, prec, rshift, rnk, rb};
 
     unsigned long long* nopack = &C->scratch[13];
     TCB_CUDA(cudaMemsetAsync(nopack, 0, sizeof(unsigned long long), ctx->stream));
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo, key32, dbk,
                nopack);
+    if (!fwd && !xonly) {  // ranks in the owner order: the values of the UP lists
+        const int64_t ntiles = ceil_div(n, RK_TILE);
+        int64_t* hist = ctx->wsT<int64_t>(WS_SORT_HIST, size_t(NBKT) * ntiles);
+        TCB_LAUNCH(ctx, k_rank_hist, unsigned(ntiles), RK_BLOCK, 0, (const uint8_t*)dbk, n, hist,
+                   ntiles);
+        scan_inplace(ctx, hist, int64_t(NBKT) * ntiles, nullptr);
+        TCB_LAUNCH(ctx, k_rank_assign, unsigned(ntiles), RK_BLOCK, 0, (const uint8_t*)dbk, n,
+                   (const int64_t*)hist, ntiles, rnk, rb);
+    }
     TCB_CUDA(cudaMemsetAsync(cls + nwords, 0, sizeof(uint2), ctx->stream));
     const uint32_t* bits =
         owner_bits(ctx, src, nb, vinfo, key32, nopack, nnz, fwd | (xonly << 1), cls);
@@ -1653,7 +1799,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
                (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P);
     TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
-               (const uint8_t*)dbk, (const uint2*)vb, L, ucnt, prec);
+               (const uint8_t*)dbk, (const uint32_t*)rnk, (const uint2*)vb, L, ucnt, prec);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, n, SPLIT_WARPS * 32), SPLIT_WARPS * 32, 0, n,
                (const int32_t*)L,
                (const uint2*)vb, rshift, split);
@@ -1679,7 +1825,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     ctx->record(5);
     ctx->record(7);  // no separate hub kernel in this design: hub stage = 0
     TCB_LAUNCH(ctx, k_isect_cta, ctx->isect_cta_blocks, C_THREADS, csm, (const longlong4*)citems,
-               (const unsigned long long*)nc, ls, (const int32_t*)P, fc, C, hc,
+               (const unsigned long long*)nc, ls, (const int32_t*)P, fc, C, hc, bmw_cap,
                debug_flags() | ctx->test_flags,
                (const int2*)vinfo, fwd);
     ctx->record(6);
