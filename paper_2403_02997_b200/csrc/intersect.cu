@@ -888,6 +888,12 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         }
         // fewest range groups G (power of two <= F) whose OFF slices all fit
         // HC; group 0 also stages UP(x) (not range-split: it is rank-sorted)
+#ifdef TCB_ONLY_SMALL  // measurement-only: CTA items of small owners only
+        if (st > TCB_ONLY_SMALL) continue;
+#endif
+#ifdef TCB_ONLY_BIG  // measurement-only: CTA items of big owners only
+        if (st <= TCB_ONLY_BIG) continue;
+#endif
         // (UP(x) is staged beside them as a rank bitmap, or after them in
         // rank windows: it takes no table slots)
         const int* sx = ls.split + x * (F + 1);
@@ -1228,13 +1234,13 @@ __device__ __forceinline__ void probe_all(const Probe& h, int (&w)[J], uint32_t&
     }
 }
 
-// A chunk that crosses slice boundaries: each lane walks forward from the
-// chunk's first slice k0; a lane crosses a boundary in few of its J
-// elements.  FULL: the chunk holds CHUNK elements (no bounds checks).
-template <bool FULL, typename Probe>
-__device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const SegTab& sg,
-                                            int nseg, int k0, int c0, int c1, const Probe& h,
-                                            uint32_t& hits) {
+// A full chunk (CHUNK elements): each lane walks forward from the chunk's
+// first slice k0 (a lane crosses a boundary in few of its J elements; a
+// chunk inside one slice never does), all J loads in flight before the probes.
+template <typename Probe>
+__device__ __forceinline__ void full_chunk(const int32_t* __restrict__ L, const SegTab& sg,
+                                           int nseg, int k0, int c0, const Probe& h,
+                                           uint32_t& hits) {
     constexpr int J = CHUNK / 32;
     const int i0 = c0 + int(lane_id());
     int w[J];
@@ -1244,76 +1250,86 @@ __device__ __forceinline__ void cross_chunk(const int32_t* __restrict__ L, const
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int i = i0 + 32 * j;
-        w[j] = PAD;
-        if (FULL || i < c1) {
-            if (nx <= i) {
-                do {
-                    TCB_DASSERT(k + 1 < nseg);
-                    ++k;
-                    nx = sg.start[k + 1];
-                } while (nx <= i);
-                base = sg.base[k];
-            }
-#ifdef TCB_NOLOAD  // measurement-only variant: probe without streaming
-            w[j] = int(((base + uint32_t(i)) * 2654435761u) >> 8);
-#else
-            w[j] = L[base + uint32_t(i)];
-#endif
+        if (nx <= i) {
+            do {
+                TCB_DASSERT(k + 1 < nseg);
+                ++k;
+                nx = sg.start[k + 1];
+            } while (nx <= i);
+            base = sg.base[k];
         }
+#ifdef TCB_NOLOAD  // measurement-only variant: probe without streaming
+        w[j] = int(((base + uint32_t(i)) * 2654435761u) >> 8);
+#else
+        w[j] = L[base + uint32_t(i)];
+#endif
     }
-    probe_all<J, !FULL>(h, w, hits);
+    probe_all<J, false>(h, w, hits);
 }
 
-// One chunk [c0, c1) of one class.  A chunk that lies inside one slice takes
-// a warp-uniform fast path with coalesced loads and no per-element
-// bookkeeping.
+// The compact path — the last chunk of a class (fewer than CHUNK elements)
+// and every chunk of a pass whose cuckoo build failed (bucket table): rounds
+// of PART_U elements per lane, not unrolled across rounds.  Keeping these
+// rare cases out of the unrolled code keeps the kernel's hot loop small
+// (the instruction cache: DESIGN.md §8).
+constexpr int PART_U = 16;
+template <typename Probe>
+__device__ __forceinline__ void compact_chunk(const int32_t* __restrict__ L, const SegTab& sg,
+                                              int nseg, int k0, int c0, int c1, const Probe& h,
+                                              uint32_t& hits) {
+    constexpr int J = CHUNK / 32;
+    static_assert(J % PART_U == 0, "rounds of PART_U");
+    const int i0 = c0 + int(lane_id());
+    int k = k0;
+    int nx = sg.start[k + 1];
+    uint32_t base = sg.base[k];
+#pragma unroll 1
+    for (int j0 = 0; j0 < J && c0 + 32 * j0 < c1; j0 += PART_U) {
+        int w[PART_U];
+#pragma unroll
+        for (int q = 0; q < PART_U; ++q) {
+            const int i = i0 + 32 * (j0 + q);
+            w[q] = PAD;
+            if (i < c1) {
+                if (nx <= i) {
+                    do {
+                        TCB_DASSERT(k + 1 < nseg);
+                        ++k;
+                        nx = sg.start[k + 1];
+                    } while (nx <= i);
+                    base = sg.base[k];
+                }
+                w[q] = L[base + uint32_t(i)];
+            }
+        }
+        probe_all<PART_U, true>(h, w, hits);
+    }
+}
+
+// One chunk [c0, c1) of one class.
 template <typename Probe>
 __device__ __forceinline__ uint32_t chunk_hits(const int32_t* __restrict__ L, const SegTab& sg,
                                                int nseg, int c0, int c1, const Probe& h) {
-    constexpr int J = CHUNK / 32;
-    const int lane = int(lane_id());
     const int k0 = find_segment(sg.start, nseg, c0);
-    const int e1 = sg.start[k0 + 1];
-    if (lane == 0) {
+    if (lane_id() == 0) {
         TCB_STAT(4, 1);
-        TCB_STAT(5, e1 >= c1 ? 1 : 0);
+        TCB_STAT(5, sg.start[k0 + 1] >= c1 ? 1 : 0);
     }
-    TCB_DASSERT(k0 >= 0 && k0 < nseg && sg.start[k0] <= c0 && c0 < e1);
+    TCB_DASSERT(k0 >= 0 && k0 < nseg && sg.start[k0] <= c0 && c0 < sg.start[k0 + 1]);
     uint32_t hits = 0;
-    if (e1 >= c1) {
-        // fast path: one slice
-        const uint32_t base = sg.base[k0] + uint32_t(c0 + lane);
-        const int32_t* p = L + base;
-        int w[J];
-        if (c1 - c0 == CHUNK) {
-#ifdef TCB_NOLOAD
-#pragma unroll
-            for (int j = 0; j < J; ++j) w[j] = int(((base + 32u * j) * 2654435761u) >> 8);
-#else
-#pragma unroll
-            for (int j = 0; j < J; ++j) w[j] = p[32 * j];
-#endif
-            probe_all<J, false>(h, w, hits);
-        } else {
-#pragma unroll
-            for (int j = 0; j < J; ++j) w[j] = c0 + lane + 32 * j < c1 ? p[32 * j] : PAD;
-            probe_all<J, true>(h, w, hits);
-        }
-    } else if (c1 - c0 == CHUNK) {
-        cross_chunk<true>(L, sg, nseg, k0, c0, c1, h, hits);
-    } else {
-        cross_chunk<false>(L, sg, nseg, k0, c0, c1, h, hits);
-    }
+    if (c1 - c0 == CHUNK) full_chunk(L, sg, nseg, k0, c0, h, hits);
+    else compact_chunk(L, sg, nseg, k0, c0, c1, h, hits);
     return hits;
 }
 
 // Warps consume the flattened stream in CHUNK grabs: [0, tsup) are the OFF
 // slices, [roundup(tsup, CHUNK), total) the UP slices, so a grab (a CHUNK
-// multiple) never mixes the classes.
-template <typename Probe>
+// multiple) never mixes the classes.  fb: the pass's OFF ids sit in the
+// bucket table hb (the cuckoo build failed), probed on the compact path.
 __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, const SegTab& sg,
                                               int nseg, int total, int tsup, int* s_next,
-                                              const Probe& h, const BitmapSet& bm, Tally& tl) {
+                                              const CuckooHash& h, const BucketHash& hb, bool fb,
+                                              const BitmapSet& bm, Tally& tl) {
     TCB_DASSERT(nseg <= NSEG && total >= 0);
     const int lane = int(lane_id());
     while (true) {
@@ -1321,8 +1337,16 @@ __device__ __forceinline__ void stream_chunks(const int32_t* __restrict__ L, con
         if (lane == 0) c0 = atomicAdd(s_next, CHUNK);
         c0 = __shfl_sync(0xffffffffu, c0, 0);
         if (c0 >= total) break;
-        if (c0 >= tsup) tl.sup += chunk_hits(L, sg, nseg, c0, min(total, c0 + CHUNK), bm);
-        else tl.c1 += chunk_hits(L, sg, nseg, c0, min(tsup, c0 + CHUNK), h);
+        if (c0 >= tsup) {
+            tl.sup += chunk_hits(L, sg, nseg, c0, min(total, c0 + CHUNK), bm);
+        } else if (!fb) {
+            tl.c1 += chunk_hits(L, sg, nseg, c0, min(tsup, c0 + CHUNK), h);
+        } else {
+            uint32_t hits = 0;
+            compact_chunk(L, sg, nseg, find_segment(sg.start, nseg, c0), c0,
+                          min(tsup, c0 + CHUNK), hb, hits);
+            tl.c1 += hits;
+        }
     }
 }
 
@@ -1361,9 +1385,14 @@ __device__ __forceinline__ void block_scan_pair(int64_t a, int b, int64_t& ea, i
 }
 
 // Cuckoo slots for len staged ids: a power of two with load <= 3/8
-// (len <= HC -> <= C_SLOTS).
+// (len <= HC -> <= C_SLOTS), at least CUCKOO_MIN (kick chains cycle far more
+// often in a table of a few dozen slots).
+#ifndef TCB_CUCKOO_MIN
+#define TCB_CUCKOO_MIN 256
+#endif
+constexpr int CUCKOO_MIN = TCB_CUCKOO_MIN;
 __device__ __forceinline__ int cuckoo_slots(int len) {
-    return len == 0 ? 0 : max(64, 1 << ceil_log2_dev((len * 8 + 2) / 3));
+    return len == 0 ? 0 : max(CUCKOO_MIN, 1 << ceil_log2_dev((len * 8 + 2) / 3));
 }
 static_assert((HC * 8 + 2) / 3 <= C_SLOTS, "HC ids fit the table at load 3/8");
 
@@ -1536,9 +1565,9 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
             }
             __syncthreads();
             CuckooHash ch;
-            ch.setup(tab, max(cs, 64));
+            ch.setup(tab, max(cs, CUCKOO_MIN));
             BucketHash h;
-            h.setup(tab, max(cs, 64));
+            h.setup(tab, max(cs, CUCKOO_MIN));
             const BitmapSet bm{tab + cs, UP_TAG | wb};
             // INSERT_U staged values are loaded before their inserts (one
             // exposed load latency per batch instead of one per value)
@@ -1660,6 +1689,20 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 }
             }
             __syncthreads();
+#ifdef TCB_ONESLICE  // measurement-only: the same element count as ONE slice, all OFF class
+            const uint32_t b0_ = sg.base[0];
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                sg.start[0] = 0;
+                sg.base[0] = b0_ / 2;
+                sg.start[1] = tsup + tup;
+            }
+            __syncthreads();
+            const int os_total = tsup + tup;
+#define nseg 1
+#define total os_total
+#define tsup os_total
+#endif
             if (s_fail) {  // rare: rebuild the OFF sub-chunk as a bucket table
                 for (int i = threadIdx.x; i < cs; i += C_THREADS) tab[i] = EMPTY;
                 __syncthreads();
@@ -1670,10 +1713,14 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 __syncthreads();
             }
             if (!(dbg & 1)) {
-                if (!s_fail) stream_chunks(L, sg, nseg, total, tsup, &s_next, ch, bm, tl);
-                else stream_chunks(L, sg, nseg, total, tsup, &s_next, h, bm, tl);
+                stream_chunks(L, sg, nseg, total, tsup, &s_next, ch, h, s_fail != 0, bm, tl);
             }
             __syncthreads();
+#ifdef TCB_ONESLICE
+#undef nseg
+#undef total
+#undef tsup
+#endif
             if (phase == 2) break;
             if (phase == 0) {
                 cb += olen;
