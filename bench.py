@@ -359,9 +359,9 @@ def main():
     # the level rule applied before the intersection (intersect.cu) an edge
     # (owner x, partner p) streams OFF(p) (p's neighbours on another level)
     # and p's same-level neighbours ranked above x (degree bucket desc, id
-    # asc): 4 B/id.  Plus the partner id and its list bounds per cover edge
-    # (36 B), and the owner's OFF(x) ∪ UP(x) staged once per item (<= 1024
-    # partners).
+    # asc): 4 B/id.  Plus the partner's record per cover edge (16 B: list
+    # starts, OFF size, exact UP cut, written by k_edge_prep), and the owner's
+    # OFF(x) ∪ UP(x) staged once per item (<= 1024 partners).
     cu, cv = full.cover_u.long(), full.cover_v.long()
     # owner order (intersect.cu): degree bucket floor(log2 d) desc, id asc
     bk = torch.floor(torch.log2(deg.clamp(min=1).double())).long()
@@ -400,7 +400,7 @@ def main():
         own_ids, per_owner = torch.unique(oc, return_counts=True)
         staged = int(((n_off + n_up)[own_ids] * ((per_owner + 1023) // 1024)).sum().item())
     W_min_cta = int(torch.minimum(du, dv)[cta].sum().item())
-    b_cta = 4 * stream_cta + 36 * S_cta + 4 * staged
+    b_cta = 4 * stream_cta + 16 * S_cta + 4 * staged
     del keys, pc, oc, above, row_end, n_off, n_up, rk, partner, owner, cta
     del du, dv, deg, full
 
@@ -541,7 +541,7 @@ def main():
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_kind": peak_kind, "algorithmic_bytes": b_cta,
                 "formula": ("4*sum_{S_cta} (|OFF(p)| + |same-level N(p) ranked above x|) "
-                            "+ 36*|S_cta| + 4*staged |OFF(x)|+|UP(x)| per item"),
+                            "+ 16*|S_cta| + 4*staged |OFF(x)|+|UP(x)| per item"),
                 "stream_ids": stream_cta, "W_min_cta": W_min_cta,
                 "t_ms": stages["isect_cta"],
                 "survey_8d_intersect_stage": {

@@ -8,6 +8,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include <cstdio>
 
 struct tcb_context : tcb::Context {};
 

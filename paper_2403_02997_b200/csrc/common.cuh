@@ -71,6 +71,7 @@ enum Slot : int {
     WS_CLASS,         // intersection: per-32-entry class bits + word prefixes
     WS_VBEG,          // intersection: per-vertex list starts int64[2(n+1)]
     WS_BFS_BITS,      // BFS: visited + two frontier bitmaps, 3 x ceil(n/32) words
+    WS_EDGE_REC,      // intersection: CTA-tier partner records uint4[m]
     WS_NSLOTS
 };
 
@@ -161,12 +162,14 @@ struct Context {
     }
 };
 
-#define TCB_LAUNCH(ctx, kernel, grid, block, smem, ...)                          \
+#define TCB_LAUNCH_ON(ctx, st, kernel, grid, block, smem, ...)                   \
     do {                                                                         \
-        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);         \
+        kernel<<<(grid), (block), (smem), (st)>>>(__VA_ARGS__);                  \
         (ctx)->launches++;                                                       \
         TCB_CUDA(cudaGetLastError());                                            \
     } while (0)
+#define TCB_LAUNCH(ctx, kernel, grid, block, smem, ...) \
+    TCB_LAUNCH_ON(ctx, (ctx)->stream, kernel, grid, block, smem, __VA_ARGS__)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -117,6 +117,7 @@ constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per l
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
+constexpr int ITEM_FIRST = 1 << 16;   // CTA item flag: first listed group of its partner block
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t UP_TAG = 0x80000000u;  // UP lists hold UP_TAG | rank (never EMPTY: rank < n < 2^31 - 1)
 constexpr int PAD = -1;                   // padding key of a partial chunk (== EMPTY: never a value)
@@ -125,6 +126,10 @@ constexpr int NBKT = 32;
 #define TCB_UPCUT_ROUNDS 2
 #endif
 constexpr int UPCUT_ROUNDS = TCB_UPCUT_ROUNDS;  // interpolation windows before the binary search
+#ifndef TCB_UPCUT_SKIP
+#define TCB_UPCUT_SKIP 64
+#endif
+constexpr int UPCUT_SKIP = TCB_UPCUT_SKIP;  // CTA tier: bucket runs up to this long are streamed whole
 // Per-vertex partner record for the CTA tier: one 32-byte sector with the
 // list starts, the OFF size and the UP prefix counts of the degree buckets
 // CTA-tier owners have (|UP(v)| <= sqrt(2m) < 2^16 since 2m < 2^32).
@@ -918,13 +923,15 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         int ng = 0;  // groups with something staged
         for (int g = 0; g < G; ++g) ng += staged_any(g);
         unsigned long long base = atomicAdd(nc, (unsigned long long)(my * ng));
+        int first = ITEM_FIRST;  // the partner blocks' records are built from the first group's items
         for (int g = 0; g < G; ++g) {
             if (!staged_any(g)) continue;
             for (int64_t i = 0; i < per; ++i) {
                 if (!mine(x, i)) continue;
                 const int64_t p0 = s + i * PC;
-                citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
+                citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g | first);
             }
+            first = 0;
         }
     }
 }
@@ -1150,11 +1157,90 @@ __global__ void __launch_bounds__(W_WARPS * 32, 4)
 }
 
 #ifdef TCB_STATS  // measurement-only: CTA-tier work counters, printed per call
-__device__ unsigned long long g_cta_stats[16];  // items, passes, slices, elements, chunks, fast
+__device__ unsigned long long g_cta_stats[32];  // items, passes, slices, elements, chunks, fast
 #define TCB_STAT(i, v) atomicAdd(&g_cta_stats[i], (unsigned long long)(v))
+// phase clocks of thread 0 (TCB_TICK(i): time since the last tick -> slot 16 + i)
+#define TCB_TICK(i)                                                   \
+    do {                                                              \
+        if (threadIdx.x == 0) {                                       \
+            const long long now_ = clock64();                         \
+            atomicAdd(&g_cta_stats[16 + (i)], (unsigned long long)(now_ - tick_)); \
+            tick_ = now_;                                             \
+        }                                                             \
+    } while (0)
+#define TCB_TICK0 long long tick_ = clock64()
 #else
 #define TCB_STAT(i, v) ((void)0)
+#define TCB_TICK(i) ((void)0)
+#define TCB_TICK0 ((void)0)
 #endif
+
+// ---------------------------------------------------------------------------
+// 5b. partner records of the CTA tier's cover edges.  For the edge at slot p
+//     of P (owner x, partner y): R[p] = (OFF(y) start, |OFF(y)|, UP(y) start,
+//     the exact cut = UP(y) values ranked above x).  Finding them is a chain
+//     of dependent reads per edge (P -> the partner's record -> the cut's
+//     search windows); here every edge of the tier is in flight at once, and
+//     a CTA of k_isect_cta, which runs its items one after the other, starts
+//     an item with one coalesced 16-byte read per partner instead.
+__device__ __forceinline__ uint4 partner_rec(const Lists& ls, int y, bool want_up, int kx, int xk,
+                                             uint32_t va0, uint32_t vz0) {
+    // the record's header and the words holding uc[kx], uc[kx + 1]: one sector
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(ls.prec + y);
+    const uint4 hd = *reinterpret_cast<const uint4*>(rw);  // ob, ub, noff, uc[0..1]
+    int ucut = 0;
+    if (want_up) {
+        int hi, lo;
+        const int ui = kx - PR_K0;
+        if (ui >= 0 && ui + 1 < PR_NK) {
+            hi = int((rw[3 + (ui >> 1)] >> ((ui & 1) * 16)) & 0xFFFFu);
+            lo = int((rw[3 + ((ui + 1) >> 1)] >> (((ui + 1) & 1) * 16)) & 0xFFFFu);
+        } else {
+            hi = lo = PR_FULL;
+        }
+        if (hi == PR_FULL || lo == PR_FULL) {  // outside the record
+            hi = ls.ucnt[int64_t(y) * NBKT + kx];
+            lo = kx + 1 < NBKT ? ls.ucnt[int64_t(y) * NBKT + kx + 1] : 0;
+        }
+        // A short run is streamed whole instead of searched: its values
+        // ranked below x (at most UPCUT_SKIP - 1, read in sequence) miss the
+        // bitmap by the probe's clamp, which costs less than the search's
+        // random sector per edge — the setup's random reads are what bounds it.
+        ucut = hi - lo <= UPCUT_SKIP ? hi : ls.up_cut(hd.y, lo, hi, xk, va0, vz0);
+    }
+    return make_uint4(hd.x, hd.z, hd.y, uint32_t(ucut));
+}
+
+#ifndef TCB_EDGE_PREP
+#define TCB_EDGE_PREP 1
+#endif
+constexpr int EP_U = 2;  // partners per lane per round (their chains overlap)
+__global__ void __launch_bounds__(256)
+    k_edge_prep(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
+                Lists ls, const int32_t* __restrict__ P, const int2* __restrict__ vinfo,
+                uint4* __restrict__ R) {
+    const int64_t nitems = int64_t(block_load(nitems_p));
+    const int lane = int(lane_id());
+    const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t it = gw; it < nitems; it += nwarps) {
+        const longlong4 item = items[it];
+        if (!(item.w & ITEM_FIRST)) continue;
+        const int x = int(item.x);
+        const bool ns = ls.ub(x + 1) > ls.ub(x);
+        const int kx = dbucket(vinfo[x].y);
+        const int xk = ns ? int(ls.rnk[x]) : int(UP_TAG);
+        const uint32_t va0 = ns ? ls.rank_lo(kx) : 0u, vz0 = ns ? ls.rank_hi(kx) : 0u;
+        for (int64_t p0 = item.y + lane; p0 < item.z; p0 += 32 * EP_U) {
+            int y[EP_U];
+#pragma unroll
+            for (int q = 0; q < EP_U; ++q) y[q] = p0 + 32 * q < item.z ? P[p0 + 32 * q] : -1;
+#pragma unroll
+            for (int q = 0; q < EP_U; ++q)
+                if (y[q] >= 0) R[p0 + 32 * q] = partner_rec(ls, y[q], ns, kx, xk, va0, vz0);
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // 6. CTA tier
@@ -1195,19 +1281,23 @@ static_assert(31 * 65 + 64 >= NSEG - 1, "find_segment covers NSEG slices");
 // (rank - window base) of bm.  Everything in UP(x), and everything a partner
 // streams against it (the exact cut), ranks above x, so the window [0,
 // rank(x)) holds them all: one LDS.32 per probe, exact, nothing to hash.
+// Streamed values at or below x's rank (the tail of a bucket run that was not
+// cut, partner_rec) are clamped to bit `lim` = rank(x) - window base, which
+// is inside the bitmap and never set (x is not its own neighbour).
 struct BitmapSet {
     uint32_t* bm;
     uint32_t wbase;  // UP_TAG | first rank of the window (a multiple of 32)
+    uint32_t lim;    // rank(x) - first rank of the window
     static constexpr bool kNegSafe = false;  // a padding key indexes outside the window
     __device__ __forceinline__ void set(int key) const {
         const uint32_t i = uint32_t(key) - wbase;
         atomicOr(&bm[i >> 5], 1u << (i & 31));
     }
     __device__ __forceinline__ uint32_t first(int key) const {
-        return bm[(uint32_t(key) - wbase) >> 5];
+        return bm[min(uint32_t(key) - wbase, lim) >> 5];
     }
     __device__ __forceinline__ uint32_t second(int key, uint32_t v) const {
-        return (v >> (uint32_t(key) & 31u)) & 1u;
+        return (v >> (min(uint32_t(key) - wbase, lim) & 31u)) & 1u;
     }
 };
 
@@ -1401,9 +1491,9 @@ static_assert((HC * 8 + 2) / 3 <= C_SLOTS, "HC ids fit the table at load 3/8");
 #endif
 __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     k_isect_cta(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
-                Lists ls, const int32_t* __restrict__ P, unsigned long long* fetch,
-                DevCounters* C, int hc, int bmw_cap, int dbg, const int2* __restrict__ vinfo,
-                int fwd) {
+                Lists ls, const int32_t* __restrict__ P, const uint4* __restrict__ R,
+                unsigned long long* fetch, DevCounters* C, int hc, int bmw_cap, int dbg,
+                const int2* __restrict__ vinfo, int fwd) {
     extern __shared__ uint4 smem4[];
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem4);           // C_SLOTS: cuckoo set | bitmap
     SegTab sg;                                                    // stream table
@@ -1425,14 +1515,16 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
     dbg |= 2;
 #endif
     Tally tl;
+    TCB_TICK0;
     while (true) {
         if (threadIdx.x == 0) s_item = atomicAdd(fetch, 1ull);
         __syncthreads();
         const unsigned long long it = s_item;
         if (it >= nitems) break;
+        TCB_TICK(0);  // item fetch
         const longlong4 item = items[it];
         const int x = int(item.x);
-        const int lg = int(item.w >> 8), g = int(item.w & 255);
+        const int lg = int(item.w >> 8) & 255, g = int(item.w & 255);
         const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;  // ranges [q0, q1)
         const int* sx = ls.split + int64_t(x) * (F + 1);
         // the owner's staged slices: OFF [xo0, xo1) of its id ranges, and
@@ -1446,51 +1538,47 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         // streams against it, is below it
         const uint32_t xk = ns ? ls.rnk[x] : UP_TAG;
         const uint32_t xr = xk & ~UP_TAG;
-        const uint32_t va0 = ns ? ls.rank_lo(kx) : 0u, vz0 = ns ? ls.rank_hi(kx) : 0u;
         const int np = int(item.z - item.y);
-        // partners t and t + C_THREADS of this thread: both ids are loaded
-        // before either partner's rows, so the two dependent chains overlap
+        // partners t and t + C_THREADS of this thread: their records (k_edge_prep)
+        // give the list starts, the OFF size and the exact UP cut; only a
+        // range-split owner reads the partner's split row as well
         static_assert(PC == 2 * C_THREADS, "two partners per thread");
         {
+            uint4 rec[2];
             int yy[2];
+#if TCB_EDGE_PREP
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int t = threadIdx.x + r * C_THREADS;
+                rec[r] = t < np ? R[item.y + t] : make_uint4(0u, 0u, 0u, 0u);
+                yy[r] = lg > 0 && t < np ? P[item.y + t] : -1;
+            }
+#else  // measured alternative: the records computed here, item by item
+            const uint32_t va0 = ns ? ls.rank_lo(kx) : 0u, vz0 = ns ? ls.rank_hi(kx) : 0u;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int t = threadIdx.x + r * C_THREADS;
                 yy[r] = t < np ? P[item.y + t] : -1;
             }
 #pragma unroll
+            for (int r = 0; r < 2; ++r)
+                if (yy[r] >= 0) rec[r] = partner_rec(ls, yy[r], ns != 0, kx, int(xk), va0, vz0);
+#endif
+#pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int t = threadIdx.x + r * C_THREADS;
-                if (yy[r] < 0) continue;
-                const int y = yy[r];
-                const int* sy = ls.split + int64_t(y) * (F + 1);
-                // the record's header and the words holding uc[kx], uc[kx + 1]: one sector
-                const uint32_t* rw = reinterpret_cast<const uint32_t*>(ls.prec + y);
-                const uint4 hd = *reinterpret_cast<const uint4*>(rw);  // ob, ub, noff, uc[0..1]
-                // range ends at 0 / F come from the record, not the split row
-                const int a = q0 > 0 ? sy[q0] : 0;
-                const int b = q1 == F ? int(hd.z) : sy[q1];
-                s_pos[t] = hd.x + uint32_t(a);
+                if (t >= np) continue;
+                int a = 0, b = int(rec[r].y);
+                if (lg > 0) {  // range ends at 0 / F come from the record, not the split row
+                    const int* sy = ls.split + int64_t(yy[r]) * (F + 1);
+                    if (q0 > 0) a = sy[q0];
+                    if (q1 < F) b = sy[q1];
+                }
+                s_pos[t] = rec[r].x + uint32_t(a);
                 s_len[t] = no ? b - a : 0;
                 // the prefix of UP(y) that can be in UP(x): ranked above x
-                s_pos[PC + t] = hd.y;
-                int ucut = 0;
-                if (ns) {
-                    int hi, lo;
-                    const int ui = kx - PR_K0;
-                    if (ui >= 0 && ui + 1 < PR_NK) {
-                        hi = int((rw[3 + (ui >> 1)] >> ((ui & 1) * 16)) & 0xFFFFu);
-                        lo = int((rw[3 + ((ui + 1) >> 1)] >> (((ui + 1) & 1) * 16)) & 0xFFFFu);
-                    } else {
-                        hi = lo = PR_FULL;
-                    }
-                    if (hi == PR_FULL || lo == PR_FULL) {  // outside the record
-                        hi = ls.ucnt[int64_t(y) * NBKT + kx];
-                        lo = kx + 1 < NBKT ? ls.ucnt[int64_t(y) * NBKT + kx + 1] : 0;
-                    }
-                    ucut = ls.up_cut(hd.y, lo, hi, int(xk), va0, vz0);
-                }
-                s_len[PC + t] = ucut;
+                s_pos[PC + t] = rec[r].z;
+                s_len[PC + t] = ns ? int(rec[r].w) : 0;
 #ifdef TCB_NOUPSTREAM  // measurement-only: drop the UP slices
                 s_len[PC + t] = 0;
 #endif
@@ -1499,6 +1587,7 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
 #endif
             }
         }
+        TCB_TICK(1);  // item header + this thread's partners (records, cuts)
         // Passes.  One (phase 2) when the cuckoo set of the OFF slice and the
         // bitmap of [0, rank(x)) fit the table area side by side — hubs have
         // small ranks, low-degree owners few OFF ids.  Otherwise the OFF
@@ -1506,7 +1595,8 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         // matched against every partner's next unread OFF part, id-sorted),
         // then UP(x) in rank windows of the whole area (phase 1: a window is
         // matched against every partner's next unread UP part, rank-sorted).
-        const int bw = ns ? int((((xr + 31u) >> 5) + 3u) & ~3u) : 0;  // bitmap words of [0, xr)
+        const uint32_t xr1 = xr + 1u;  // the bitmap spans [0, xr]: bit xr is the clamp's target
+        const int bw = ns ? int((((xr1 + 31u) >> 5) + 3u) & ~3u) : 0;  // its words
         const int cs1 = cuckoo_slots(min(no, HC));
         const bool single = no <= hc && (ns == 0 || (bw <= bmw_cap && cs1 + bw <= C_SLOTS));
         int phase = single ? 2 : 0;
@@ -1515,13 +1605,13 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         int ud = 0;        // phase 1: staged UP values done
         while (true) {
             if (phase == 0 && cb >= no) phase = 1;
-            if (phase == 1 && (ns == 0 || wb >= xr)) break;
+            if (phase == 1 && (ns == 0 || wb >= xr1)) break;
             // this pass: OFF ids L[ob0, ob0 + olen) in a cuckoo set of cs
             // slots, UP values L[ub0, ub0 + ulen) in a bitmap of bwn words
             // over the ranks [wb, wend)
             int64_t ob0 = xo0, ub0 = xs0;
             int olen = 0, ulen = 0, cs = 0, bwn = 0;
-            uint32_t wend = xr;
+            uint32_t wend = xr1;
             bool last = true;
             if (phase == 2) {
                 olen = no;
@@ -1534,9 +1624,9 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 cs = cuckoo_slots(olen);
                 last = cb + olen >= no;
             } else {
-                wend = min(xr, wb + 32u * uint32_t(bmw_cap));
+                wend = min(xr1, wb + 32u * uint32_t(bmw_cap));
                 bwn = int((((wend - wb + 31u) >> 5) + 3u) & ~3u);
-                last = wend >= xr;
+                last = wend >= xr1;
                 ub0 = xs0 + ud;
                 if (last) {
                     ulen = ns - ud;
@@ -1564,11 +1654,12 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 s_fail = 0;
             }
             __syncthreads();
+            TCB_TICK(2);  // all threads' partners done (barrier) + table fill
             CuckooHash ch;
             ch.setup(tab, max(cs, CUCKOO_MIN));
             BucketHash h;
             h.setup(tab, max(cs, CUCKOO_MIN));
-            const BitmapSet bm{tab + cs, UP_TAG | wb};
+            const BitmapSet bm{tab + cs, UP_TAG | wb, xr - wb};
             // INSERT_U staged values are loaded before their inserts (one
             // exposed load latency per batch instead of one per value)
             if (!(dbg & 2)) {
@@ -1602,6 +1693,7 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 }
             }
             if ((dbg & TCB_TEST_FORCE_FALLBACK) && threadIdx.x == 0) s_fail = 1;
+            TCB_TICK(3);  // thread 0's staging
             // this pass's count from each slice of partners 2t, 2t+1
             // (slots 0, 1: OFF; 2, 3: UP), then the stream table
             const int vhi = phase == 0 && !last ? L[ob0 + olen - 1] : 0;
@@ -1712,10 +1804,13 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 }
                 __syncthreads();
             }
+            TCB_TICK(4);  // counts, block scan, stream table (barriers: everyone's staging)
             if (!(dbg & 1)) {
                 stream_chunks(L, sg, nseg, total, tsup, &s_next, ch, h, s_fail != 0, bm, tl);
             }
+            TCB_TICK(5);  // thread 0's warp streaming
             __syncthreads();
+            TCB_TICK(6);  // waiting for the other warps' last chunks
 #ifdef TCB_ONESLICE
 #undef nseg
 #undef total
@@ -1869,25 +1964,39 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
         ctx->isect_cta_blocks = b * ctx->num_sms;
         ctx->isect_warp_blocks = a * ctx->num_sms;
     }
+#if TCB_EDGE_PREP
+    uint4* R = ctx->wsT<uint4>(WS_EDGE_REC, m);
+    TCB_LAUNCH(ctx, k_edge_prep, ctx->num_sms * 8, 256, 0, (const longlong4*)citems,
+               (const unsigned long long*)nc, ls, (const int32_t*)P, (const int2*)vinfo, R);
+#else
+    uint4* R = nullptr;
+#endif
     ctx->record(5);
     ctx->record(7);  // no separate hub kernel in this design: hub stage = 0
     TCB_LAUNCH(ctx, k_isect_cta, ctx->isect_cta_blocks, C_THREADS, csm, (const longlong4*)citems,
-               (const unsigned long long*)nc, ls, (const int32_t*)P, fc, C, hc, bmw_cap,
+               (const unsigned long long*)nc, ls, (const int32_t*)P, (const uint4*)R, fc, C, hc,
+               bmw_cap,
                debug_flags() | ctx->test_flags,
                (const int2*)vinfo, fwd);
     ctx->record(6);
 #ifdef TCB_STATS
     {
-        unsigned long long st[16];
+        unsigned long long st[32];
         TCB_CUDA(cudaStreamSynchronize(ctx->stream));
         TCB_CUDA(cudaMemcpyFromSymbol(st, g_cta_stats, sizeof(st)));
-        const unsigned long long z[16] = {};
+        const unsigned long long z[32] = {};
         TCB_CUDA(cudaMemcpyToSymbol(g_cta_stats, z, sizeof(z)));
         unsigned long long nci = 0;
         TCB_CUDA(cudaMemcpy(&nci, nc, sizeof(nci), cudaMemcpyDeviceToHost));
         fprintf(stderr, "CTA stats: items %llu passes %llu slices %llu (UP %llu) elements %llu (UP %llu) "
                 "chunks %llu fast %llu; OFF elements by lg: %llu %llu %llu %llu %llu %llu\n", nci, st[1],
                 st[2], st[6], st[3], st[7], st[4], st[5], st[8], st[9], st[10], st[11], st[12], st[13]);
+        fprintf(stderr, "CTA phase clocks per CTA (Mcycles, thread 0): fetch %.2f partners %.2f barrier+fill "
+                "%.2f staging %.2f scan+table %.2f stream %.2f tail-wait %.2f\n",
+                st[16] / 1e6 / ctx->isect_cta_blocks, st[17] / 1e6 / ctx->isect_cta_blocks,
+                st[18] / 1e6 / ctx->isect_cta_blocks, st[19] / 1e6 / ctx->isect_cta_blocks,
+                st[20] / 1e6 / ctx->isect_cta_blocks, st[21] / 1e6 / ctx->isect_cta_blocks,
+                st[22] / 1e6 / ctx->isect_cta_blocks);
     }
 #endif
     TCB_LAUNCH(ctx, k_isect_warp, ctx->isect_warp_blocks, W_WARPS * 32, wsm, (const longlong4*)witems,

@@ -1,0 +1,3 @@
+O=gpurun_out/s5p; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sweep.py -m "gpu and not slow" -x -q 2>&1 | tail -3
+for c in rmat24 rmat22 rmat16; do python tools/variants.py run $c 3 cur aux0 aux1 2>&1 | tee $O/ab_$c.txt; done
