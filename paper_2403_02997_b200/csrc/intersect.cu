@@ -1214,7 +1214,10 @@ __device__ __forceinline__ uint4 partner_rec(const Lists& ls, int y, bool want_u
 #ifndef TCB_EDGE_PREP
 #define TCB_EDGE_PREP 1
 #endif
-constexpr int EP_U = 2;  // partners per lane per round (their chains overlap)
+#ifndef TCB_EP_U
+#define TCB_EP_U 2
+#endif
+constexpr int EP_U = TCB_EP_U;  // partners per lane per round (their chains overlap)
 __global__ void __launch_bounds__(256)
     k_edge_prep(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
                 Lists ls, const int32_t* __restrict__ P, const int2* __restrict__ vinfo,
