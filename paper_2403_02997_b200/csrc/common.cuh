@@ -72,6 +72,7 @@ enum Slot : int {
     WS_VBEG,          // intersection: per-vertex list starts int64[2(n+1)]
     WS_BFS_BITS,      // BFS: visited + two frontier bitmaps, 3 x ceil(n/32) words
     WS_EDGE_REC,      // intersection: CTA-tier partner records uint4[m]
+    WS_COVER_X,       // intersection: owner of each cover-edge slot int32[m]
     WS_NSLOTS
 };
 

@@ -117,7 +117,6 @@ constexpr int CHUNK = TCB_CHUNK;      // stream elements per warp grab (32 per l
 constexpr int LOG_F = 5;
 constexpr int F = 1 << LOG_F;         // id ranges for split points
 constexpr int TINY = 16;              // thread tier: owner degree <= TINY
-constexpr int ITEM_FIRST = 1 << 16;   // CTA item flag: first listed group of its partner block
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t UP_TAG = 0x80000000u;  // UP lists hold UP_TAG | rank (never EMPTY: rank < n < 2^31 - 1)
 constexpr int PAD = -1;                   // padding key of a partial chunk (== EMPTY: never a value)
@@ -561,17 +560,21 @@ __global__ void k_list_bounds(const int64_t* __restrict__ row, int64_t n,
 
 // OFF entries go to their slot in L, kept entries (cover edges, owner
 // side) to theirs in P (word prefix + popc).
-__global__ void k_scatter_off(const int32_t* __restrict__ nb, int64_t nnz,
-                              const uint2* __restrict__ cls,
+__global__ void k_scatter_off(const int32_t* __restrict__ src, const int32_t* __restrict__ nb,
+                              int64_t nnz, const uint2* __restrict__ cls,
                               const unsigned long long* __restrict__ pre,
                               int32_t* __restrict__ L, const uint32_t* __restrict__ bits,
                               const unsigned long long* __restrict__ prek,
-                              int32_t* __restrict__ P) {
+                              int32_t* __restrict__ P, int32_t* __restrict__ PX) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += stride) {
         const uint32_t bit = 1u << (e & 31);
         if (cls[e >> 5].x & bit) L[rank_off(cls, pre, e)] = nb[e];
-        if (bits[e >> 5] & bit) P[rank_keep(bits, prek, e)] = nb[e];
+        if (bits[e >> 5] & bit) {  // a cover edge: partner and owner of its slot
+            const int64_t slot = rank_keep(bits, prek, e);
+            P[slot] = nb[e];
+            PX[slot] = src[e];
+        }
     }
 }
 
@@ -923,15 +926,13 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
         int ng = 0;  // groups with something staged
         for (int g = 0; g < G; ++g) ng += staged_any(g);
         unsigned long long base = atomicAdd(nc, (unsigned long long)(my * ng));
-        int first = ITEM_FIRST;  // the partner blocks' records are built from the first group's items
         for (int g = 0; g < G; ++g) {
             if (!staged_any(g)) continue;
             for (int64_t i = 0; i < per; ++i) {
                 if (!mine(x, i)) continue;
                 const int64_t p0 = s + i * PC;
-                citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g | first);
+                citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
             }
-            first = 0;
         }
     }
 }
@@ -1214,34 +1215,30 @@ __device__ __forceinline__ uint4 partner_rec(const Lists& ls, int y, bool want_u
 #ifndef TCB_EDGE_PREP
 #define TCB_EDGE_PREP 1
 #endif
-#ifndef TCB_EP_U
-#define TCB_EP_U 2
+#ifndef TCB_EP_MINB
+#define TCB_EP_MINB 8
 #endif
-constexpr int EP_U = TCB_EP_U;  // partners per lane per round (their chains overlap)
-__global__ void __launch_bounds__(256)
-    k_edge_prep(const longlong4* __restrict__ items, const unsigned long long* __restrict__ nitems_p,
-                Lists ls, const int32_t* __restrict__ P, const int2* __restrict__ vinfo,
-                uint4* __restrict__ R) {
-    const int64_t nitems = int64_t(block_load(nitems_p));
-    const int lane = int(lane_id());
-    const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t it = gw; it < nitems; it += nwarps) {
-        const longlong4 item = items[it];
-        if (!(item.w & ITEM_FIRST)) continue;
-        const int x = int(item.x);
+// A thread per cover-edge slot (PX[p] = the slot's owner), so every lane has
+// an edge and the whole tier's chains are in flight; the owner's parameters
+// are the same for a run of consecutive slots (L1 hits).  Slots of thread- and
+// warp-tier owners, and of other shards' partner blocks, are skipped.
+__global__ void __launch_bounds__(256, TCB_EP_MINB)
+    k_edge_prep(const unsigned long long* __restrict__ ncover_p, Lists ls,
+                const int32_t* __restrict__ P, const int32_t* __restrict__ PX,
+                const int2* __restrict__ vinfo, const int64_t* __restrict__ seg_beg,
+                uint4* __restrict__ R, int wt, int shard, int nshards) {
+    const int64_t nc = int64_t(block_load(ncover_p));
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nc; p += stride) {
+        const int x = PX[p];
+        const int d = vinfo[x].y;
+        if (d <= wt) continue;
+        if (nshards > 1 && int((x + (p - seg_beg[x]) / PC) % nshards) != shard) continue;
         const bool ns = ls.ub(x + 1) > ls.ub(x);
-        const int kx = dbucket(vinfo[x].y);
+        const int kx = dbucket(d);
         const int xk = ns ? int(ls.rnk[x]) : int(UP_TAG);
         const uint32_t va0 = ns ? ls.rank_lo(kx) : 0u, vz0 = ns ? ls.rank_hi(kx) : 0u;
-        for (int64_t p0 = item.y + lane; p0 < item.z; p0 += 32 * EP_U) {
-            int y[EP_U];
-#pragma unroll
-            for (int q = 0; q < EP_U; ++q) y[q] = p0 + 32 * q < item.z ? P[p0 + 32 * q] : -1;
-#pragma unroll
-            for (int q = 0; q < EP_U; ++q)
-                if (y[q] >= 0) R[p0 + 32 * q] = partner_rec(ls, y[q], ns, kx, xk, va0, vz0);
-        }
+        R[p] = partner_rec(ls, P[p], ns, kx, xk, va0, vz0);
     }
 }
 
@@ -1868,6 +1865,7 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     uint8_t* dbk = reinterpret_cast<uint8_t*>(mbuf + size_t(n) * 16);
     int* rb = reinterpret_cast<int*>(mbuf + (size_t(n) * 17 + 15) / 16 * 16);  // NBKT + 1
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
+    int32_t* PX = ctx->wsT<int32_t>(WS_COVER_X, m);  // the owner of each slot of P
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
     int* split = ctx->wsT<int>(WS_COVER_V, size_t(n) * (F + 1));
     int32_t* L = ctx->wsT<int32_t>(WS_LISTS, nnz + 8);  // + one up_cut window
@@ -1941,8 +1939,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_list_bounds, grid_for(ctx, n + 1, 256), 256, 0, row, n, ccls,
                (const unsigned long long*)pre, nwords, vb, bits, (const unsigned long long*)prek,
                seg, seg + n);
-    TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, nb, nnz, ccls,
-               (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P);
+    TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, src, nb, nnz, ccls,
+               (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P, PX);
     TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
                (const uint8_t*)dbk, (const uint32_t*)rnk, (const uint2*)vb, L, ucnt, prec);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, n, SPLIT_WARPS * 32), SPLIT_WARPS * 32, 0, n,
@@ -1969,8 +1967,9 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     }
 #if TCB_EDGE_PREP
     uint4* R = ctx->wsT<uint4>(WS_EDGE_REC, m);
-    TCB_LAUNCH(ctx, k_edge_prep, ctx->num_sms * 8, 256, 0, (const longlong4*)citems,
-               (const unsigned long long*)nc, ls, (const int32_t*)P, (const int2*)vinfo, R);
+    TCB_LAUNCH(ctx, k_edge_prep, ctx->num_sms * TCB_EP_MINB, 256, 0,
+               (const unsigned long long*)&C->ncover, ls, (const int32_t*)P, (const int32_t*)PX,
+               (const int2*)vinfo, (const int64_t*)seg, R, wt, shard, nshards);
 #else
     uint4* R = nullptr;
 #endif
