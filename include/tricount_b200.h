@@ -108,6 +108,11 @@ TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_s
  * general BFS; this flag (or any nonzero flag / tuning) forces the general
  * path on them. */
 #define TCB_TEST_GENERAL_PATH 8
+/* Test hook: fill the CTA tier's partner-record array with 0xFF before the
+ * record pass, so a sharded call cannot pass on records an earlier call of
+ * another shard left in the workspace (each rank must build every record its
+ * own items read). */
+#define TCB_TEST_POISON_RECORDS 16
 TCB_API int tcb_set_test_flags(tcb_context* ctx, int flags);
 
 /* ---- input synthesis (rmat.py:45-72) ---------------------------------- */

@@ -1967,6 +1967,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     }
 #if TCB_EDGE_PREP
     uint4* R = ctx->wsT<uint4>(WS_EDGE_REC, m);
+    if (ctx->test_flags & TCB_TEST_POISON_RECORDS)
+        TCB_CUDA(cudaMemsetAsync(R, 0xFF, size_t(m) * sizeof(uint4), ctx->stream));
     TCB_LAUNCH(ctx, k_edge_prep, ctx->num_sms * TCB_EP_MINB, 256, 0,
                (const unsigned long long*)&C->ncover, ls, (const int32_t*)P, (const int32_t*)PX,
                (const int2*)vinfo, (const int64_t*)seg, R, wt, shard, nshards);

@@ -133,6 +133,35 @@ def test_gpu_shards_sum_to_total(world):
             assert (h["c1"], h["c2"], h["triangles"]) == (p.c1, p.c2, -1 if world > 1 else h["triangles"])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 5])
+def test_gpu_shards_build_their_own_records(world):
+    """Every shard's CTA-tier items read partner records that the same call's
+    record pass wrote: the record array is poisoned before each call
+    (TCB_TEST_POISON_RECORDS), the tiers are shrunk so hub-and-spoke RMAT
+    graphs run the CTA tier with several partner blocks per owner, and the
+    shards' tallies must add up to the single-GPU ones."""
+    import numpy as np
+    import paper_2403_02997_b200 as tb
+    ctx = tb._lib.context()
+    for seed in (1, 2):
+        g = tb.normalize(tb.generate_rmat(tb.RmatParams(scale=13, edge_factor=24, seed=seed)))
+        dg = tb.device_graph(g)
+        whole = tb.cetc(dg)
+        try:
+            ctx.set_test_flags(16 | 8)  # poison the records; general path
+            for tuning in ((4, 16), (16, 4096), (0, 0)):
+                ctx.set_tuning(*tuning)
+                parts = [tb.ops.cetc_shard(dg, r, world) for r in range(world)]
+                assert sum(p.c1 for p in parts) == whole.c1, (seed, tuning)
+                assert sum(p.c2 for p in parts) == whole.c2, (seed, tuning)
+                one = tb.cetc(dg)
+                assert (one.triangles, one.c1, one.c2) == (whole.triangles, whole.c1, whole.c2)
+        finally:
+            ctx.set_tuning(0, 0)
+            ctx.set_test_flags(0)
+
+
 def _nccl_worker(rank, world, port, out):
     """One rank per GPU over NCCL: the product's distributed entries, each
     rank on its own GPU with its own replica of the graph."""
