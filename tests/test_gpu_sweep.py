@@ -236,3 +236,43 @@ def test_sweep_large():
         _check_default(n, row, nb, ref, f"large seed {s}")
         if s < 3:
             _check_tuned(n, pairs, ref, f"large seed {s}")
+
+
+def g_wide_layer(rng):
+    """A root joined to k = 600..1500 vertices that form a dense random graph
+    whose degrees exceed the warp tier's 256: the CTA tier runs with its
+    DEFAULT thresholds — UP(x) in the rank bitmap, long same-level lists with
+    many degree ties, short bucket runs streamed uncut — and a sparse second
+    layer gives every owner OFF ids as well."""
+    k = int(rng.integers(600, 1500))
+    p = float(rng.uniform(0.35, 0.8))
+    iu = np.stack(np.triu_indices(k, 1), 1)
+    layer = iu[rng.random(len(iu)) < p] + 1
+    root = np.stack([np.zeros(k, np.int64), np.arange(1, k + 1)], 1)
+    m2 = int(rng.integers(k, 40 * k))
+    second = np.stack([rng.integers(1, k + 1, m2), rng.integers(k + 1, 3 * k + 1, m2)], 1)
+    n = 3 * k + 1
+    pairs = np.concatenate([root, layer, second])
+    return n, (_permute(n, pairs, rng) if rng.random() < 0.7 else pairs)
+
+
+def test_sweep_cta_tier_default_thresholds():
+    """Graphs whose owners exceed degree 256, so the CTA tier (rank bitmap,
+    partner records, clamped probes) runs as shipped; also with the bitmap
+    window shrunk to 64 / 512 words (rank windows) and the bucket fallback."""
+    for s in range(4):
+        n, pairs, row, nb, ref = _case(g_wide_layer, 120_000 + s)
+        assert int(np.diff(row).max()) > 256
+        dg = tb.device_graph(tb.normalize(tb.EdgeList(n=n, edges=pairs)))
+        ctx = tb._lib.context()
+        try:
+            for flags in (GENERAL_PATH, GENERAL_PATH | 4):
+                ctx.set_test_flags(flags)
+                for t in ((0, 0), (256, 64), (256, 512), (64, 4096)):
+                    ctx.set_tuning(*t)
+                    r = tb.cetc(dg)
+                    assert (r.triangles, r.c1, r.c2) == (ref["T"], ref["c1"], ref["c2"]), (s, flags, t)
+        finally:
+            ctx.set_tuning(0, 0)
+            ctx.set_test_flags(0)
+
