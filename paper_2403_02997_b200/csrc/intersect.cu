@@ -1603,9 +1603,11 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
         int cb = 0;        // phase 0: staged OFF ids done
         uint32_t wb = 0;   // phase 1: the window's first rank
         int ud = 0;        // phase 1: staged UP values done
+        bool ran = false;  // a pass ran (block-uniform): it ended with a barrier
         while (true) {
             if (phase == 0 && cb >= no) phase = 1;
             if (phase == 1 && (ns == 0 || wb >= xr1)) break;
+            ran = true;
             // this pass: OFF ids L[ob0, ob0 + olen) in a cuckoo set of cs
             // slots, UP values L[ub0, ub0 + ulen) in a bitmap of bwn words
             // over the ranks [wb, wend)
@@ -1824,9 +1826,10 @@ __global__ void __launch_bounds__(C_THREADS, TCB_CTA_PER_SM)
                 ud += ulen;
             }
         }
-        // an item whose staged slices are empty runs no pass: without this
+        // an item whose staged slices are empty runs no pass: without a
         // barrier thread 0 could overwrite s_item before all threads read it
-        __syncthreads();
+        // (a pass ends with one)
+        if (!ran) __syncthreads();
     }
     tl.flush(C);
 }
