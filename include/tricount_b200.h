@@ -96,8 +96,10 @@ TCB_API int tcb_stage_times(tcb_context* ctx, float* ms_out, int n);
 TCB_API int tcb_level_records(tcb_context* ctx, int64_t* out, int cap);
 /* Intersection work-split knobs (0 = built-in default): owners with degree
  * <= warp_tier_max_degree (max 1024) use the per-warp tier; larger owners
- * are staged <= cta_stage_max ids (4..4096) per CTA pass.  Results do not
- * depend on them; tests shrink them to drive every code path. */
+ * stage <= cta_stage_max off-level ids (4..6144) per CTA pass, and the same
+ * number bounds the 32-bit words of one rank window of the same-level bitmap
+ * (a shrunk value forces several windows).  Results do not depend on them;
+ * tests shrink them to drive every code path. */
 TCB_API int tcb_set_tuning(tcb_context* ctx, int warp_tier_max_degree, int cta_stage_max);
 /* Test hook (no reference counterpart): TCB_TEST_FORCE_FALLBACK makes every
  * CTA-tier pass use the bucket-table fallback that otherwise runs only when
