@@ -28,12 +28,14 @@
 // _kernels.py:745-748) is 3 x this tally; the counters hold c2 in those
 // units.  Ranking by degree keeps the same-level stream short: p streams
 // only the part of UP(p) ranked above x — a prefix of the sorted list: the
-// buckets above x's (ucnt table) plus the ids below x in x's own bucket (one
-// binary search per edge, Lists::up_cut) — and hubs have few neighbours
-// above them.  (The bucket order streams within 1% of the ids the exact
-// degree order would, and its sorted lists come from a counting sort.)
-// Same-level neighbours ranked below the endpoint are never read, and a hit needs no level lookup: the
-// list it was streamed from says which tally it belongs to.
+// buckets above x's (ucnt table) plus the values below x in x's own bucket
+// (one search per edge, Lists::up_cut, done for all edges of the CTA tier at
+// once by k_edge_prep; a short bucket run is streamed whole) — and hubs have
+// few neighbours above them.  (The bucket order streams within 1% of the ids
+// the exact degree order would, and its sorted lists come from a counting
+// sort.)  Same-level neighbours ranked below the endpoint are never read,
+// and a hit needs no level lookup: the list it was streamed from says which
+// tally it belongs to.
 //
 // UP lists hold RANKS, not ids: rank(v) = v's position in the owner order over
 // all vertices (k_rank_*: one stable counting pass by degree bucket), stored
@@ -41,9 +43,10 @@
 // keep both classes in one set).  Counting needs equality only, the sorted
 // UP list is then simply ascending, and everything ranked above an owner x
 // lies in [0, rank(x)): for a CTA-tier owner (degree > 256) that is the few
-// hundred thousand hubs, so UP(x) is staged as a BITMAP over [0, rank(x)) —
+// hundred thousand hubs, so UP(x) is staged as a BITMAP over [0, rank(x)] —
 // one shared-memory read per streamed element, exact, no hashing and no kick
-// chains — while OFF(x) keeps the cuckoo set.
+// chains (values at or below rank(x), the tail of an uncut run, are clamped
+// to bit rank(x), which is never set) — while OFF(x) keeps the cuckoo set.
 //
 //  1. owner bits: a keep bit per CSR entry (x, y) with level[x]==level[y] &&
 //     owns(x, y), and the OFF/UP class bits.  A word-level prefix of the keep
@@ -61,8 +64,11 @@
 //     items (x, p0, p1), <= PW partners each; others -> CTA items
 //     (x, p0, p1, group), <= PC partners.  With nshards > 1 only this
 //     shard's partner blocks are listed (dist.py shard_of).
+//  4b. k_edge_prep: the 16-byte partner record of every cover edge of a
+//     CTA-tier owner (list starts, OFF size, UP cut), a thread per slot of P.
 //  5. k_isect_tiny / k_isect_warp: one thread / warp per item; the warp tier
-//     keeps a per-warp bucket hash of OFF(x) ∪ UP(x) (4-entry buckets).
+//     keeps a per-warp cuckoo set of OFF(x) ∪ UP(x) (bucket table if a kick
+//     chain fails).
 //  6. k_isect_cta: one CTA per item; the group's slice of OFF(x) staged in a
 //     two-table cuckoo set and, in group 0, UP(x) in a rank bitmap beside it;
 //     the partners' slices (two per partner) are flattened into one element
