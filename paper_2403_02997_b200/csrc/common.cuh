@@ -73,6 +73,7 @@ enum Slot : int {
     WS_BFS_BITS,      // BFS: visited + two frontier bitmaps, 3 x ceil(n/32) words
     WS_EDGE_REC,      // intersection: CTA-tier partner records uint4[m]
     WS_COVER_X,       // intersection: owner of each cover-edge slot int32[m]
+    WS_LONG_ROWS,     // intersection: rows above UP_LONG entries (built first)
     WS_NSLOTS
 };
 

@@ -451,11 +451,13 @@ __device__ __forceinline__ int64_t rank_keep(const uint32_t* __restrict__ bits,
 // Per vertex: (level, degree), the packed key and the degree bucket.
 __global__ void k_vinfo(const int64_t* __restrict__ row, const int32_t* __restrict__ level,
                         int64_t n, int2* __restrict__ vinfo, uint32_t* __restrict__ key32,
-                        uint8_t* __restrict__ dbk, unsigned long long* nopack) {
+                        uint8_t* __restrict__ dbk, unsigned long long* nopack,
+                        int* __restrict__ long_rows, unsigned long long* nlong, int up_long) {
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
         const int l = level[v], d = int(row[v + 1] - row[v]);
         vinfo[v] = make_int2(l, d);
+        if (d > up_long) long_rows[atomicAdd(nlong, 1ull)] = int(v);  // k_build_up phase A
         dbk[v] = uint8_t(dbucket(d));
         const bool fits = l >= 0 && l < (1 << (32 - KEY_DB)) && d < (1 << KEY_DB);
         key32[v] = fits ? (uint32_t(l) << KEY_DB) | uint32_t(d) : 0u;
@@ -596,6 +598,9 @@ constexpr int UP_WARPS = 8;
 #ifndef TCB_UPW
 #define TCB_UPW 4  // long-row UP words whose loads are in flight together
 #endif
+#ifndef TCB_UP_QUARTER
+#define TCB_UP_QUARTER 1  // rows of <= 8 entries: four at a time, a quarter warp each
+#endif
 #ifndef TCB_UP_MINB
 #define TCB_UP_MINB 8  // k_build_up is latency-bound: keep 64 warps per SM
 #endif
@@ -630,12 +635,18 @@ __device__ __forceinline__ int stable_slot(int* h, bool act, int b) {
     return base + __popc(peers & lanemask_lt());
 }
 constexpr int UP_SHORT = 256;
+#ifndef TCB_UP_LONG
+#define TCB_UP_LONG 8192
+#endif
+constexpr int UP_LONG = TCB_UP_LONG;  // rows above this are listed and built first (k_build_up phase A)
 static_assert(NBKT == 32, "one degree bucket per lane");
 __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
     k_build_up(const int64_t* __restrict__ row, const int32_t* __restrict__ nb, int64_t n,
                const uint2* __restrict__ cls, const uint8_t* __restrict__ dbk,
                const uint32_t* __restrict__ rnk, const uint2* __restrict__ vb,
-               int32_t* __restrict__ L, int* __restrict__ ucnt, PRec* __restrict__ prec) {
+               int32_t* __restrict__ L, int* __restrict__ ucnt, PRec* __restrict__ prec,
+               const int* __restrict__ long_rows, const unsigned long long* __restrict__ nlong_p,
+               unsigned long long* group_ctr) {
     __shared__ int s_h[UP_WARPS][NBKT];
     __shared__ int s_w[UP_WARPS][UP_SHORT];
     __shared__ uint8_t s_b[UP_WARPS][UP_SHORT];
@@ -644,42 +655,9 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
     int* h = s_h[warp];
     const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t vbase = gw * 32; vbase < n; vbase += nwarps * 32) {
-        // A lane per row first: bounds and records for 32 rows at once; rows
-        // without UP entries (isolated vertices included) end here, and the
-        // warp takes the others one by one.
-        const int64_t lv = vbase + lane;
-        int64_t lr0 = 0, lr1 = 0;
-        uint2 lb0 = make_uint2(0, 0), lb1 = lb0;
-        if (lv < n) {
-            lr0 = row[lv];
-            lr1 = row[lv + 1];
-            lb0 = vb[lv];
-            lb1 = vb[lv + 1];
-        }
-        const bool live = lv < n && lr1 > lr0;
-        if (live) {
-            PRec* pr = prec + lv;
-            pr->ob = lb0.x;
-            pr->ub = lb0.y;
-            pr->noff = lb1.x - lb0.x;
-            if (lb1.y == lb0.y) {  // no UP entries: zero prefix counts
-                int4* uc4 = reinterpret_cast<int4*>(ucnt + lv * NBKT);
-#pragma unroll
-                for (int q = 0; q < NBKT / 4; ++q) uc4[q] = make_int4(0, 0, 0, 0);
-#pragma unroll
-                for (int q = 0; q < PR_NK; ++q) pr->uc[q] = 0;
-            }
-        }
-        unsigned work = __ballot_sync(0xffffffffu, live && lb1.y != lb0.y);
-        while (work) {
-        const int src = __ffs(work) - 1;
-        work &= work - 1;
-        const int64_t v = vbase + src;
-        const int64_t r0 = __shfl_sync(0xffffffffu, lr0, src);
-        const int64_t r1 = __shfl_sync(0xffffffffu, lr1, src);
-        const uint32_t u0 = __shfl_sync(0xffffffffu, lb0.y, src);
-        const uint32_t nup = __shfl_sync(0xffffffffu, lb1.y, src) - u0;
+    // One row (UP entries u0 .. u0 + nup of L), by the whole warp.
+    auto do_row = [&](int64_t v, int64_t r0, int64_t r1, uint32_t u0, uint32_t nup) {
+        (void)nup;
         PRec* pr = prec + v;
         h[lane] = 0;
         __syncwarp();
@@ -720,7 +698,7 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
                 if (act) L[int64_t(u0) + pos] = s_w[warp][i];
             }
             __syncwarp();
-            continue;
+            return;
         }
         const int64_t j0 = r0 >> 5, j1 = (r1 - 1) >> 5;
         // Long rows: lanes read 32 class words at a time; every word with UP
@@ -789,6 +767,116 @@ __global__ void __launch_bounds__(UP_WARPS * 32, TCB_UP_MINB)
             if (up) L[int64_t(u0) + pos] = w;
         });
         __syncwarp();
+    };
+    // Phase A: the longest rows (> UP_LONG entries, listed by k_vinfo) first,
+    // a warp each from the start of the kernel: a hub row of 4e5 entries is
+    // ~2.5 ms of one warp, which would otherwise end the kernel that much
+    // after everything else wherever its turn came.  Phase B hands out the
+    // 32-row groups dynamically, so the warps that took a long row take fewer.
+    {
+        const int64_t nlong = int64_t(block_load(nlong_p));
+        for (int64_t i = gw; i < nlong; i += nwarps) {
+            const int64_t v = long_rows[i];
+            const uint2 b0 = vb[v], b1 = vb[v + 1];
+            if (b1.y != b0.y) do_row(v, row[v], row[v + 1], b0.y, b1.y - b0.y);
+        }
+    }
+    while (true) {
+        unsigned long long g_ = 0;
+        if (lane == 0) g_ = atomicAdd(group_ctr, 1ull);
+        const int64_t vbase = int64_t(__shfl_sync(0xffffffffu, g_, 0)) * 32;
+        if (vbase >= n) break;
+        // A lane per row first: bounds and records for 32 rows at once; rows
+        // without UP entries (isolated vertices included) end here, and the
+        // warp takes the others one by one.
+        const int64_t lv = vbase + lane;
+        int64_t lr0 = 0, lr1 = 0;
+        uint2 lb0 = make_uint2(0, 0), lb1 = lb0;
+        if (lv < n) {
+            lr0 = row[lv];
+            lr1 = row[lv + 1];
+            lb0 = vb[lv];
+            lb1 = vb[lv + 1];
+        }
+        const bool live = lv < n && lr1 > lr0;
+        if (live) {
+            PRec* pr = prec + lv;
+            pr->ob = lb0.x;
+            pr->ub = lb0.y;
+            pr->noff = lb1.x - lb0.x;
+            if (lb1.y == lb0.y) {  // no UP entries: zero prefix counts
+                int4* uc4 = reinterpret_cast<int4*>(ucnt + lv * NBKT);
+#pragma unroll
+                for (int q = 0; q < NBKT / 4; ++q) uc4[q] = make_int4(0, 0, 0, 0);
+#pragma unroll
+                for (int q = 0; q < PR_NK; ++q) pr->uc[q] = 0;
+            }
+        }
+        unsigned work =
+            __ballot_sync(0xffffffffu, live && lb1.y != lb0.y && lr1 - lr0 <= UP_LONG);
+#if TCB_UP_QUARTER
+        // Rows of <= 8 entries (two in five of the rows with UP entries at
+        // RMAT scale): four at a time, a quarter warp each, a lane per entry.
+        // A row's cost is its chain of dependent reads (class word, entry,
+        // bucket and rank gathers), not its length, so four chains in flight
+        // are four times the rows per warp.  The order inside the quarter is
+        // computed with eight shuffles (larger bucket first, then lane = row =
+        // id order) — no histogram, no shared memory.
+        {
+            unsigned sm = work & __ballot_sync(0xffffffffu, lr1 - lr0 <= 8);
+            work &= ~sm;
+            const int q = lane >> 3, ql = lane & 7;
+            while (sm) {  // warp-uniform
+                int pick = -1;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int s_ = sm ? __ffs(sm) - 1 : -1;
+                    if (sm) sm &= sm - 1;
+                    if (t == q) pick = s_;
+                }
+                const int sl = max(pick, 0);
+                const int64_t r0 = __shfl_sync(0xffffffffu, lr0, sl);
+                const int64_t r1 = __shfl_sync(0xffffffffu, lr1, sl);
+                const uint32_t u0 = __shfl_sync(0xffffffffu, lb0.y, sl);
+                const int64_t v = vbase + sl;
+                const int64_t e = r0 + ql;
+                const bool up = pick >= 0 && e < r1 && ((cls[e >> 5].y >> (e & 31)) & 1u);
+                int b = -1, rk = 0;
+                if (up) {
+                    const int w = nb[e];
+                    b = dbk[w];
+                    rk = int(rnk[w]);
+                }
+                int pos = 0;
+                int c[4] = {0, 0, 0, 0};  // entries in buckets >= 4 ql + t
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int bj = __shfl_sync(0xffffffffu, b, (lane & ~7) + j);
+                    pos += (bj > b) || (bj == b && j < ql);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) c[t] += bj >= 4 * ql + t;
+                }
+                if (up) L[int64_t(u0) + pos] = rk;
+                if (pick >= 0) {
+                    *reinterpret_cast<int4*>(ucnt + v * NBKT + 4 * ql) =
+                        make_int4(c[0], c[1], c[2], c[3]);
+                    PRec* pr = prec + v;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int k = 4 * ql + t - PR_K0;
+                        if (k >= 0 && k < PR_NK) pr->uc[k] = uint16_t(c[t]);
+                    }
+                }
+            }
+        }
+#endif
+        while (work) {
+            const int src = __ffs(work) - 1;
+            work &= work - 1;
+            const uint32_t u0 = __shfl_sync(0xffffffffu, lb0.y, src);
+            do_row(vbase + src, __shfl_sync(0xffffffffu, lr0, src),
+                   __shfl_sync(0xffffffffu, lr1, src), u0,
+                   __shfl_sync(0xffffffffu, lb1.y, src) - u0);
         }
     }
 }
@@ -871,73 +959,104 @@ __global__ void k_make_items(const int64_t* __restrict__ row, const int64_t* __r
     auto mine = [shard, nshards](int64_t x, int64_t i) {
         return nshards <= 1 || int((x + i) % nshards) == shard;
     };
-    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < n; x += stride) {
-        const int64_t d = row[x + 1] - row[x];
-        if (d == 0) continue;
-        const int64_t s = seg_beg[x], e = seg_end[x];
-        if (e <= s) continue;
-        // nothing staged (no OFF neighbours, no same-level neighbour ranked
-        // above x): no edge of x can have an apex
-        const int64_t nup = ls.ub(x + 1) - ls.ub(x);
-        const int64_t st = (ls.ob(x + 1) - ls.ob(x)) + nup;
-        if (st == 0) continue;
-        if (d <= tiny) {  // <= TINY partners, each with <= TINY ids
-            if (!mine(x, 0)) continue;
-            const unsigned long long slot = atomicAdd(nt, 1ull);
-            titems[slot] = make_longlong4(x, s, e, 0);
-            continue;
-        }
-        if (d <= wt) {
-            const int64_t cnt = (e - s + PW - 1) / PW;
-            int64_t my = 0;
-            for (int64_t i = 0; i < cnt; ++i) my += mine(x, i);
-            if (my == 0) continue;
-            unsigned long long base = atomicAdd(nw, (unsigned long long)my);
-            for (int64_t i = 0; i < cnt; ++i) {
-                if (!mine(x, i)) continue;
-                const int64_t p0 = s + i * PW;
-                witems[base++] = make_longlong4(x, p0, min(p0 + PW, e), 0);
-            }
-            continue;
-        }
-        // fewest range groups G (power of two <= F) whose OFF slices all fit
-        // HC; group 0 also stages UP(x) (not range-split: it is rank-sorted)
-#ifdef TCB_ONLY_SMALL  // measurement-only: CTA items of small owners only
-        if (st > TCB_ONLY_SMALL) continue;
-#endif
-#ifdef TCB_ONLY_BIG  // measurement-only: CTA items of big owners only
-        if (st <= TCB_ONLY_BIG) continue;
-#endif
-        // (UP(x) is staged beside them as a rank bitmap, or after them in
-        // rank windows: it takes no table slots)
-        const int* sx = ls.split + x * (F + 1);
+    // A lane per vertex; the item slots of a warp's 32 vertices are taken
+    // with ONE atomic per list (warp scan of the counts): millions of owners
+    // adding to the same three counters were what this kernel waited for.
+    const int lane = int(lane_id());
+    for (int64_t xb = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; xb < n; xb += stride) {
+        const int64_t x = xb + lane;
+        int kind = 0;  // 1 thread item, 2 warp items, 3 CTA items
+        int cnt = 0;   // items of this vertex
+        int64_t s = 0, e = 0, nup = 0;
         int lg = 0;
-        if (st - nup > hc) {
-            for (lg = 1; lg < LOG_F; ++lg) {
-                const int step = F >> lg;
-                int mx = 0;
-                for (int q = 0; q < F; q += step) mx = max(mx, sx[q + step] - sx[q]);
-                if (mx <= hc) break;
-            }
-        }
-        const int G = 1 << lg;
-        const int64_t per = (e - s + PC - 1) / PC;
-        int64_t my = 0;
-        for (int64_t i = 0; i < per; ++i) my += mine(x, i);
-        if (my == 0) continue;
+        const int* sx = nullptr;
         auto staged_any = [&](int g) {
             const int q0 = (g << LOG_F) >> lg, q1 = ((g + 1) << LOG_F) >> lg;
             return sx[q1] - sx[q0] > 0 || (g == 0 && nup > 0);
         };
-        int ng = 0;  // groups with something staged
-        for (int g = 0; g < G; ++g) ng += staged_any(g);
-        unsigned long long base = atomicAdd(nc, (unsigned long long)(my * ng));
-        for (int g = 0; g < G; ++g) {
-            if (!staged_any(g)) continue;
-            for (int64_t i = 0; i < per; ++i) {
+        if (x < n) do {
+            const int64_t d = row[x + 1] - row[x];
+            if (d == 0) break;
+            s = seg_beg[x];
+            e = seg_end[x];
+            if (e <= s) break;
+            // nothing staged (no OFF neighbours, no same-level neighbour ranked
+            // above x): no edge of x can have an apex
+            nup = ls.ub(x + 1) - ls.ub(x);
+            const int64_t st = (ls.ob(x + 1) - ls.ob(x)) + nup;
+            if (st == 0) break;
+            if (d <= tiny) {  // <= TINY partners, each with <= TINY ids
+                if (mine(x, 0)) {
+                    kind = 1;
+                    cnt = 1;
+                }
+                break;
+            }
+            if (d <= wt) {
+                const int64_t nb_ = (e - s + PW - 1) / PW;
+                for (int64_t i = 0; i < nb_; ++i) cnt += mine(x, i);
+                kind = cnt ? 2 : 0;
+                break;
+            }
+#ifdef TCB_ONLY_SMALL  // measurement-only: CTA items of small owners only
+            if (st > TCB_ONLY_SMALL) break;
+#endif
+#ifdef TCB_ONLY_BIG  // measurement-only: CTA items of big owners only
+            if (st <= TCB_ONLY_BIG) break;
+#endif
+            // fewest range groups G (power of two <= F) whose OFF slices all
+            // fit HC; group 0 also stages UP(x) (not range-split: it is
+            // rank-sorted, and it takes no table slots: a rank bitmap beside
+            // the OFF set, or rank windows after it)
+            sx = ls.split + x * (F + 1);
+            if (st - nup > hc) {
+                for (lg = 1; lg < LOG_F; ++lg) {
+                    const int step = F >> lg;
+                    int mx = 0;
+                    for (int q = 0; q < F; q += step) mx = max(mx, sx[q + step] - sx[q]);
+                    if (mx <= hc) break;
+                }
+            }
+            const int64_t per = (e - s + PC - 1) / PC;
+            int my = 0;
+            for (int64_t i = 0; i < per; ++i) my += mine(x, i);
+            int ng = 0;  // groups with something staged
+            for (int g = 0; g < (1 << lg); ++g) ng += staged_any(g);
+            cnt = my * ng;
+            kind = cnt ? 3 : 0;
+        } while (false);
+        // slots: one atomic per warp and list
+        unsigned long long base = 0;
+#pragma unroll
+        for (int k = 1; k <= 3; ++k) {
+            const int c = kind == k ? cnt : 0;
+            const int incl = warp_inclusive_scan(c);
+            const int tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (tot == 0) continue;  // warp-uniform
+            unsigned long long b0 = 0;
+            if (lane == 31)
+                b0 = atomicAdd(k == 1 ? nt : k == 2 ? nw : nc, (unsigned long long)tot);
+            b0 = __shfl_sync(0xffffffffu, b0, 31);
+            if (kind == k) base = b0 + (unsigned long long)(incl - c);
+        }
+        if (kind == 1) {
+            titems[base] = make_longlong4(x, s, e, 0);
+        } else if (kind == 2) {
+            const int64_t nb_ = (e - s + PW - 1) / PW;
+            for (int64_t i = 0; i < nb_; ++i) {
                 if (!mine(x, i)) continue;
-                const int64_t p0 = s + i * PC;
-                citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
+                const int64_t p0 = s + i * PW;
+                witems[base++] = make_longlong4(x, p0, min(p0 + PW, e), 0);
+            }
+        } else if (kind == 3) {
+            const int64_t per = (e - s + PC - 1) / PC;
+            for (int g = 0; g < (1 << lg); ++g) {
+                if (!staged_any(g)) continue;
+                for (int64_t i = 0; i < per; ++i) {
+                    if (!mine(x, i)) continue;
+                    const int64_t p0 = s + i * PC;
+                    citems[base++] = make_longlong4(x, p0, min(p0 + PC, e), (lg << 8) | g);
+                }
             }
         }
     }
@@ -1883,6 +2002,10 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     uint32_t* rnk = reinterpret_cast<uint32_t*>(mbuf + size_t(n) * 12);
     uint8_t* dbk = reinterpret_cast<uint8_t*>(mbuf + size_t(n) * 16);
     int* rb = reinterpret_cast<int*>(mbuf + (size_t(n) * 17 + 15) / 16 * 16);  // NBKT + 1
+    // rows above UP_LONG entries (at most 2m / UP_LONG of them), built first
+    int* long_rows = ctx->wsT<int>(WS_LONG_ROWS, size_t(nnz / UP_LONG) + 64);
+    unsigned long long* nlong = &C->scratch[10];
+    unsigned long long* up_groups = &C->scratch[14];
     int32_t* P = ctx->wsT<int32_t>(WS_COVER_U, m);
     int32_t* PX = ctx->wsT<int32_t>(WS_COVER_X, m);  // the owner of each slot of P
     int64_t* seg = ctx->wsT<int64_t>(WS_COUNT_TMP, 2 * n);
@@ -1925,8 +2048,10 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
 
     unsigned long long* nopack = &C->scratch[13];
     TCB_CUDA(cudaMemsetAsync(nopack, 0, sizeof(unsigned long long), ctx->stream));
+    TCB_CUDA(cudaMemsetAsync(nlong, 0, sizeof(unsigned long long), ctx->stream));
+    TCB_CUDA(cudaMemsetAsync(up_groups, 0, sizeof(unsigned long long), ctx->stream));
     TCB_LAUNCH(ctx, k_vinfo, grid_for(ctx, n, 256), 256, 0, row, level, n, vinfo, key32, dbk,
-               nopack);
+               nopack, long_rows, nlong, UP_LONG);
     if (!fwd && !xonly) {  // ranks in the owner order: the values of the UP lists
         const int64_t ntiles = ceil_div(n, RK_TILE);
         int64_t* hist = ctx->wsT<int64_t>(WS_SORT_HIST, size_t(NBKT) * ntiles);
@@ -1961,7 +2086,8 @@ void cetc_intersect_owner(Context* ctx, const int64_t* row, const int32_t* nb, c
     TCB_LAUNCH(ctx, k_scatter_off, grid_for(ctx, nnz, 256), 256, 0, src, nb, nnz, ccls,
                (const unsigned long long*)pre, L, bits, (const unsigned long long*)prek, P, PX);
     TCB_LAUNCH(ctx, k_build_up, ctx->num_sms * 8, UP_WARPS * 32, 0, row, nb, n, ccls,
-               (const uint8_t*)dbk, (const uint32_t*)rnk, (const uint2*)vb, L, ucnt, prec);
+               (const uint8_t*)dbk, (const uint32_t*)rnk, (const uint2*)vb, L, ucnt, prec,
+               (const int*)long_rows, (const unsigned long long*)nlong, up_groups);
     TCB_LAUNCH(ctx, k_split_points, grid_for(ctx, n, SPLIT_WARPS * 32), SPLIT_WARPS * 32, 0, n,
                (const int32_t*)L,
                (const uint2*)vb, rshift, split);
