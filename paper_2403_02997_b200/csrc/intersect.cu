@@ -1123,7 +1123,10 @@ __global__ void __launch_bounds__(256)
 //    (OFF slices first) and streamed in rounds of 32 x JW elements, each lane
 //    walking the slice boundaries like the CTA tier's cross_chunk.
 
-constexpr int JW = 8;           // elements per lane per warp-tier round
+#ifndef TCB_JW
+#define TCB_JW 16  // 4 / 8 / 16 / 24 / 32: 4.81 / 4.48 / 4.36 / 4.50 / 5.10 ms at RMAT-24
+#endif
+constexpr int JW = TCB_JW;      // elements per lane per warp-tier round
 constexpr int W_SEG = 2 * PW;   // slices per warp item
 
 template <typename Probe>
